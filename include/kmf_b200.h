@@ -1,0 +1,220 @@
+/*
+ * kmf_b200.h -- C ABI of the B200-native q-LSKUM hot path (libkmf_b200.so).
+ *
+ * The reference (arXiv 2108.07031 desk re-implementation, package `kmf`,
+ * /root/reference/pkg/src/kmf) is pure Python/numpy and has no FFI; its
+ * "operator API" is the Python surface of solver.py / lsq.py / state.py /
+ * kinetics.py.  Each entry point below replaces one reference function and
+ * cites it.  The Python mirror (paper_2108_07031_b200/) binds these through
+ * ctypes with exactly the reference's names and argument meaning.
+ *
+ * Conventions
+ *   - plain pointers and sizes, no torch types; host buffers are caller
+ *     owned and every call is synchronous on return;
+ *   - four-vector fields use the reference layout (4, n) row-major
+ *     (component c of point i at [c*n + i]), scalars (n,);
+ *   - status codes: KMF_OK, KMF_EPOSITIVITY (reference PositivityError),
+ *     KMF_EINVAL (reference ValueError), KMF_ECUDA, KMF_ENCCL;
+ *   - a context is bound to one CUDA device and is not thread-safe; use one
+ *     context per process/GPU.
+ */
+#ifndef KMF_B200_H
+#define KMF_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KMF_ABI_VERSION 1
+
+enum {
+    KMF_OK = 0,
+    KMF_EPOSITIVITY = 1,
+    KMF_EINVAL = 2,
+    KMF_ECUDA = 3,
+    KMF_ENCCL = 4
+};
+
+/* Which reference raise site a positivity failure corresponds to. */
+enum {
+    KMF_CTX_NONE = 0,
+    KMF_CTX_INITIAL = 1,       /* state.py:80-88 validate("initial state")   */
+    KMF_CTX_FLUX_XP = 2,       /* solver.py:164-170 flux_residual[x+]        */
+    KMF_CTX_FLUX_XM = 3,       /*                   flux_residual[x-]        */
+    KMF_CTX_FLUX_YP = 4,       /*                   flux_residual[y+]        */
+    KMF_CTX_FLUX_YM = 5,       /*                   flux_residual[y-]        */
+    KMF_CTX_WALL_TANGENT = 6,  /* solver.py:260-265 "wall tangent"           */
+    KMF_CTX_WALL_NORMAL = 7,   /*                   "wall normal"            */
+    KMF_CTX_OUTER_TANGENT = 8, /*                   "outer tangent"          */
+    KMF_CTX_OUTER_NORMAL = 9,  /*                   "outer normal"           */
+    KMF_CTX_C2P_DENSITY = 10,  /* state.py:110-117 conserved_to_primitives   */
+    KMF_CTX_C2P_PRESSURE = 11, /* state.py:121-128                           */
+    KMF_CTX_Q2P = 12,          /* state.py:151-157 q_to_primitives (NaN q4)  */
+    KMF_CTX_P2Q = 13           /* state.py:80-88 validate("primitives_to_q") */
+};
+
+/* One CSR stencil family with its cached LS sums -- geometry.py:222-266
+ * StencilSet.  ptr has n_owners+1 entries; idx/dx/dy n_edges. */
+typedef struct {
+    int64_t n_owners;
+    int64_t n_edges;
+    const int64_t *ptr;
+    const int64_t *idx;
+    const double *dx, *dy;
+    const double *sxx, *sxy, *syy, *det;
+} kmf_stencil;
+
+/* Rotated-frame stencils of one boundary class -- geometry.py:269-291
+ * FrameStencils (dx = dt, dy = dn in the local frame, owners numbered
+ * locally 0..b-1, points[] their global indices). */
+typedef struct {
+    int64_t b;
+    const int64_t *points;
+    const double *tx, *ty, *nx, *ny;
+    kmf_stencil tplus, tminus, normal;
+} kmf_frame;
+
+/* Connectivity -- geometry.py:294-312 (+ the cloud, geometry.py:56-112).
+ * The four split families (geometry.py:544-549) are order-preserving
+ * subsets of `full` selected by dx<=0, dx>=0, dy<=0, dy>=0; only their LS
+ * sums and det_safe (geometry.py:505-508) cross the ABI, membership is
+ * re-derived on the device from the sign of the full-stencil offsets.
+ * When full.dx/dy equal x[idx]-x[owner] bitwise (what build_stencils
+ * produces, geometry.py:377-384) the device recomputes them from x, y and
+ * never stores per-edge offsets. */
+typedef struct {
+    int64_t n;
+    const double *x, *y;
+    const int64_t *flag;        /* 0 interior, 1 wall, 2 outer */
+    const double *d_min;        /* geometry.py:537-539 */
+    kmf_stencil full;
+    const double *split_sxx[4]; /* x+, x-, y+, y- */
+    const double *split_sxy[4];
+    const double *split_syy[4];
+    const double *det_safe[4];
+    int has_wall, has_outer;
+    kmf_frame wall, outer;
+    /* optional point permutation (space-filling-curve order), NULL for
+     * identity: device slot k holds caller point perm[k].  Neighbour lists
+     * keep their reference order, so results are bitwise identical. */
+    const int64_t *perm;
+} kmf_geometry;
+
+/* solver.py:69-99 SolverConfig, as consumed by the hot loop */
+typedef struct {
+    double gamma;
+    double cfl;
+    double fs[4];            /* free_stream(mach, aoa, gamma) primitives, state.py:170-185 */
+    int n_inner;             /* Jacobi sweeps per stage (lsq.py:229) */
+    int mode;                /* 0 fused, 1 split4 (solver.py:51, :218-229) */
+    double convergence_tol;  /* <= 0: none (solver.py:557-559) */
+    int instrument;          /* per-stage device timing (solver.py:461-474) */
+    int timing_skip;         /* iterations excluded from timing (solver.py:516) */
+} kmf_params;
+
+/* Positivity / error report (PositivityError, state.py:28-38). */
+typedef struct {
+    int code;            /* KMF_* of the failing call */
+    int iteration;       /* 1-based outer iteration (solver.py:552) or 0 */
+    int stage;           /* RK stage 1..4, or 0 */
+    int context;         /* KMF_CTX_* */
+    int64_t count;       /* offending entries */
+    int64_t n_indices;   /* entries written to kmf_last_indices */
+    char message[256];
+} kmf_error_info;
+
+typedef struct kmf_ctx kmf_ctx;
+
+int kmf_abi_version(void);
+/* number of CUDA devices visible (0 without a GPU; no CUDA call fails) */
+int kmf_device_count(void);
+
+/* ---- context: Connectivity upload + the on-device outer loop ------------ */
+
+/* deep-copies the geometry to `device`; replaces the per-call packing the
+ * reference does implicitly inside solve (solver.py:500-506) */
+int kmf_create(kmf_ctx **out, const kmf_geometry *g, int device);
+void kmf_destroy(kmf_ctx *ctx);
+/* initial primitives (4,n); the next kmf_run seeds U, q and dt from them
+ * with its own gamma/cfl (solver.py:502-506, :520) */
+int kmf_set_state(kmf_ctx *ctx, const double *prims);
+/* solver.py:515-559: n_iter outer iterations of timestep + 4 SSP-RK stages
+ * + residue; history[0..*iters_done-1] = residue_norm per iteration. */
+int kmf_run(kmf_ctx *ctx, const kmf_params *p, int n_iter, double *history, int *iters_done,
+            int *converged);
+/* final primitives and conserved (each (4,n)), either may be NULL */
+int kmf_get_state(kmf_ctx *ctx, double *prims, double *U);
+/* device seconds per STAGE_NAMES key (solver.py:53-60) accumulated by the
+ * last instrumented kmf_run over its timed iterations */
+int kmf_stage_seconds(kmf_ctx *ctx, double out[6]);
+/* error details of the last failing call on this context (or global) */
+int kmf_last_error(kmf_ctx *ctx, kmf_error_info *info);
+int kmf_last_indices(kmf_ctx *ctx, int64_t *idx, int64_t cap);
+
+/* ---- positivity diagnostics (PositivityError details) ------------------- *
+ * After a KMF_EPOSITIVITY from kmf_run / kmf_op_flux_residual /
+ * kmf_op_boundary the device still holds the failing stage's q and
+ * gradients (every later kernel was skipped).  These calls recompute the
+ * reference's positivity predicates on that data so the host can rebuild
+ * the exact PositivityError (context, count, indices) of solver.py:164-170,
+ * :260-265 and state.py:110-128.  `which` selects the gradient buffer that
+ * holds the final sweep: 0 for the op API and even n_inner, 1 for odd. */
+/* per caller-CSR edge of the full stencil: bit0 q~4 >= 0 at either end,
+ * bit1 NaN at the neighbour end, bit2 NaN at the owner end */
+int kmf_diag_flux(kmf_ctx *ctx, int which, uint8_t *flags);
+/* per frame edge of family fam (0 tplus, 1 tminus, 2 normal) over the
+ * wall-then-outer boundary table: 1 where q~4 >= 0 at either end */
+int kmf_diag_frame(kmf_ctx *ctx, int which, int fam, uint8_t *flags);
+/* conserved state written by the failing stage's update, (4,n) */
+int kmf_diag_stage_state(kmf_ctx *ctx, int stage, double *U);
+
+/* ---- stage operators on a context (host in/out, synchronous) ------------ */
+
+/* solver.py:154-159 local_timestep */
+int kmf_op_timestep(kmf_ctx *ctx, const double *prims, double cfl, double gamma, double *dt);
+/* lsq.py:164-175 first_order_q_gradients */
+int kmf_op_first_order(kmf_ctx *ctx, const double *q, double *qx, double *qy);
+/* lsq.py:184-245 compute_q_derivatives; prev_qx/prev_qy may be NULL (cold
+ * start); inner_residuals has n_inner entries (may be NULL) */
+int kmf_op_q_derivatives(kmf_ctx *ctx, const double *q, int n_inner, const double *prev_qx,
+                         const double *prev_qy, double *qx, double *qy, double *inner_residuals);
+/* solver.py:198-235 flux_residual (boundary rows zero) */
+int kmf_op_flux_residual(kmf_ctx *ctx, const double *q, const double *qx, const double *qy,
+                         int mode, double gamma, double *R);
+/* solver.py:336-373 apply_boundary; R is updated in place */
+int kmf_op_boundary(kmf_ctx *ctx, const double *q, const double *qx, const double *qy,
+                    const double fs[4], double gamma, double *R);
+
+/* ---- context-free point operators --------------------------------------- */
+
+/* state.py:132-138 primitives_to_q; flags[i] != 0 marks validate failures */
+int kmf_op_primitives_to_q(int64_t n, const double *prims, double gamma, double *q, uint8_t *flags);
+/* state.py:141-163 q_to_primitives; flags[i] != 0 where !(q4 < 0) */
+int kmf_op_q_to_primitives(int64_t n, const double *q, double gamma, double *prims, uint8_t *flags);
+/* state.py:91-96 primitives_to_conserved */
+int kmf_op_primitives_to_conserved(int64_t n, const double *prims, double gamma, double *U,
+                                   uint8_t *flags);
+/* state.py:99-129 conserved_to_primitives; flags bit0 density, bit1 pressure */
+int kmf_op_conserved_to_primitives(int64_t n, const double *U, double gamma, double *prims,
+                                   uint8_t *flags);
+/* kinetics.py:71-106 split_flux; axis 0/1 = x/y, sign +1/-1 */
+int kmf_op_split_flux(int64_t n, const double *prims, int axis, int sign, double gamma, double *G);
+/* kinetics.py:59-68 full_flux */
+int kmf_op_full_flux(int64_t n, const double *prims, int axis, double gamma, double *F);
+/* solver.py:385-409 state_update_rk (positivity is checked by the caller
+ * through kmf_op_conserved_to_primitives, as the reference does) */
+int kmf_op_state_update(int64_t n, const double *U_outer, const double *U_stage, int stage,
+                        const double *dt, const double *R, double *U_new);
+/* solver.py:412-421 residue_norm, exactly summed (math.fsum semantics) */
+int kmf_op_residue(int64_t n, const double *U_new, const double *U_old, double *out);
+
+/* last global (context-free) error string */
+const char *kmf_strerror(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KMF_B200_H */

@@ -1,0 +1,1203 @@
+// kmf_b200.cu -- context, CUDA-graph outer loop and C ABI (include/kmf_b200.h).
+//
+// Build: paper_2108_07031_b200/csrc/Makefile (nvcc -gencode
+// arch=compute_100a,code=sm_100a -O3 -lineinfo -fmad=false).
+#include "../../include/kmf_b200.h"
+#include "kmf_kernels.cuh"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+using namespace kmf;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+void set_msg(const char *fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+}
+
+#define CK(expr)                                                                                  \
+    do {                                                                                          \
+        cudaError_t e_ = (expr);                                                                  \
+        if (e_ != cudaSuccess) {                                                                  \
+            set_msg("%s:%d %s: %s", __FILE__, __LINE__, #expr, cudaGetErrorString(e_));           \
+            return KMF_ECUDA;                                                                     \
+        }                                                                                         \
+    } while (0)
+
+inline int nblk(long long n, int tb = kTB) { return (int)((n + tb - 1) / tb); }
+
+template <typename T>
+struct DBuf {
+    T *p = nullptr;
+    size_t n = 0;
+    ~DBuf() { release(); }
+    void release()
+    {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    cudaError_t alloc(size_t count)
+    {
+        release();
+        n = count;
+        if (!count) return cudaSuccess;
+        return cudaMalloc((void **)&p, sizeof(T) * count);
+    }
+    cudaError_t upload(const T *h, size_t count)
+    {
+        cudaError_t e = alloc(count);
+        if (e != cudaSuccess || !count) return e;
+        return cudaMemcpy(p, h, sizeof(T) * count, cudaMemcpyHostToDevice);
+    }
+};
+
+struct GraphKey {
+    double gamma, cfl, fs[4], tol;
+    int n_inner, mode, unroll, cap, base;
+    const void *hist;
+    bool operator==(const GraphKey &o) const { return std::memcmp(this, &o, sizeof o) == 0; }
+};
+
+}  // namespace
+
+struct kmf_ctx {
+    int device = 0;
+    int n = 0, ld = 0;
+    bool xy = true;  // offsets recomputed from coordinates
+    bool has_perm = false;
+    cudaStream_t s0 = nullptr, s1 = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+
+    // geometry
+    DBuf<double> x, y, dmin, fsum, fcoef, edx, edy;
+    DBuf<unsigned char> flag;
+    DBuf<int> eoff, deg, eidx;
+    DBuf<long long> perm, cptr;
+    long long n_edges = 0;
+    // boundary
+    int nb = 0, nb_wall = 0;
+    DBuf<int> bpoint, bptr[3], bidx[3];
+    DBuf<unsigned char> btype;
+    DBuf<double> bframe, bcoef, bdt[3], bdn[3];
+    long long bedges[3] = {0, 0, 0};
+
+    // state
+    DBuf<double> Uo, Us, q, GA, GB, R, dt, stage_buf, stage_buf2;
+    DBuf<Ctrl> ctrl;
+    DBuf<double> history;
+    DBuf<unsigned char> diag;
+    DBuf<double> P0;  // initial primitives (caller order) pending the next run
+    bool have_state = false, pending_init = false;
+    double state_gamma = 1.4;
+
+    // graphs
+    cudaGraphExec_t exec1 = nullptr, execU = nullptr;
+    GraphKey key1{}, keyU{};
+
+    // instrumentation
+    double stage_sec[6] = {0, 0, 0, 0, 0, 0};
+    cudaEvent_t ev[8] = {};
+
+    // last error
+    kmf_error_info err{};
+    std::vector<long long> err_idx;
+    int last_G = 0;  // which gradient buffer holds the final gradients of the last stage
+
+    DG dg() const
+    {
+        DG g;
+        g.n = n;
+        g.ld = ld;
+        g.x = x.p;
+        g.y = y.p;
+        g.flag = flag.p;
+        g.dmin = dmin.p;
+        g.eoff = eoff.p;
+        g.deg = deg.p;
+        g.eidx = eidx.p;
+        g.edx = edx.p;
+        g.edy = edy.p;
+        g.fsum = fsum.p;
+        g.fcoef = fcoef.p;
+        g.cptr = cptr.p;
+        return g;
+    }
+    DB db() const
+    {
+        DB b;
+        b.nb = nb;
+        b.point = bpoint.p;
+        b.type = btype.p;
+        b.frame = bframe.p;
+        b.coef = bcoef.p;
+        for (int f = 0; f < 3; f++) {
+            b.ptr[f] = bptr[f].p;
+            b.idx[f] = bidx[f].p;
+            b.dt[f] = bdt[f].p;
+            b.dn[f] = bdn[f].p;
+        }
+        return b;
+    }
+    ~kmf_ctx()
+    {
+        if (exec1) cudaGraphExecDestroy(exec1);
+        if (execU) cudaGraphExecDestroy(execU);
+        for (auto &e : ev)
+            if (e) cudaEventDestroy(e);
+        if (fork) cudaEventDestroy(fork);
+        if (join) cudaEventDestroy(join);
+        if (s0) cudaStreamDestroy(s0);
+        if (s1) cudaStreamDestroy(s1);
+    }
+};
+
+namespace {
+
+// ------------------------------------------------------------------ create
+
+int build_context(kmf_ctx *c, const kmf_geometry *g)
+{
+    const long long n = g->n;
+    if (n <= 0 || n > (1ll << 30)) {
+        set_msg("kmf_create: bad point count %lld", n);
+        return KMF_EINVAL;
+    }
+    const kmf_stencil &F = g->full;
+    if (F.n_owners != n || !F.ptr || !F.idx || !F.sxx || !F.sxy || !F.syy || !F.det) {
+        set_msg("kmf_create: full stencil missing or owner count mismatch");
+        return KMF_EINVAL;
+    }
+    const long long E = F.ptr[n];
+    if (E != F.n_edges || E >= (1ll << 31)) {
+        set_msg("kmf_create: edge count mismatch (%lld vs %lld)", E, (long long)F.n_edges);
+        return KMF_EINVAL;
+    }
+    c->n = (int)n;
+    c->ld = (int)((n + 31) / 32 * 32);
+    c->n_edges = E;
+    const int ld = c->ld;
+
+    // permutation: slot k holds caller point perm[k]
+    std::vector<long long> perm(n), inv(n);
+    c->has_perm = g->perm != nullptr;
+    for (long long k = 0; k < n; k++) perm[k] = c->has_perm ? g->perm[k] : k;
+    {
+        std::vector<char> seen(n, 0);
+        for (long long k = 0; k < n; k++) {
+            long long p = perm[k];
+            if (p < 0 || p >= n || seen[p]) {
+                set_msg("kmf_create: perm is not a permutation of 0..n-1");
+                return KMF_EINVAL;
+            }
+            seen[p] = 1;
+            inv[p] = k;
+        }
+    }
+
+    // offsets derivable from coordinates? (geometry.py:382-383)
+    bool xy = g->x && g->y;
+    if (xy && F.dx && F.dy) {
+        for (long long i = 0; i < n && xy; i++)
+            for (long long e = F.ptr[i]; e < F.ptr[i + 1]; e++) {
+                long long j = F.idx[e];
+                if (j < 0 || j >= n) {
+                    set_msg("kmf_create: neighbour index %lld out of range", j);
+                    return KMF_EINVAL;
+                }
+                double dx = g->x[j] - g->x[i], dy = g->y[j] - g->y[i];
+                if (std::memcmp(&dx, &F.dx[e], 8) || std::memcmp(&dy, &F.dy[e], 8)) {
+                    xy = false;
+                    break;
+                }
+            }
+    } else if (!F.dx || !F.dy) {
+        if (!xy) {
+            set_msg("kmf_create: need either x/y or full.dx/dy");
+            return KMF_EINVAL;
+        }
+    }
+    c->xy = xy;
+
+    auto pad = [&](const double *src, double fill) {
+        std::vector<double> v(ld, fill);
+        for (long long k = 0; k < n; k++) v[k] = src ? src[perm[k]] : fill;
+        return v;
+    };
+    std::vector<double> hx = pad(g->x, 0.0), hy = pad(g->y, 0.0), hd = pad(g->d_min, 1.0);
+    CK(c->x.upload(hx.data(), ld));
+    CK(c->y.upload(hy.data(), ld));
+    CK(c->dmin.upload(hd.data(), ld));
+    {
+        std::vector<unsigned char> fl(ld, 0);
+        for (long long k = 0; k < n; k++) fl[k] = (unsigned char)g->flag[perm[k]];
+        CK(c->flag.upload(fl.data(), ld));
+    }
+    // full-stencil sums [4][ld]
+    {
+        std::vector<double> fs(4 * (size_t)ld, 0.0);
+        for (long long k = 0; k < n; k++) {
+            long long p = perm[k];
+            fs[k] = F.sxx[p];
+            fs[ld + k] = F.sxy[p];
+            fs[2 * ld + k] = F.syy[p];
+            fs[3 * ld + k] = F.det[p];
+        }
+        for (long long k = n; k < ld; k++) fs[3 * ld + k] = 1.0;
+        CK(c->fsum.upload(fs.data(), fs.size()));
+    }
+    // split-family weight coefficients [8][ld]: x-family w = (syy dx - sxy dy)/det,
+    // y-family w = (sxx dy - sxy dx)/det  (solver.py:192-195, det = det_safe)
+    {
+        std::vector<double> cf(8 * (size_t)ld, 0.0);
+        for (int f = 0; f < 4; f++) {
+            if (!g->split_sxx[f] || !g->split_sxy[f] || !g->split_syy[f] || !g->det_safe[f]) {
+                set_msg("kmf_create: split family %d sums missing", f);
+                return KMF_EINVAL;
+            }
+        }
+        for (long long k = 0; k < n; k++) {
+            long long p = perm[k];
+            for (int f = 0; f < 4; f++) {
+                double det = g->det_safe[f][p];
+                double sxx = g->split_sxx[f][p], sxy = g->split_sxy[f][p], syy = g->split_syy[f][p];
+                double cx, cy;
+                if (f < 2) {
+                    cx = syy / det;
+                    cy = -sxy / det;
+                } else {
+                    cx = -sxy / det;
+                    cy = sxx / det;
+                }
+                cf[(2 * f) * (size_t)ld + k] = cx;
+                cf[(2 * f + 1) * (size_t)ld + k] = cy;
+            }
+        }
+        CK(c->fcoef.upload(cf.data(), cf.size()));
+    }
+    // sliced ELL of the full stencil, slots in caller CSR order
+    {
+        const long long ns = (n + 31) / 32;
+        std::vector<int> off(ns + 1, 0), dg(ld, 0);
+        long long total = 0;
+        for (long long s = 0; s < ns; s++) {
+            int w = 0;
+            for (long long k = s * 32; k < std::min(n, s * 32 + 32); k++) {
+                long long p = perm[k];
+                int d = (int)(F.ptr[p + 1] - F.ptr[p]);
+                dg[k] = d;
+                w = std::max(w, d);
+            }
+            if (total > (1ll << 31) - 1) {
+                set_msg("kmf_create: ELL too large");
+                return KMF_EINVAL;
+            }
+            off[s] = (int)total;
+            total += (long long)w * 32;
+        }
+        off[ns] = (int)total;
+        std::vector<int> ei(total > 0 ? total : 1, 0);
+        std::vector<double> ex, ey;
+        if (!xy) {
+            ex.assign(ei.size(), 0.0);
+            ey.assign(ei.size(), 0.0);
+        }
+        std::vector<long long> cp(ld, 0);
+        for (long long k = 0; k < n; k++) {
+            long long p = perm[k];
+            long long base = off[k / 32] + (k % 32);
+            cp[k] = F.ptr[p];
+            for (long long e = F.ptr[p], s = 0; e < F.ptr[p + 1]; e++, s++) {
+                ei[base + s * 32] = (int)inv[F.idx[e]];
+                if (!xy) {
+                    ex[base + s * 32] = F.dx[e];
+                    ey[base + s * 32] = F.dy[e];
+                }
+            }
+            // padding slots point at the owner itself (never read: s < deg)
+            for (long long s = F.ptr[p + 1] - F.ptr[p]; s < (off[k / 32 + 1] - off[k / 32]) / 32; s++)
+                ei[base + s * 32] = (int)k;
+        }
+        CK(c->eoff.upload(off.data(), off.size()));
+        CK(c->deg.upload(dg.data(), dg.size()));
+        CK(c->eidx.upload(ei.data(), ei.size()));
+        CK(c->cptr.upload(cp.data(), cp.size()));
+        if (!xy) {
+            CK(c->edx.upload(ex.data(), ex.size()));
+            CK(c->edy.upload(ey.data(), ey.size()));
+        }
+    }
+    if (c->has_perm) CK(c->perm.upload(perm.data(), n));
+
+    // boundary table: wall entries then outer entries
+    {
+        std::vector<const kmf_frame *> frames;
+        if (g->has_wall) frames.push_back(&g->wall);
+        if (g->has_outer) frames.push_back(&g->outer);
+        int nb = 0;
+        for (auto *fr : frames) nb += (int)fr->b;
+        c->nb = nb;
+        c->nb_wall = g->has_wall ? (int)g->wall.b : 0;
+        std::vector<int> bp(std::max(nb, 1)), bpt[3];
+        std::vector<unsigned char> bt(std::max(nb, 1));
+        std::vector<double> bfr(4 * (size_t)std::max(nb, 1)), bco(6 * (size_t)std::max(nb, 1));
+        std::vector<int> bi[3];
+        std::vector<double> bd[3], bn[3];
+        for (int f = 0; f < 3; f++) bpt[f].push_back(0);
+        int row = 0;
+        for (size_t fi = 0; fi < frames.size(); fi++) {
+            const kmf_frame *fr = frames[fi];
+            const bool is_wall = g->has_wall && fi == 0;
+            const kmf_stencil *fam[3] = {&fr->tplus, &fr->tminus, &fr->normal};
+            for (int f = 0; f < 3; f++) {
+                if (fam[f]->n_owners != fr->b || !fam[f]->ptr) {
+                    set_msg("kmf_create: frame family %d owner mismatch", f);
+                    return KMF_EINVAL;
+                }
+            }
+            for (long long l = 0; l < fr->b; l++, row++) {
+                long long gp = fr->points[l];
+                if (gp < 0 || gp >= n) {
+                    set_msg("kmf_create: frame point out of range");
+                    return KMF_EINVAL;
+                }
+                bp[row] = (int)inv[gp];
+                bt[row] = is_wall ? 1 : 2;
+                bfr[row] = fr->tx[l];
+                bfr[(size_t)nb + row] = fr->ty[l];
+                bfr[2 * (size_t)nb + row] = fr->nx[l];
+                bfr[3 * (size_t)nb + row] = fr->ny[l];
+                for (int f = 0; f < 3; f++) {
+                    const kmf_stencil *s = fam[f];
+                    double det = s->det[l];
+                    double ct, cn;
+                    if (f < 2) {  // d/dt row: (syy st - sxy sn)/det
+                        ct = s->syy[l] / det;
+                        cn = -s->sxy[l] / det;
+                    } else {  // d/dn row: (sxx sn - sxy st)/det
+                        ct = -s->sxy[l] / det;
+                        cn = s->sxx[l] / det;
+                    }
+                    bco[(2 * f) * (size_t)nb + row] = ct;
+                    bco[(2 * f + 1) * (size_t)nb + row] = cn;
+                    for (long long e = s->ptr[l]; e < s->ptr[l + 1]; e++) {
+                        bi[f].push_back((int)inv[s->idx[e]]);
+                        bd[f].push_back(s->dx[e]);
+                        bn[f].push_back(s->dy[e]);
+                    }
+                    bpt[f].push_back((int)bi[f].size());
+                }
+            }
+        }
+        if (nb > 0) {
+            CK(c->bpoint.upload(bp.data(), nb));
+            CK(c->btype.upload(bt.data(), nb));
+            CK(c->bframe.upload(bfr.data(), 4 * (size_t)nb));
+            CK(c->bcoef.upload(bco.data(), 6 * (size_t)nb));
+            for (int f = 0; f < 3; f++) {
+                c->bedges[f] = (long long)bi[f].size();
+                if (bi[f].empty()) {
+                    bi[f].push_back(0);
+                    bd[f].push_back(0);
+                    bn[f].push_back(0);
+                }
+                CK(c->bptr[f].upload(bpt[f].data(), bpt[f].size()));
+                CK(c->bidx[f].upload(bi[f].data(), bi[f].size()));
+                CK(c->bdt[f].upload(bd[f].data(), bd[f].size()));
+                CK(c->bdn[f].upload(bn[f].data(), bn[f].size()));
+            }
+        }
+    }
+
+    // state buffers
+    CK(c->Uo.alloc(4 * (size_t)ld));
+    CK(c->Us.alloc(4 * (size_t)ld));
+    CK(c->q.alloc(4 * (size_t)ld));
+    CK(c->GA.alloc(8 * (size_t)ld));
+    CK(c->GB.alloc(8 * (size_t)ld));
+    CK(c->R.alloc(4 * (size_t)ld));
+    CK(c->dt.alloc(ld));
+    CK(c->stage_buf.alloc(8 * (size_t)n));
+    CK(c->stage_buf2.alloc(8 * (size_t)n));
+    CK(c->ctrl.alloc(1));
+    CK(cudaMemset(c->ctrl.p, 0, sizeof(Ctrl)));
+    CK(cudaMemset(c->R.p, 0, sizeof(double) * 4 * ld));
+    CK(c->diag.alloc(std::max<long long>(E, std::max(std::max(c->bedges[0], c->bedges[1]), c->bedges[2])) + 1));
+    CK(cudaStreamCreateWithFlags(&c->s0, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->s1, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
+    for (auto &e : c->ev) CK(cudaEventCreate(&e));
+    return KMF_OK;
+}
+
+// ------------------------------------------------------------ stage launch
+
+// q-derivatives of one stage: first order into GA, sweeps ping-pong;
+// returns the buffer holding the result (0 = GA, 1 = GB).
+int launch_qgrad(kmf_ctx *c, cudaStream_t s, int stage, int n_inner, Ctrl *ctl, int want_res,
+                 double *res_host_dev_unused = nullptr)
+{
+    (void)res_host_dev_unused;
+    DG g = c->dg();
+    const int nb = nblk(c->n);
+    if (c->xy)
+        k_first_order<true><<<nb, kTB, 0, s>>>(g, c->q.p, c->GA.p, ctl, stage);
+    else
+        k_first_order<false><<<nb, kTB, 0, s>>>(g, c->q.p, c->GA.p, ctl, stage);
+    double *cur = c->GA.p, *nxt = c->GB.p;
+    int which = 0;
+    for (int it = 0; it < n_inner; it++) {
+        if (c->xy)
+            k_sweep<true><<<nb, kTB, 0, s>>>(g, c->q.p, cur, nxt, ctl, stage, 1 + it, want_res);
+        else
+            k_sweep<false><<<nb, kTB, 0, s>>>(g, c->q.p, cur, nxt, ctl, stage, 1 + it, want_res);
+        std::swap(cur, nxt);
+        which ^= 1;
+    }
+    return which;
+}
+
+template <bool XY>
+void launch_flux_xy(kmf_ctx *c, cudaStream_t s, const double *G, int mode, double gamma, int zero_bnd,
+                    Ctrl *ctl, int stage)
+{
+    DG g = c->dg();
+    const int nb = nblk(c->n);
+    const double inv_gm1 = 1.0 / (gamma - 1.0), c_i0 = (2.0 - gamma) / (gamma - 1.0);
+    if (mode == 0) {
+        k_flux<XY, -1><<<nb, kTB, 0, s>>>(g, c->q.p, G, c->R.p, inv_gm1, c_i0, zero_bnd, ctl, stage);
+    } else {
+        k_flux<XY, 0><<<nb, kTB, 0, s>>>(g, c->q.p, G, c->R.p, inv_gm1, c_i0, zero_bnd, ctl, stage);
+        k_flux<XY, 1><<<nb, kTB, 0, s>>>(g, c->q.p, G, c->R.p, inv_gm1, c_i0, zero_bnd, ctl, stage);
+        k_flux<XY, 2><<<nb, kTB, 0, s>>>(g, c->q.p, G, c->R.p, inv_gm1, c_i0, zero_bnd, ctl, stage);
+        k_flux<XY, 3><<<nb, kTB, 0, s>>>(g, c->q.p, G, c->R.p, inv_gm1, c_i0, zero_bnd, ctl, stage);
+    }
+}
+
+void launch_flux(kmf_ctx *c, cudaStream_t s, const double *G, int mode, double gamma, int zero_bnd, Ctrl *ctl,
+                 int stage)
+{
+    if (c->xy)
+        launch_flux_xy<true>(c, s, G, mode, gamma, zero_bnd, ctl, stage);
+    else
+        launch_flux_xy<false>(c, s, G, mode, gamma, zero_bnd, ctl, stage);
+}
+
+void launch_boundary(kmf_ctx *c, cudaStream_t s, const double *G, const double fs[4], double gamma, Ctrl *ctl,
+                     int stage)
+{
+    if (c->nb == 0) return;
+    const double inv_gm1 = 1.0 / (gamma - 1.0), c_i0 = (2.0 - gamma) / (gamma - 1.0);
+    const int warps_per_block = kTB / 32;
+    k_boundary<<<(c->nb + warps_per_block - 1) / warps_per_block, kTB, 0, s>>>(
+        c->dg(), c->db(), c->q.p, G, c->R.p, inv_gm1, c_i0, fs[0], fs[1], fs[2], fs[3], ctl, stage);
+}
+
+void launch_update(kmf_ctx *c, cudaStream_t s, int stage, double gamma, double cfl)
+{
+    DG g = c->dg();
+    const int nb = nblk(c->n);
+    Ctrl *ctl = c->ctrl.p;
+    switch (stage) {
+    case 1: k_update<1><<<nb, kTB, 0, s>>>(g, c->Uo.p, c->Us.p, c->R.p, c->dt.p, c->q.p, gamma, cfl, ctl); break;
+    case 2: k_update<2><<<nb, kTB, 0, s>>>(g, c->Uo.p, c->Us.p, c->R.p, c->dt.p, c->q.p, gamma, cfl, ctl); break;
+    case 3: k_update<3><<<nb, kTB, 0, s>>>(g, c->Uo.p, c->Us.p, c->R.p, c->dt.p, c->q.p, gamma, cfl, ctl); break;
+    default: k_update<4><<<nb, kTB, 0, s>>>(g, c->Uo.p, c->Us.p, c->R.p, c->dt.p, c->q.p, gamma, cfl, ctl); break;
+    }
+}
+
+// One outer iteration (solver.py:515-559) enqueued on s0; the boundary
+// closure runs on a forked branch concurrently with the interior flux.
+void enqueue_iteration(kmf_ctx *c, const kmf_params *p, double *hist, int hist_base, int cap, bool timed)
+{
+    Ctrl *ctl = c->ctrl.p;
+    for (int stage = 1; stage <= 4; stage++) {
+        if (timed) cudaEventRecord(c->ev[0], c->s0);
+        int which = launch_qgrad(c, c->s0, stage, p->n_inner, ctl, 0);
+        const double *G = which ? c->GB.p : c->GA.p;
+        c->last_G = which;
+        if (timed) cudaEventRecord(c->ev[1], c->s0);
+        cudaEventRecord(c->fork, c->s0);
+        cudaStreamWaitEvent(c->s1, c->fork, 0);
+        launch_boundary(c, c->s1, G, p->fs, p->gamma, ctl, stage);
+        cudaEventRecord(c->join, c->s1);
+        launch_flux(c, c->s0, G, p->mode, p->gamma, 0, ctl, stage);
+        cudaStreamWaitEvent(c->s0, c->join, 0);
+        if (timed) cudaEventRecord(c->ev[2], c->s0);
+        launch_update(c, c->s0, stage, p->gamma, p->cfl);
+        if (timed) {
+            cudaEventRecord(c->ev[3], c->s0);
+            cudaEventSynchronize(c->ev[3]);
+            float a = 0, b = 0, d = 0;
+            cudaEventElapsedTime(&a, c->ev[0], c->ev[1]);
+            cudaEventElapsedTime(&b, c->ev[1], c->ev[2]);
+            cudaEventElapsedTime(&d, c->ev[2], c->ev[3]);
+            c->stage_sec[2] += a * 1e-3;
+            c->stage_sec[3] += b * 1e-3;
+            c->stage_sec[4] += d * 1e-3;
+        }
+    }
+    if (timed) cudaEventRecord(c->ev[4], c->s0);
+    k_finalize<<<1, 1, 0, c->s0>>>(ctl, c->n, hist, hist_base, cap, p->convergence_tol);
+    if (timed) {
+        cudaEventRecord(c->ev[5], c->s0);
+        cudaEventSynchronize(c->ev[5]);
+        float a = 0;
+        cudaEventElapsedTime(&a, c->ev[4], c->ev[5]);
+        c->stage_sec[5] += a * 1e-3;
+    }
+}
+
+int get_graph(kmf_ctx *c, const kmf_params *p, int unroll, double *hist, int hist_base, int cap,
+              cudaGraphExec_t *exec, GraphKey *key)
+{
+    GraphKey k;
+    std::memset(&k, 0, sizeof k);
+    k.gamma = p->gamma;
+    k.cfl = p->cfl;
+    for (int i = 0; i < 4; i++) k.fs[i] = p->fs[i];
+    k.tol = p->convergence_tol;
+    k.n_inner = p->n_inner;
+    k.mode = p->mode;
+    k.unroll = unroll;
+    k.cap = cap;
+    k.base = hist_base;
+    k.hist = hist;
+    if (*exec && *key == k) return KMF_OK;
+    if (*exec) {
+        cudaGraphExecDestroy(*exec);
+        *exec = nullptr;
+    }
+    cudaGraph_t graph;
+    CK(cudaStreamBeginCapture(c->s0, cudaStreamCaptureModeThreadLocal));
+    for (int u = 0; u < unroll; u++) enqueue_iteration(c, p, hist, hist_base, cap, false);
+    CK(cudaStreamEndCapture(c->s0, &graph));
+    cudaError_t e = cudaGraphInstantiate(exec, graph, 0);
+    cudaGraphDestroy(graph);
+    CK(e);
+    *key = k;
+    return KMF_OK;
+}
+
+kmf_ctx *g_default_ctx = nullptr;
+
+void record_error(kmf_ctx *c, int code, int iteration, int stage, int context, long long count, const char *msg)
+{
+    if (!c) return;
+    c->err.code = code;
+    c->err.iteration = iteration;
+    c->err.stage = stage;
+    c->err.context = context;
+    c->err.count = count;
+    c->err.n_indices = (long long)c->err_idx.size();
+    std::snprintf(c->err.message, sizeof c->err.message, "%s", msg);
+}
+
+}  // namespace
+
+// ====================================================================== ABI
+
+extern "C" {
+
+int kmf_abi_version(void) { return KMF_ABI_VERSION; }
+
+int kmf_device_count(void)
+{
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+const char *kmf_strerror(void) { return g_last_error.c_str(); }
+
+int kmf_create(kmf_ctx **out, const kmf_geometry *g, int device)
+{
+    if (!out || !g) return KMF_EINVAL;
+    *out = nullptr;
+    CK(cudaSetDevice(device));
+    kmf_ctx *c = new kmf_ctx();
+    c->device = device;
+    int rc = build_context(c, g);
+    if (rc != KMF_OK) {
+        delete c;
+        return rc;
+    }
+    *out = c;
+    return KMF_OK;
+}
+
+void kmf_destroy(kmf_ctx *c)
+{
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    delete c;
+}
+
+int kmf_set_state(kmf_ctx *c, const double *prims)
+{
+    if (!c || !prims) return KMF_EINVAL;
+    CK(cudaSetDevice(c->device));
+    if (!c->P0.p) CK(c->P0.alloc(4 * (size_t)c->n));
+    CK(cudaMemcpyAsync(c->P0.p, prims, sizeof(double) * 4 * (size_t)c->n, cudaMemcpyHostToDevice, c->s0));
+    CK(cudaStreamSynchronize(c->s0));
+    c->have_state = true;
+    c->pending_init = true;
+    return KMF_OK;
+}
+
+namespace {
+// U, q, dt of the first iteration (solver.py:502-506, :520) from the pending
+// initial primitives, or q, dt refreshed from U when continuing.
+int seed_state(kmf_ctx *c, double gamma, double cfl)
+{
+    DG g = c->dg();
+    if (c->pending_init) {
+        k_init<<<nblk(c->n), kTB, 0, c->s0>>>(g, c->P0.p, c->has_perm ? c->perm.p : nullptr, c->Uo.p, c->q.p,
+                                              c->dt.p, gamma, cfl);
+        c->pending_init = false;
+    } else {
+        k_refresh<<<nblk(c->n), kTB, 0, c->s0>>>(g, c->Uo.p, c->q.p, c->dt.p, gamma, cfl);
+    }
+    CK(cudaGetLastError());
+    c->state_gamma = gamma;
+    return KMF_OK;
+}
+}  // namespace
+
+int kmf_run(kmf_ctx *c, const kmf_params *p, int n_iter, double *history, int *iters_done, int *converged)
+{
+    if (!c || !p || n_iter < 0) return KMF_EINVAL;
+    if (!c->have_state) {
+        set_msg("kmf_run: no state (call kmf_set_state first)");
+        return KMF_EINVAL;
+    }
+    if (p->n_inner < 1 || !(p->gamma > 1.0 && p->gamma < 2.0) || !(p->cfl > 0.0 && p->cfl <= 1.0) ||
+        (p->mode != 0 && p->mode != 1)) {
+        set_msg("kmf_run: invalid parameters");
+        return KMF_EINVAL;
+    }
+    CK(cudaSetDevice(c->device));
+    if (iters_done) *iters_done = 0;
+    if (converged) *converged = 0;
+    c->err = kmf_error_info{};
+    c->err_idx.clear();
+    if (n_iter == 0) return KMF_OK;
+    if (int rc = seed_state(c, p->gamma, p->cfl)) return rc;
+    if ((int)c->history.n < n_iter) CK(c->history.alloc(n_iter));
+    Ctrl init;
+    std::memset(&init, 0, sizeof init);
+    init.iter = 1;
+    CK(cudaMemcpyAsync(c->ctrl.p, &init, sizeof init, cudaMemcpyHostToDevice, c->s0));
+    for (double &s : c->stage_sec) s = 0.0;
+
+    const int skip = std::max(0, std::min(p->timing_skip, n_iter));
+    int done = 0;
+    if (p->instrument) {
+        // timed iterations launch eagerly with events around every group
+        for (int it = 0; it < n_iter; it++) {
+            enqueue_iteration(c, p, c->history.p, 1, n_iter, it >= skip);
+        }
+        done = n_iter;
+    } else {
+        const int U = 8;
+        int full = n_iter / U, rest = n_iter % U;
+        if (full) {
+            int rc = get_graph(c, p, U, c->history.p, 1, n_iter, &c->execU, &c->keyU);
+            if (rc) return rc;
+            for (int k = 0; k < full; k++) CK(cudaGraphLaunch(c->execU, c->s0));
+        }
+        if (rest) {
+            int rc = get_graph(c, p, 1, c->history.p, 1, n_iter, &c->exec1, &c->key1);
+            if (rc) return rc;
+            for (int k = 0; k < rest; k++) CK(cudaGraphLaunch(c->exec1, c->s0));
+        }
+        done = n_iter;
+    }
+    (void)done;
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(c->s0));
+    Ctrl fin;
+    CK(cudaMemcpy(&fin, c->ctrl.p, sizeof fin, cudaMemcpyDeviceToHost));
+    const int status = (int)(fin.state & 3ull);
+    int completed = fin.iter - 1;
+    if (completed > n_iter) completed = n_iter;
+    if (history && completed > 0)
+        CK(cudaMemcpy(history, c->history.p, sizeof(double) * completed, cudaMemcpyDeviceToHost));
+    if (iters_done) *iters_done = completed;
+    if (converged) *converged = status == 2;
+    if (status == 1) {
+        // pick the first raise site in reference order within the failing
+        // stage: interior flux (solver.py:540) < boundary (:541) < decode (:547)
+        unsigned m = fin.ctx_mask;
+        int ctx = 0;
+        const int order[] = {KMF_CTX_FLUX_XP, KMF_CTX_WALL_TANGENT, KMF_CTX_WALL_NORMAL, KMF_CTX_OUTER_TANGENT,
+                             KMF_CTX_OUTER_NORMAL, KMF_CTX_C2P_DENSITY, KMF_CTX_C2P_PRESSURE};
+        for (int o : order)
+            if (m & (1u << o)) {
+                ctx = o;
+                break;
+            }
+        c->last_G = 0;
+        record_error(c, KMF_EPOSITIVITY, fin.err_iter, fin.err_stage, ctx, 0, "positivity");
+        return KMF_EPOSITIVITY;
+    }
+    return KMF_OK;
+}
+
+int kmf_get_state(kmf_ctx *c, double *prims, double *U)
+{
+    if (!c) return KMF_EINVAL;
+    CK(cudaSetDevice(c->device));
+    if (!c->have_state) {
+        set_msg("kmf_get_state: no state");
+        return KMF_EINVAL;
+    }
+    if (c->pending_init)
+        if (int rc = seed_state(c, c->state_gamma, 1.0)) return rc;
+    double *dp = prims ? c->stage_buf.p : nullptr;
+    double *du = U ? c->stage_buf2.p : nullptr;
+    k_get_state<<<nblk(c->n), kTB, 0, c->s0>>>(c->dg(), c->Uo.p, c->has_perm ? c->perm.p : nullptr, c->state_gamma,
+                                               dp, du);
+    CK(cudaGetLastError());
+    if (prims) CK(cudaMemcpyAsync(prims, dp, sizeof(double) * 4 * (size_t)c->n, cudaMemcpyDeviceToHost, c->s0));
+    if (U) CK(cudaMemcpyAsync(U, du, sizeof(double) * 4 * (size_t)c->n, cudaMemcpyDeviceToHost, c->s0));
+    CK(cudaStreamSynchronize(c->s0));
+    return KMF_OK;
+}
+
+int kmf_stage_seconds(kmf_ctx *c, double out[6])
+{
+    if (!c || !out) return KMF_EINVAL;
+    for (int i = 0; i < 6; i++) out[i] = c->stage_sec[i];
+    return KMF_OK;
+}
+
+int kmf_last_error(kmf_ctx *c, kmf_error_info *info)
+{
+    if (!c || !info) return KMF_EINVAL;
+    *info = c->err;
+    return KMF_OK;
+}
+
+int kmf_last_indices(kmf_ctx *c, int64_t *idx, int64_t cap)
+{
+    if (!c) return KMF_EINVAL;
+    int64_t k = 0;
+    for (; k < cap && k < (int64_t)c->err_idx.size(); k++) idx[k] = c->err_idx[k];
+    return (int)k;
+}
+
+// ------------------------------------------------------- context operators
+
+namespace {
+int upload_fields(kmf_ctx *c, const double *h, int nc, double *dev)
+{
+    CK(cudaMemcpyAsync(c->stage_buf.p, h, sizeof(double) * nc * (size_t)c->n, cudaMemcpyHostToDevice, c->s0));
+    k_to_dev<<<nblk(c->n), kTB, 0, c->s0>>>(c->n, c->ld, nc, c->stage_buf.p, c->has_perm ? c->perm.p : nullptr,
+                                            dev);
+    CK(cudaGetLastError());
+    return KMF_OK;
+}
+int download_fields(kmf_ctx *c, const double *dev, int nc, double *h)
+{
+    k_from_dev<<<nblk(c->n), kTB, 0, c->s0>>>(c->n, c->ld, nc, dev, c->has_perm ? c->perm.p : nullptr,
+                                              c->stage_buf.p);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(h, c->stage_buf.p, sizeof(double) * nc * (size_t)c->n, cudaMemcpyDeviceToHost, c->s0));
+    CK(cudaStreamSynchronize(c->s0));
+    return KMF_OK;
+}
+int reset_ctrl(kmf_ctx *c)
+{
+    CK(cudaMemsetAsync(c->ctrl.p, 0, sizeof(Ctrl), c->s0));
+    return KMF_OK;
+}
+int read_ctrl(kmf_ctx *c, Ctrl *out)
+{
+    CK(cudaMemcpyAsync(out, c->ctrl.p, sizeof(Ctrl), cudaMemcpyDeviceToHost, c->s0));
+    CK(cudaStreamSynchronize(c->s0));
+    return KMF_OK;
+}
+}  // namespace
+
+int kmf_op_timestep(kmf_ctx *c, const double *prims, double cfl, double gamma, double *dt)
+{
+    if (!c || !prims || !dt) return KMF_EINVAL;
+    if (!(cfl > 0.0 && cfl <= 1.0)) {
+        set_msg("cfl must lie in (0, 1]");
+        return KMF_EINVAL;
+    }
+    CK(cudaSetDevice(c->device));
+    int rc = upload_fields(c, prims, 4, c->R.p);
+    if (rc) return rc;
+    k_op_timestep<<<nblk(c->n), kTB, 0, c->s0>>>(c->dg(), c->R.p, cfl, gamma, c->dt.p);
+    CK(cudaGetLastError());
+    return download_fields(c, c->dt.p, 1, dt);
+}
+
+int kmf_op_first_order(kmf_ctx *c, const double *q, double *qx, double *qy)
+{
+    if (!c || !q || !qx || !qy) return KMF_EINVAL;
+    CK(cudaSetDevice(c->device));
+    int rc = upload_fields(c, q, 4, c->q.p);
+    if (rc) return rc;
+    if ((rc = reset_ctrl(c))) return rc;
+    const int nb = nblk(c->n);
+    if (c->xy)
+        k_first_order<true><<<nb, kTB, 0, c->s0>>>(c->dg(), c->q.p, c->GA.p, c->ctrl.p, 0);
+    else
+        k_first_order<false><<<nb, kTB, 0, c->s0>>>(c->dg(), c->q.p, c->GA.p, c->ctrl.p, 0);
+    CK(cudaGetLastError());
+    if ((rc = download_fields(c, c->GA.p, 4, qx))) return rc;
+    return download_fields(c, c->GA.p + 4 * (size_t)c->ld, 4, qy);
+}
+
+int kmf_op_q_derivatives(kmf_ctx *c, const double *q, int n_inner, const double *pqx, const double *pqy,
+                         double *qx, double *qy, double *inner_residuals)
+{
+    if (!c || !q || !qx || !qy) return KMF_EINVAL;
+    if (n_inner < 1) {
+        set_msg("n_inner must be at least 1");
+        return KMF_EINVAL;
+    }
+    CK(cudaSetDevice(c->device));
+    int rc = upload_fields(c, q, 4, c->q.p);
+    if (rc) return rc;
+    if ((rc = reset_ctrl(c))) return rc;
+    const int nb = nblk(c->n);
+    DG g = c->dg();
+    if (pqx && pqy) {
+        if ((rc = upload_fields(c, pqx, 4, c->GA.p))) return rc;
+        if ((rc = upload_fields(c, pqy, 4, c->GA.p + 4 * (size_t)c->ld))) return rc;
+    } else if (c->xy) {
+        k_first_order<true><<<nb, kTB, 0, c->s0>>>(g, c->q.p, c->GA.p, c->ctrl.p, 0);
+    } else {
+        k_first_order<false><<<nb, kTB, 0, c->s0>>>(g, c->q.p, c->GA.p, c->ctrl.p, 0);
+    }
+    double *cur = c->GA.p, *nxt = c->GB.p;
+    for (int it = 0; it < n_inner; it++) {
+        CK(cudaMemsetAsync(&c->ctrl.p->resmax, 0, sizeof(unsigned long long), c->s0));
+        if (c->xy)
+            k_sweep<true><<<nb, kTB, 0, c->s0>>>(g, c->q.p, cur, nxt, c->ctrl.p, 0, 1 + it, 1);
+        else
+            k_sweep<false><<<nb, kTB, 0, c->s0>>>(g, c->q.p, cur, nxt, c->ctrl.p, 0, 1 + it, 1);
+        CK(cudaGetLastError());
+        if (inner_residuals) {
+            unsigned long long b = 0;
+            CK(cudaMemcpyAsync(&b, &c->ctrl.p->resmax, sizeof b, cudaMemcpyDeviceToHost, c->s0));
+            CK(cudaStreamSynchronize(c->s0));
+            std::memcpy(&inner_residuals[it], &b, 8);
+        }
+        std::swap(cur, nxt);
+    }
+    if ((rc = download_fields(c, cur, 4, qx))) return rc;
+    return download_fields(c, cur + 4 * (size_t)c->ld, 4, qy);
+}
+
+namespace {
+int upload_flow(kmf_ctx *c, const double *q, const double *qx, const double *qy)
+{
+    int rc = upload_fields(c, q, 4, c->q.p);
+    if (rc) return rc;
+    if ((rc = upload_fields(c, qx, 4, c->GA.p))) return rc;
+    return upload_fields(c, qy, 4, c->GA.p + 4 * (size_t)c->ld);
+}
+}  // namespace
+
+int kmf_op_flux_residual(kmf_ctx *c, const double *q, const double *qx, const double *qy, int mode, double gamma,
+                         double *R)
+{
+    if (!c || !q || !qx || !qy || !R) return KMF_EINVAL;
+    if (mode != 0 && mode != 1) {
+        set_msg("mode must be one of ('fused', 'split4')");
+        return KMF_EINVAL;
+    }
+    CK(cudaSetDevice(c->device));
+    int rc = upload_flow(c, q, qx, qy);
+    if (rc) return rc;
+    if ((rc = reset_ctrl(c))) return rc;
+    c->err = kmf_error_info{};
+    c->err_idx.clear();
+    launch_flux(c, c->s0, c->GA.p, mode, gamma, 1, c->ctrl.p, 0);
+    CK(cudaGetLastError());
+    Ctrl fin;
+    if ((rc = read_ctrl(c, &fin))) return rc;
+    if (fin.state & 1ull) {
+        c->last_G = 0;
+        record_error(c, KMF_EPOSITIVITY, 0, 0, KMF_CTX_FLUX_XP, 0, "positivity");
+        return KMF_EPOSITIVITY;
+    }
+    return download_fields(c, c->R.p, 4, R);
+}
+
+int kmf_op_boundary(kmf_ctx *c, const double *q, const double *qx, const double *qy, const double fs[4],
+                    double gamma, double *R)
+{
+    if (!c || !q || !qx || !qy || !R || !fs) return KMF_EINVAL;
+    CK(cudaSetDevice(c->device));
+    int rc = upload_flow(c, q, qx, qy);
+    if (rc) return rc;
+    if ((rc = upload_fields(c, R, 4, c->R.p))) return rc;
+    if ((rc = reset_ctrl(c))) return rc;
+    c->err = kmf_error_info{};
+    c->err_idx.clear();
+    launch_boundary(c, c->s0, c->GA.p, fs, gamma, c->ctrl.p, 0);
+    CK(cudaGetLastError());
+    Ctrl fin;
+    if ((rc = read_ctrl(c, &fin))) return rc;
+    if (fin.state & 1ull) {
+        unsigned m = fin.ctx_mask;
+        int ctx = KMF_CTX_WALL_TANGENT;
+        const int order[] = {KMF_CTX_WALL_TANGENT, KMF_CTX_WALL_NORMAL, KMF_CTX_OUTER_TANGENT, KMF_CTX_OUTER_NORMAL};
+        for (int o : order)
+            if (m & (1u << o)) {
+                ctx = o;
+                break;
+            }
+        c->last_G = 0;
+        record_error(c, KMF_EPOSITIVITY, 0, 0, ctx, 0, "positivity");
+        return KMF_EPOSITIVITY;
+    }
+    return download_fields(c, c->R.p, 4, R);
+}
+
+// flags for every caller-CSR edge of the full stencil computed from the
+// device's current q and the gradient buffer `which` (0 GA, 1 GB)
+int kmf_diag_flux(kmf_ctx *c, int which, uint8_t *flags)
+{
+    if (!c || !flags) return KMF_EINVAL;
+    CK(cudaSetDevice(c->device));
+    const double *G = which ? c->GB.p : c->GA.p;
+    if (c->xy)
+        k_diag_flux<true><<<nblk(c->n), kTB, 0, c->s0>>>(c->dg(), c->q.p, G, c->diag.p);
+    else
+        k_diag_flux<false><<<nblk(c->n), kTB, 0, c->s0>>>(c->dg(), c->q.p, G, c->diag.p);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(flags, c->diag.p, (size_t)c->n_edges, cudaMemcpyDeviceToHost, c->s0));
+    CK(cudaStreamSynchronize(c->s0));
+    return KMF_OK;
+}
+
+// flags per frame edge of family fam (0 tplus, 1 tminus, 2 normal) over the
+// concatenated boundary table (wall rows first, then outer)
+int kmf_diag_frame(kmf_ctx *c, int which, int fam, uint8_t *flags)
+{
+    if (!c || !flags || fam < 0 || fam > 2) return KMF_EINVAL;
+    if (c->nb == 0) return KMF_OK;
+    CK(cudaSetDevice(c->device));
+    const double *G = which ? c->GB.p : c->GA.p;
+    k_diag_frame<<<nblk(c->nb), kTB, 0, c->s0>>>(c->dg(), c->db(), fam, c->q.p, G, c->diag.p);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(flags, c->diag.p, (size_t)c->bedges[fam], cudaMemcpyDeviceToHost, c->s0));
+    CK(cudaStreamSynchronize(c->s0));
+    return KMF_OK;
+}
+
+// the stage-state U written by the last update launch ((4,n), caller order):
+// U_stage for stages 1-3, U_outer for stage 4
+int kmf_diag_stage_state(kmf_ctx *c, int stage, double *U)
+{
+    if (!c || !U) return KMF_EINVAL;
+    CK(cudaSetDevice(c->device));
+    return download_fields(c, stage == 4 ? c->Uo.p : c->Us.p, 4, U);
+}
+
+// ------------------------------------------------------ point operators
+
+}  // extern "C"
+
+namespace {
+struct Tmp {
+    std::vector<void *> ptrs;
+    ~Tmp()
+    {
+        for (void *p : ptrs) cudaFree(p);
+    }
+    template <typename T>
+    T *get(size_t count)
+    {
+        void *p = nullptr;
+        if (cudaMalloc(&p, sizeof(T) * (count ? count : 1)) != cudaSuccess) return nullptr;
+        ptrs.push_back(p);
+        return (T *)p;
+    }
+};
+
+#define TMP_OR_FAIL(var, T, count)                    \
+    T *var = tmp.get<T>(count);                       \
+    if (!var) {                                       \
+        set_msg("cudaMalloc failed (%zu)", (size_t)(count)); \
+        return KMF_ECUDA;                             \
+    }
+
+int ensure_device()
+{
+    int n = kmf_device_count();
+    if (n <= 0) {
+        set_msg("no CUDA device visible");
+        return KMF_ECUDA;
+    }
+    return KMF_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int kmf_op_primitives_to_q(int64_t n, const double *prims, double gamma, double *q, uint8_t *flags)
+{
+    if (n <= 0 || !prims || !q || !flags) return KMF_EINVAL;
+    if (int rc = ensure_device()) return rc;
+    Tmp tmp;
+    TMP_OR_FAIL(dp, double, 4 * n);
+    TMP_OR_FAIL(dq, double, 4 * n);
+    TMP_OR_FAIL(df, unsigned char, n);
+    CK(cudaMemcpy(dp, prims, sizeof(double) * 4 * n, cudaMemcpyHostToDevice));
+    k_op_p2q<<<nblk(n), kTB>>>((int)n, dp, gamma, dq, df);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(q, dq, sizeof(double) * 4 * n, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(flags, df, n, cudaMemcpyDeviceToHost));
+    return KMF_OK;
+}
+
+int kmf_op_q_to_primitives(int64_t n, const double *q, double gamma, double *prims, uint8_t *flags)
+{
+    if (n <= 0 || !prims || !q || !flags) return KMF_EINVAL;
+    if (int rc = ensure_device()) return rc;
+    Tmp tmp;
+    TMP_OR_FAIL(dq, double, 4 * n);
+    TMP_OR_FAIL(dp, double, 4 * n);
+    TMP_OR_FAIL(df, unsigned char, n);
+    CK(cudaMemcpy(dq, q, sizeof(double) * 4 * n, cudaMemcpyHostToDevice));
+    k_op_q2p<<<nblk(n), kTB>>>((int)n, dq, gamma, dp, df);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(prims, dp, sizeof(double) * 4 * n, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(flags, df, n, cudaMemcpyDeviceToHost));
+    return KMF_OK;
+}
+
+int kmf_op_primitives_to_conserved(int64_t n, const double *prims, double gamma, double *U, uint8_t *flags)
+{
+    if (n <= 0 || !prims || !U || !flags) return KMF_EINVAL;
+    if (int rc = ensure_device()) return rc;
+    Tmp tmp;
+    TMP_OR_FAIL(dp, double, 4 * n);
+    TMP_OR_FAIL(du, double, 4 * n);
+    TMP_OR_FAIL(df, unsigned char, n);
+    CK(cudaMemcpy(dp, prims, sizeof(double) * 4 * n, cudaMemcpyHostToDevice));
+    k_op_p2u<<<nblk(n), kTB>>>((int)n, dp, gamma, du, df);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(U, du, sizeof(double) * 4 * n, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(flags, df, n, cudaMemcpyDeviceToHost));
+    return KMF_OK;
+}
+
+int kmf_op_conserved_to_primitives(int64_t n, const double *U, double gamma, double *prims, uint8_t *flags)
+{
+    if (n <= 0 || !prims || !U || !flags) return KMF_EINVAL;
+    if (int rc = ensure_device()) return rc;
+    Tmp tmp;
+    TMP_OR_FAIL(du, double, 4 * n);
+    TMP_OR_FAIL(dp, double, 4 * n);
+    TMP_OR_FAIL(df, unsigned char, n);
+    CK(cudaMemcpy(du, U, sizeof(double) * 4 * n, cudaMemcpyHostToDevice));
+    k_op_u2p<<<nblk(n), kTB>>>((int)n, du, gamma, dp, df);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(prims, dp, sizeof(double) * 4 * n, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(flags, df, n, cudaMemcpyDeviceToHost));
+    return KMF_OK;
+}
+
+int kmf_op_split_flux(int64_t n, const double *prims, int axis, int sign, double gamma, double *G)
+{
+    if (n <= 0 || !prims || !G || (axis != 0 && axis != 1) || (sign != 1 && sign != -1)) return KMF_EINVAL;
+    if (int rc = ensure_device()) return rc;
+    Tmp tmp;
+    TMP_OR_FAIL(dp, double, 4 * n);
+    TMP_OR_FAIL(dg, double, 4 * n);
+    CK(cudaMemcpy(dp, prims, sizeof(double) * 4 * n, cudaMemcpyHostToDevice));
+    k_op_split_flux<<<nblk(n), kTB>>>((int)n, dp, axis, (double)sign, gamma, dg);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(G, dg, sizeof(double) * 4 * n, cudaMemcpyDeviceToHost));
+    return KMF_OK;
+}
+
+int kmf_op_full_flux(int64_t n, const double *prims, int axis, double gamma, double *F)
+{
+    if (n <= 0 || !prims || !F || (axis != 0 && axis != 1)) return KMF_EINVAL;
+    if (int rc = ensure_device()) return rc;
+    Tmp tmp;
+    TMP_OR_FAIL(dp, double, 4 * n);
+    TMP_OR_FAIL(df, double, 4 * n);
+    CK(cudaMemcpy(dp, prims, sizeof(double) * 4 * n, cudaMemcpyHostToDevice));
+    k_op_full_flux<<<nblk(n), kTB>>>((int)n, dp, axis, gamma, df);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(F, df, sizeof(double) * 4 * n, cudaMemcpyDeviceToHost));
+    return KMF_OK;
+}
+
+int kmf_op_state_update(int64_t n, const double *Uo, const double *Us, int stage, const double *dt,
+                        const double *R, double *Un)
+{
+    if (n <= 0 || !Uo || !Us || !dt || !R || !Un) return KMF_EINVAL;
+    if (stage < 1 || stage > 4) {
+        set_msg("stage must be 1..4");
+        return KMF_EINVAL;
+    }
+    if (int rc = ensure_device()) return rc;
+    Tmp tmp;
+    TMP_OR_FAIL(a, double, 4 * n);
+    TMP_OR_FAIL(b, double, 4 * n);
+    TMP_OR_FAIL(r, double, 4 * n);
+    TMP_OR_FAIL(d, double, n);
+    TMP_OR_FAIL(o, double, 4 * n);
+    CK(cudaMemcpy(a, Uo, sizeof(double) * 4 * n, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(b, Us, sizeof(double) * 4 * n, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(r, R, sizeof(double) * 4 * n, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d, dt, sizeof(double) * n, cudaMemcpyHostToDevice));
+    k_op_update<<<nblk(n), kTB>>>((int)n, a, b, stage, d, r, o);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(Un, o, sizeof(double) * 4 * n, cudaMemcpyDeviceToHost));
+    return KMF_OK;
+}
+
+int kmf_op_residue(int64_t n, const double *Un, const double *Uold, double *out)
+{
+    if (n <= 0 || !Un || !Uold || !out) return KMF_EINVAL;
+    if (int rc = ensure_device()) return rc;
+    Tmp tmp;
+    TMP_OR_FAIL(a, double, n);
+    TMP_OR_FAIL(b, double, n);
+    TMP_OR_FAIL(l, unsigned long long, kLimbs);
+    TMP_OR_FAIL(o, double, 1);
+    CK(cudaMemcpy(a, Un, sizeof(double) * n, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(b, Uold, sizeof(double) * n, cudaMemcpyHostToDevice));
+    CK(cudaMemset(l, 0, sizeof(unsigned long long) * kLimbs));
+    k_op_residue<<<nblk(n), kTB>>>((int)n, a, b, l);
+    k_op_residue_fin<<<1, 1>>>((int)n, l, o);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(out, o, sizeof(double), cudaMemcpyDeviceToHost));
+    return KMF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,883 @@
+// kmf_kernels.cuh -- sm_100a kernels of the q-LSKUM outer iteration.
+//
+// Device data layout:
+//   * per-point fields are SoA with a padded leading dimension `ld`
+//     (component c of device slot i at [c*ld + i]): q[4], G[8] = (qx[4],
+//     qy[4]), U_outer[4], U_stage[4], R[4], dt, flags;
+//   * the full stencil is stored as sliced ELLPACK with slice height 32
+//     (one warp): neighbour slot s of point i lives at
+//     eoff[i/32] + s*32 + i%32, so the per-slot gathers of a warp are one
+//     coalesced 128 B index load; slots keep the reference CSR order
+//     (np.sort order, geometry.py:345) because that order IS the summation
+//     order of every least-squares sum;
+//   * the four split families are not stored: membership is the sign of
+//     dx/dy (geometry.py:544-549), recomputed bitwise from x, y.
+//
+// One thread per point everywhere except the boundary closure (one warp
+// per boundary point, lanes over frame edges).
+#pragma once
+#include "kmf_math.cuh"
+
+namespace kmf {
+
+constexpr int kTB = 128;   // threads per block, point kernels
+constexpr int kSlotFlux = 0xE00;
+constexpr int kSlotUpdate = 0xE01;
+constexpr int kStageFinal = 7;
+
+// Control block in device memory.  `state` packs a status and the sequence
+// number of the launch that set it: 0 running, (seq<<2)|1 positivity error,
+// (seq<<2)|2 converged.  Kernels skip their work once state != 0 unless they
+// carry the very same seq (so every block of the failing launch, and the
+// boundary kernel that shares its seq, still completes).
+struct Ctrl {
+    unsigned long long state;
+    int iter;
+    int err_iter;
+    int err_stage;
+    unsigned int ctx_mask;
+    unsigned long long resmax;  // inner-residual max (bits of a nonnegative double)
+    unsigned long long limbs[kLimbs];
+};
+
+KMF_HD long long seq_of(int iter, int stage, int slot)
+{
+    return ((long long)iter << 16) | ((long long)stage << 12) | (long long)slot;
+}
+
+KMF_HD bool should_skip(const Ctrl *c, int stage, int slot)
+{
+    unsigned long long st = *(volatile const unsigned long long *)&c->state;
+    if (st == 0ull) return false;
+    long long me = seq_of(*(volatile const int *)&c->iter, stage, slot);
+    return (long long)(st >> 2) != me;
+}
+
+__device__ __forceinline__ void raise_err(Ctrl *c, int stage, int slot, int ctx)
+{
+    atomicOr(&c->ctx_mask, 1u << ctx);
+    unsigned long long want = ((unsigned long long)seq_of(c->iter, stage, slot) << 2) | 1ull;
+    if (atomicCAS(&c->state, 0ull, want) == 0ull) {
+        c->err_iter = c->iter;
+        c->err_stage = stage;
+    }
+}
+
+// Geometry as seen by the point kernels.
+struct DG {
+    int n, ld;
+    const double *__restrict__ x;
+    const double *__restrict__ y;
+    const unsigned char *__restrict__ flag;
+    const double *__restrict__ dmin;
+    const int *__restrict__ eoff;   // per 32-point slice
+    const int *__restrict__ deg;    // per point
+    const int *__restrict__ eidx;   // ELL neighbour slots
+    const double *__restrict__ edx;  // ELL offsets (only when not derived from x, y)
+    const double *__restrict__ edy;
+    const double *__restrict__ fsum;   // [4][ld] full-stencil sxx, sxy, syy, det
+    const double *__restrict__ fcoef;  // [8][ld] (cx, cy) of x+, x-, y+, y-
+    const long long *__restrict__ cptr;  // caller CSR ptr of the point in this slot (diag)
+};
+
+// Boundary frames (wall entries first, then outer), geometry.py:573-646.
+struct DB {
+    int nb;
+    const int *__restrict__ point;          // device slot of the owner
+    const unsigned char *__restrict__ type;  // 1 wall, 2 outer
+    const double *__restrict__ frame;       // [4][nb] tx, ty, nx, ny
+    const double *__restrict__ coef;        // [6][nb] (ct, cn) of tplus, tminus, normal
+    const int *__restrict__ ptr[3];
+    const int *__restrict__ idx[3];
+    const double *__restrict__ dt[3];
+    const double *__restrict__ dn[3];
+};
+
+template <bool XY>
+KMF_HD void edge_offsets(const DG &g, int ent, int j, double xi, double yi, double &dx, double &dy)
+{
+    if (XY) {
+        dx = SUB(g.x[j], xi);  // geometry.py:382-383, bitwise
+        dy = SUB(g.y[j], yi);
+    } else {
+        dx = g.edx[ent];
+        dy = g.edy[ent];
+    }
+}
+
+KMF_HD int ell_base(const DG &g, int i) { return g.eoff[i >> 5] + (i & 31); }
+
+// ---------------------------------------------------------------------------
+// lsq.py:164-175 first_order_q_gradients -- bitwise (CSR-order sums, no FMA)
+template <bool XY>
+__global__ void __launch_bounds__(kTB) k_first_order(DG g, const double *__restrict__ q,
+                                                     double *__restrict__ G, Ctrl *c, int stage)
+{
+    if (c && should_skip(c, stage, 0)) return;
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= g.n) return;
+    const int ld = g.ld;
+    double qi[4], sx[4], sy[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        qi[k] = q[k * ld + i];
+        sx[k] = 0.0;
+        sy[k] = 0.0;
+    }
+    const double xi = g.x[i], yi = g.y[i];
+    const int base = ell_base(g, i), d = g.deg[i];
+    for (int s = 0; s < d; s++) {
+        const int ent = base + s * 32;
+        const int j = g.eidx[ent];
+        double dx, dy;
+        edge_offsets<XY>(g, ent, j, xi, yi, dx, dy);
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            double dq = SUB(q[k * ld + j], qi[k]);
+            sx[k] = ADD(sx[k], MUL(dx, dq));
+            sy[k] = ADD(sy[k], MUL(dy, dq));
+        }
+    }
+    const double sxx = g.fsum[i], sxy = g.fsum[ld + i], syy = g.fsum[2 * ld + i], det = g.fsum[3 * ld + i];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        G[k * ld + i] = DIV(SUB(MUL(syy, sx[k]), MUL(sxy, sy[k])), det);
+        G[(4 + k) * ld + i] = DIV(SUB(MUL(sxx, sy[k]), MUL(sxy, sx[k])), det);
+    }
+}
+
+// lsq.py:214-227 one Jacobi sweep of the defect-corrected gradients --
+// bitwise.  With `resmax` the max |new - old| (lsq.py:238-243) is reduced.
+template <bool XY>
+__global__ void __launch_bounds__(kTB) k_sweep(DG g, const double *__restrict__ q,
+                                               const double *__restrict__ Gin, double *__restrict__ Gout,
+                                               Ctrl *c, int stage, int slot, int want_res)
+{
+    if (c && should_skip(c, stage, slot)) return;
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    double rmax = 0.0;
+    if (i < g.n) {
+        const int ld = g.ld;
+        double qi[4], gxi[4], gyi[4], sx[4], sy[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            qi[k] = q[k * ld + i];
+            gxi[k] = Gin[k * ld + i];
+            gyi[k] = Gin[(4 + k) * ld + i];
+            sx[k] = 0.0;
+            sy[k] = 0.0;
+        }
+        const double xi = g.x[i], yi = g.y[i];
+        const int base = ell_base(g, i), d = g.deg[i];
+        for (int s = 0; s < d; s++) {
+            const int ent = base + s * 32;
+            const int j = g.eidx[ent];
+            double dx, dy;
+            edge_offsets<XY>(g, ent, j, xi, yi, dx, dy);
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                double ti = qtilde(q[k * ld + j], Gin[k * ld + j], Gin[(4 + k) * ld + j], dx, dy);
+                double t0 = qtilde(qi[k], gxi[k], gyi[k], dx, dy);
+                double dq = SUB(ti, t0);
+                sx[k] = ADD(sx[k], MUL(dx, dq));
+                sy[k] = ADD(sy[k], MUL(dy, dq));
+            }
+        }
+        const double sxx = g.fsum[i], sxy = g.fsum[ld + i], syy = g.fsum[2 * ld + i],
+                     det = g.fsum[3 * ld + i];
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            double nx_ = DIV(SUB(MUL(syy, sx[k]), MUL(sxy, sy[k])), det);
+            double ny_ = DIV(SUB(MUL(sxx, sy[k]), MUL(sxy, sx[k])), det);
+            Gout[k * ld + i] = nx_;
+            Gout[(4 + k) * ld + i] = ny_;
+            if (want_res) {
+                rmax = fmax(rmax, fabs(nx_ - gxi[k]));
+                rmax = fmax(rmax, fabs(ny_ - gyi[k]));
+                if (isnan(nx_ - gxi[k]) || isnan(ny_ - gyi[k])) rmax = __longlong_as_double(0x7ff8000000000000ll);
+            }
+        }
+    }
+    if (want_res) {
+        unsigned long long b = (unsigned long long)__double_as_longlong(rmax);
+        for (int o = 16; o; o >>= 1) {
+            unsigned long long t = __shfl_xor_sync(0xffffffffu, b, o);
+            b = t > b ? t : b;
+        }
+        if ((threadIdx.x & 31) == 0) atomicMax(&c->resmax, b);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// solver.py:162-235 flux_residual (interior rows).  FAM < 0: fused, all four
+// split families in one pass over the stencil; FAM = 0..3: split4, one
+// family per launch, R accumulated in the order x+, x-, y+, y-.
+//
+// Per edge the two perturbed states q~_i, q~_0 (solver.py:184-185, bitwise)
+// are decoded ONCE and shared by the x- and the y-family flux of that edge
+// (the reference decodes them once per family).  The LS derivative of each
+// family is accumulated as sum_e w_f(e) * dG_f(e) with the static weight
+// w_f(e) = cx_f*dx + cy_f*dy (cx, cy = rows of the inverse 2x2 matrix,
+// solver.py:192-195), in CSR order per family.  Fused and split4 run the
+// same per-edge code and add families in the same order: bitwise equal.
+template <bool XY, int FAM>
+__global__ void __launch_bounds__(kTB) k_flux(DG g, const double *__restrict__ q,
+                                              const double *__restrict__ G, double *__restrict__ R,
+                                              double inv_gm1, double c_i0, int zero_boundary, Ctrl *c,
+                                              int stage)
+{
+    if (c && should_skip(c, stage, kSlotFlux)) return;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= g.n) return;
+    const int ld = g.ld;
+    const bool interior = g.flag[i] == 0;
+    double qi[4], gxi[4], gyi[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        qi[k] = q[k * ld + i];
+        gxi[k] = G[k * ld + i];
+        gyi[k] = G[(4 + k) * ld + i];
+    }
+    double cf[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) cf[k] = interior ? g.fcoef[k * ld + i] : 0.0;
+    double acc[4][4];
+#pragma unroll
+    for (int f = 0; f < 4; f++)
+#pragma unroll
+        for (int k = 0; k < 4; k++) acc[f][k] = 0.0;
+
+    const double xi = g.x[i], yi = g.y[i];
+    const int base = ell_base(g, i), d = g.deg[i];
+    bool bad = false;
+    for (int s = 0; s < d; s++) {
+        const int ent = base + s * 32;
+        const int j = g.eidx[ent];
+        double dx, dy;
+        edge_offsets<XY>(g, ent, j, xi, yi, dx, dy);
+        if (FAM == 0 && !(dx <= 0.0)) continue;
+        if (FAM == 1 && !(dx >= 0.0)) continue;
+        if (FAM == 2 && !(dy <= 0.0)) continue;
+        if (FAM == 3 && !(dy >= 0.0)) continue;
+        double ti[4], t0[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            ti[k] = qtilde(q[k * ld + j], G[k * ld + j], G[(4 + k) * ld + j], dx, dy);
+            t0[k] = qtilde(qi[k], gxi[k], gyi[k], dx, dy);
+        }
+        // solver.py:164 positivity (q4 >= 0, NaN caught by q_to_primitives)
+        if (!(ti[3] < 0.0) || !(t0[3] < 0.0)) {
+            bad = true;
+            continue;
+        }
+        if (!interior) continue;  // rows zeroed (solver.py:233-234)
+        EState si, s0;
+        decode(ti[0], ti[1], ti[2], ti[3], inv_gm1, si);
+        decode(t0[0], t0[1], t0[2], t0[3], inv_gm1, s0);
+        EShared hi, h0;
+        shared_of(si, c_i0, hi);
+        shared_of(s0, c_i0, h0);
+        double gi[4], g0[4];
+        if (FAM < 2) {
+            // x family: x+ holds dx <= 0 (tie in both), x- dx >= 0
+            const bool primary_p = FAM < 0 ? (dx <= 0.0) : (FAM == 0);
+            const double sg = primary_p ? 1.0 : -1.0;
+            const double cx = primary_p ? cf[0] : cf[2];
+            const double cy = primary_p ? cf[1] : cf[3];
+            sflux(si, hi, false, sg, gi);
+            sflux(s0, h0, false, sg, g0);
+            const double w = fma(cx, dx, cy * dy);
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                double a = fma(w, gi[k] - g0[k], primary_p ? acc[0][k] : acc[1][k]);
+                if (primary_p)
+                    acc[0][k] = a;
+                else
+                    acc[1][k] = a;
+            }
+            if (FAM < 0 && dx == 0.0) {  // tie: also in x-
+                sflux(si, hi, false, -1.0, gi);
+                sflux(s0, h0, false, -1.0, g0);
+                const double w2 = fma(cf[2], dx, cf[3] * dy);
+#pragma unroll
+                for (int k = 0; k < 4; k++) acc[1][k] = fma(w2, gi[k] - g0[k], acc[1][k]);
+            }
+        }
+        if (FAM < 0 || FAM >= 2) {
+            const bool primary_p = FAM < 0 ? (dy <= 0.0) : (FAM == 2);
+            const double sg = primary_p ? 1.0 : -1.0;
+            const double cx = primary_p ? cf[4] : cf[6];
+            const double cy = primary_p ? cf[5] : cf[7];
+            sflux(si, hi, true, sg, gi);
+            sflux(s0, h0, true, sg, g0);
+            const double w = fma(cx, dx, cy * dy);
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                double a = fma(w, gi[k] - g0[k], primary_p ? acc[2][k] : acc[3][k]);
+                if (primary_p)
+                    acc[2][k] = a;
+                else
+                    acc[3][k] = a;
+            }
+            if (FAM < 0 && dy == 0.0) {
+                sflux(si, hi, true, -1.0, gi);
+                sflux(s0, h0, true, -1.0, g0);
+                const double w2 = fma(cf[6], dx, cf[7] * dy);
+#pragma unroll
+                for (int k = 0; k < 4; k++) acc[3][k] = fma(w2, gi[k] - g0[k], acc[3][k]);
+            }
+        }
+    }
+    if (bad && c) raise_err(c, stage, kSlotFlux, 2 /*KMF_CTX_FLUX_XP: refined on host*/);
+    if (interior) {
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            double r;
+            if (FAM < 0)
+                r = ADD(ADD(ADD(acc[0][k], acc[1][k]), acc[2][k]), acc[3][k]);
+            else if (FAM == 0)
+                r = acc[0][k];
+            else
+                r = ADD(R[k * ld + i], acc[FAM][k]);
+            R[k * ld + i] = r;
+        }
+    } else if (zero_boundary && FAM <= 0) {
+#pragma unroll
+        for (int k = 0; k < 4; k++) R[k * ld + i] = 0.0;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// solver.py:336-382 apply_boundary: wall / outer frame closures.  One warp
+// per boundary point; lanes stride over the frame edges of tplus, tminus
+// and the one-sided normal family; warp-tree sums (tolerance path).
+__device__ __forceinline__ double warp_sum(double v)
+{
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__global__ void __launch_bounds__(kTB) k_boundary(DG g, DB b, const double *__restrict__ q,
+                                                  const double *__restrict__ G, double *__restrict__ R,
+                                                  double inv_gm1, double c_i0, double fsr, double fsu,
+                                                  double fsv, double fsp, Ctrl *c, int stage)
+{
+    if (c && should_skip(c, stage, kSlotFlux)) return;
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= b.nb) return;  // whole warp leaves together
+    const int ld = g.ld;
+    const int pt = b.point[w];
+    const bool wall = b.type[w] == 1;
+    const double tx = b.frame[w], ty = b.frame[b.nb + w], nx = b.frame[2 * b.nb + w],
+                 ny = b.frame[3 * b.nb + w];
+    double qi[4], gxi[4], gyi[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        qi[k] = q[k * ld + pt];
+        gxi[k] = G[k * ld + pt];
+        gyi[k] = G[(4 + k) * ld + pt];
+    }
+    // free-stream Maxwellian in this point's frame (solver.py:365-369)
+    double gfs[4] = {0, 0, 0, 0};
+    if (!wall) {
+        EState fs;
+        fs.rho = fsr;
+        fs.u1 = ADD(MUL(fsu, tx), MUL(fsv, ty));
+        fs.u2 = ADD(MUL(fsu, nx), MUL(fsv, ny));
+        fs.beta = fsr / (2.0 * fsp);
+        fs.r = __drcp_rn(2.0 * fs.beta);
+        EShared h;
+        shared_of(fs, c_i0, h);
+        sflux(fs, h, true, -1.0, gfs);
+    }
+    double acc[3][4];
+#pragma unroll
+    for (int f = 0; f < 3; f++)
+#pragma unroll
+        for (int k = 0; k < 4; k++) acc[f][k] = 0.0;
+    unsigned badmask = 0;
+#pragma unroll 1
+    for (int f = 0; f < 3; f++) {
+        const int e0 = b.ptr[f][w], e1 = b.ptr[f][w + 1];
+        const double ct = b.coef[(2 * f) * b.nb + w], cn = b.coef[(2 * f + 1) * b.nb + w];
+        for (int e = e0 + lane; e < e1; e += 32) {
+            const int j = b.idx[f][e];
+            const double dt = b.dt[f][e], dn = b.dn[f][e];
+            // solver.py:255-256 global offsets rebuilt from the rotated ones
+            const double dxg = ADD(MUL(dt, tx), MUL(dn, nx));
+            const double dyg = ADD(MUL(dt, ty), MUL(dn, ny));
+            double ti[4], t0[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                ti[k] = qtilde(q[k * ld + j], G[k * ld + j], G[(4 + k) * ld + j], dxg, dyg);
+                t0[k] = qtilde(qi[k], gxi[k], gyi[k], dxg, dyg);
+            }
+            if (!(ti[3] < 0.0) || !(t0[3] < 0.0)) {
+                badmask |= 1u << f;
+                continue;
+            }
+            // _frame_q (solver.py:238-242): rotate the velocity pair
+            EState si, s0;
+            decode(ti[0], ADD(MUL(tx, ti[1]), MUL(ty, ti[2])), ADD(MUL(nx, ti[1]), MUL(ny, ti[2])), ti[3],
+                   inv_gm1, si);
+            decode(t0[0], ADD(MUL(tx, t0[1]), MUL(ty, t0[2])), ADD(MUL(nx, t0[1]), MUL(ny, t0[2])), t0[3],
+                   inv_gm1, s0);
+            EShared hi, h0;
+            shared_of(si, c_i0, hi);
+            shared_of(s0, c_i0, h0);
+            double gi[4], g0[4], dg[4];
+            if (f < 2) {
+                const double sg = f == 0 ? 1.0 : -1.0;
+                sflux(si, hi, false, sg, gi);
+                sflux(s0, h0, false, sg, g0);
+#pragma unroll
+                for (int k = 0; k < 4; k++) dg[k] = gi[k] - g0[k];
+            } else if (wall) {
+                sflux(si, hi, true, -1.0, gi);
+                sflux(s0, h0, true, -1.0, g0);
+#pragma unroll
+                for (int k = 0; k < 4; k++) dg[k] = gi[k] - g0[k];
+            } else {
+                double gm[4];
+                sflux(si, hi, true, 1.0, gi);
+                sflux(s0, h0, true, 1.0, g0);
+                sflux(si, hi, true, -1.0, gm);
+#pragma unroll
+                for (int k = 0; k < 4; k++) dg[k] = (gi[k] - g0[k]) + (gm[k] - gfs[k]);
+            }
+            const double wgt = fma(ct, dt, cn * dn);
+#pragma unroll
+            for (int k = 0; k < 4; k++) acc[f][k] = fma(wgt, dg[k], acc[f][k]);
+        }
+    }
+#pragma unroll
+    for (int f = 0; f < 3; f++)
+#pragma unroll
+        for (int k = 0; k < 4; k++) acc[f][k] = warp_sum(acc[f][k]);
+    unsigned anybad = __reduce_or_sync(0xffffffffu, badmask);
+    if (lane == 0) {
+        if (anybad && c) {
+            if (anybad & 3u) raise_err(c, stage, kSlotFlux, wall ? 6 : 8);
+            if (anybad & 4u) raise_err(c, stage, kSlotFlux, wall ? 7 : 9);
+        }
+        double rows[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            double rt = acc[0][k] + acc[1][k];
+            if (wall)
+                rows[k] = rt + (k == 2 ? 0.0 : 2.0 * acc[2][k]);  // solver.py:303-309
+            else
+                rows[k] = rt + acc[2][k];  // solver.py:322-333
+        }
+        // _rotate_back solver.py:376-382
+        R[pt] = rows[0];
+        R[3 * ld + pt] = rows[3];
+        R[ld + pt] = ADD(MUL(tx, rows[1]), MUL(nx, rows[2]));
+        R[2 * ld + pt] = ADD(MUL(ty, rows[1]), MUL(ny, rows[2]));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// solver.py:385-409 state_update_rk + state.py:99-129 decode (bitwise),
+// fused with primitives_to_q for the next stage (state.py:132-138) and, at
+// stage 4, local_timestep for the next iteration (solver.py:154-159) and the
+// exact residue partial sum (solver.py:412-421).
+template <int STAGE>
+__global__ void __launch_bounds__(kTB) k_update(DG g, double *__restrict__ Uo, double *__restrict__ Us,
+                                                const double *__restrict__ R, double *__restrict__ dt,
+                                                double *__restrict__ q, double gamma, double cfl, Ctrl *c)
+{
+    __shared__ unsigned long long sl[kLimbs];
+    if (should_skip(c, STAGE, kSlotUpdate)) return;
+    if (STAGE == 4) {
+        for (int t = threadIdx.x; t < kLimbs; t += blockDim.x) sl[t] = 0ull;
+        __syncthreads();
+    }
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int ld = g.ld;
+    if (i < g.n) {
+        double uo[4], us[4], un[4];
+        const double d = dt[i];
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            uo[k] = Uo[k * ld + i];
+            us[k] = STAGE == 1 ? uo[k] : Us[k * ld + i];
+            const double r = R[k * ld + i];
+            if (STAGE == 3)
+                un[k] = SUB(ADD(MUL(2.0 / 3.0, uo[k]), MUL(1.0 / 3.0, us[k])), MUL(DIV(d, 6.0), r));
+            else
+                un[k] = SUB(us[k], MUL(MUL(0.5, d), r));
+        }
+        double rho, u1, u2, p;
+        const int fl = u2p(un, gamma, rho, u1, u2, p);
+        if (fl) raise_err(c, STAGE, kSlotUpdate, (fl & 1) ? 10 : 11);
+        double *out = STAGE == 4 ? Uo : Us;
+#pragma unroll
+        for (int k = 0; k < 4; k++) out[k * ld + i] = un[k];
+        double qq[4];
+        p2q(rho, u1, u2, p, gamma, qq);
+#pragma unroll
+        for (int k = 0; k < 4; k++) q[k * ld + i] = qq[k];
+        if (STAGE == 4) {
+            dt[i] = timestep(rho, u1, u2, p, gamma, cfl, g.dmin[i]);
+            const double dr = SUB(un[0], uo[0]);
+            accum_add(sl, MUL(dr, dr));
+        }
+    }
+    if (STAGE == 4) {
+        __syncthreads();
+        for (int t = threadIdx.x; t < kLimbs; t += blockDim.x)
+            if (sl[t]) atomicAdd(&c->limbs[t], sl[t]);
+    }
+}
+
+// 96-bit window of the normalised digit array starting at bit p
+KMF_HD unsigned long long bits64_at(const unsigned int *dg, int nd, int p)
+{
+    int w = p >> 5, sh = p & 31;
+    unsigned long long a = (w < nd && w >= 0) ? dg[w] : 0u;
+    unsigned long long b = (w + 1 < nd && w + 1 >= 0) ? dg[w + 1] : 0u;
+    unsigned long long cc = (w + 2 < nd && w + 2 >= 0) ? dg[w + 2] : 0u;
+    unsigned long long lo = (a >> sh) | (b << (32 - sh));
+    if (sh == 0) lo = a | (b << 32);
+    unsigned long long hi = sh ? (cc << (64 - sh)) : 0ull;
+    return lo | hi;
+}
+
+// Correctly rounded double of the exact limb sum (math.fsum semantics).
+KMF_HD double accum_round(const unsigned long long *limbs)
+{
+    constexpr int nd = kLimbs + 2;
+    unsigned int dg[nd];
+    unsigned long long carry = 0;
+    for (int l = 0; l < kLimbs; l++) {
+        unsigned long long t = limbs[l] + carry;
+        dg[l] = (unsigned int)(t & 0xffffffffull);
+        carry = t >> 32;
+    }
+    dg[kLimbs] = (unsigned int)(carry & 0xffffffffull);
+    dg[kLimbs + 1] = (unsigned int)(carry >> 32);
+    int top = -1;
+    for (int l = nd - 1; l >= 0; l--)
+        if (dg[l]) {
+            top = l;
+            break;
+        }
+    if (top < 0) return 0.0;
+    const int T = top * 32 + (31 - __clz(dg[top]));  // MSB position, unit 2^-1074
+    if (T < 53) {
+        unsigned long long v = (unsigned long long)dg[0] | ((unsigned long long)dg[1] << 32);
+        return scalbn((double)v, -1074);
+    }
+    const int lsb = T - 52;
+    unsigned long long mant = bits64_at(dg, nd, lsb) & ((1ull << 53) - 1);
+    const int rpos = lsb - 1;
+    const unsigned long long rbit = (bits64_at(dg, nd, rpos) & 1ull);
+    bool sticky = false;
+    if (rpos > 0) {
+        const int wfull = rpos >> 5;
+        for (int l = 0; l < wfull && !sticky; l++) sticky = dg[l] != 0;
+        if (!sticky) sticky = (dg[wfull] & ((1u << (rpos & 31)) - 1u)) != 0;
+    }
+    int e = lsb;
+    if (rbit && (sticky || (mant & 1ull))) {
+        mant++;
+        if (mant == (1ull << 53)) {
+            mant >>= 1;
+            e++;
+        }
+    }
+    return scalbn((double)mant, e - 1074);
+}
+
+// residue_norm finish: sqrt(fsum(drho^2)/n) (solver.py:418-421), history,
+// convergence test (solver.py:557-559), advance the iteration counter.
+__global__ void k_finalize(Ctrl *c, int n, double *history, int hist_base, int cap, double tol)
+{
+    if (should_skip(c, kStageFinal, 0)) return;
+    const double total = accum_round(c->limbs);
+    for (int l = 0; l < kLimbs; l++) c->limbs[l] = 0ull;
+    const double res = sqrt(total / (double)n);
+    const int it = c->iter;
+    const int h = it - hist_base;
+    if (h >= 0 && h < cap) history[h] = res;
+    if (tol > 0.0 && res <= tol)
+        c->state = ((unsigned long long)seq_of(it, kStageFinal, 0) << 2) | 2ull;
+    c->iter = it + 1;
+}
+
+// ---------------------------------------------------------------- set/get
+
+// caller-order SoA (4, n) -> device slots; perm == nullptr: identity
+__global__ void k_init(DG g, const double *__restrict__ prims, const long long *__restrict__ perm,
+                       double *__restrict__ Uo, double *__restrict__ q, double *__restrict__ dt,
+                       double gamma, double cfl)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= g.n) return;
+    const long long src = perm ? perm[i] : i;
+    const int n = g.n, ld = g.ld;
+    const double rho = prims[src], u1 = prims[n + src], u2 = prims[2 * n + src], p = prims[3 * n + src];
+    double U[4], qq[4];
+    p2u(rho, u1, u2, p, gamma, U);
+    p2q(rho, u1, u2, p, gamma, qq);
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        Uo[k * ld + i] = U[k];
+        q[k * ld + i] = qq[k];
+    }
+    dt[i] = timestep(rho, u1, u2, p, gamma, cfl, g.dmin[i]);
+}
+
+// continuation of a previous run: q and dt from the current U exactly as
+// the stage-4 update produced them (decode -> p2q / timestep, bitwise)
+__global__ void k_refresh(DG g, const double *__restrict__ Uo, double *__restrict__ q, double *__restrict__ dt,
+                          double gamma, double cfl)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= g.n) return;
+    const int ld = g.ld;
+    double u[4], qq[4], rho, u1, u2, p;
+#pragma unroll
+    for (int k = 0; k < 4; k++) u[k] = Uo[k * ld + i];
+    u2p(u, gamma, rho, u1, u2, p);
+    p2q(rho, u1, u2, p, gamma, qq);
+#pragma unroll
+    for (int k = 0; k < 4; k++) q[k * ld + i] = qq[k];
+    dt[i] = timestep(rho, u1, u2, p, gamma, cfl, g.dmin[i]);
+}
+
+__global__ void k_get_state(DG g, const double *__restrict__ Uo, const long long *__restrict__ perm,
+                            double gamma, double *__restrict__ prims, double *__restrict__ U)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= g.n) return;
+    const long long dst = perm ? perm[i] : i;
+    const int n = g.n, ld = g.ld;
+    double u[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) u[k] = Uo[k * ld + i];
+    double rho, u1, u2, p;
+    u2p(u, gamma, rho, u1, u2, p);
+    if (prims) {
+        prims[dst] = rho;
+        prims[n + dst] = u1;
+        prims[2 * n + dst] = u2;
+        prims[3 * n + dst] = p;
+    }
+    if (U)
+#pragma unroll
+        for (int k = 0; k < 4; k++) U[k * n + dst] = u[k];
+}
+
+// device slots <-> caller order for (nc, n) SoA fields
+__global__ void k_to_dev(int n, int ld, int nc, const double *__restrict__ src, const long long *__restrict__ perm,
+                         double *__restrict__ dst)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const long long s = perm ? perm[i] : i;
+    for (int k = 0; k < nc; k++) dst[k * ld + i] = src[(long long)k * n + s];
+}
+
+__global__ void k_from_dev(int n, int ld, int nc, const double *__restrict__ src, const long long *__restrict__ perm,
+                           double *__restrict__ dst)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const long long s = perm ? perm[i] : i;
+    for (int k = 0; k < nc; k++) dst[(long long)k * n + s] = src[k * ld + i];
+}
+
+// --------------------------------------------------------------- diagnostics
+
+// per caller-CSR edge: bit0 q~4 >= 0 at either end, bit1 NaN q~4 at the
+// neighbour end, bit2 NaN q~4 at the owner end (solver.py:164-171)
+template <bool XY>
+__global__ void k_diag_flux(DG g, const double *__restrict__ q, const double *__restrict__ G,
+                            unsigned char *__restrict__ out)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= g.n) return;
+    const int ld = g.ld;
+    const double xi = g.x[i], yi = g.y[i];
+    const int base = ell_base(g, i), d = g.deg[i];
+    const long long e0 = g.cptr[i];
+    for (int s = 0; s < d; s++) {
+        const int ent = base + s * 32;
+        const int j = g.eidx[ent];
+        double dx, dy;
+        edge_offsets<XY>(g, ent, j, xi, yi, dx, dy);
+        double ti = qtilde(q[3 * ld + j], G[3 * ld + j], G[7 * ld + j], dx, dy);
+        double t0 = qtilde(q[3 * ld + i], G[3 * ld + i], G[7 * ld + i], dx, dy);
+        unsigned char f = 0;
+        if (ti >= 0.0 || t0 >= 0.0) f |= 1;
+        if (isnan(ti)) f |= 2;
+        if (isnan(t0)) f |= 4;
+        out[e0 + s] = f;
+    }
+}
+
+// per frame edge (all three families, concatenated): bit0 q~4 >= 0
+__global__ void k_diag_frame(DG g, DB b, int fam, const double *__restrict__ q, const double *__restrict__ G,
+                             unsigned char *__restrict__ out)
+{
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= b.nb) return;
+    const int ld = g.ld, pt = b.point[w];
+    const double tx = b.frame[w], ty = b.frame[b.nb + w], nx = b.frame[2 * b.nb + w],
+                 ny = b.frame[3 * b.nb + w];
+    for (int e = b.ptr[fam][w]; e < b.ptr[fam][w + 1]; e++) {
+        const int j = b.idx[fam][e];
+        const double dt = b.dt[fam][e], dn = b.dn[fam][e];
+        const double dxg = ADD(MUL(dt, tx), MUL(dn, nx));
+        const double dyg = ADD(MUL(dt, ty), MUL(dn, ny));
+        double ti = qtilde(q[3 * ld + j], G[3 * ld + j], G[7 * ld + j], dxg, dyg);
+        double t0 = qtilde(q[3 * ld + pt], G[3 * ld + pt], G[7 * ld + pt], dxg, dyg);
+        out[e] = (ti >= 0.0 || t0 >= 0.0) ? 1 : 0;
+    }
+}
+
+// ------------------------------------------------------- point operators
+// Context-free (n,) / (4,n) kernels for the stage-operator API.
+
+__global__ void k_op_p2q(int n, const double *pr, double gamma, double *q, unsigned char *fl)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double rho = pr[i], u1 = pr[n + i], u2 = pr[2 * n + i], p = pr[3 * n + i];
+    fl[i] = !((rho > 0.0) && (p > 0.0));
+    double qq[4];
+    p2q(rho, u1, u2, p, gamma, qq);
+    for (int k = 0; k < 4; k++) q[(long long)k * n + i] = qq[k];
+}
+
+__global__ void k_op_q2p(int n, const double *q, double gamma, double *pr, unsigned char *fl)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double qq[4] = {q[i], q[n + i], q[2 * n + i], q[3 * n + i]};
+    fl[i] = !(qq[3] < 0.0);
+    double rho, u1, u2, p;
+    q2p_ref(qq, gamma, rho, u1, u2, p);
+    pr[i] = rho;
+    pr[n + i] = u1;
+    pr[2 * n + i] = u2;
+    pr[3 * n + i] = p;
+}
+
+__global__ void k_op_p2u(int n, const double *pr, double gamma, double *U, unsigned char *fl)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double rho = pr[i], u1 = pr[n + i], u2 = pr[2 * n + i], p = pr[3 * n + i];
+    fl[i] = !((rho > 0.0) && (p > 0.0));
+    double u[4];
+    p2u(rho, u1, u2, p, gamma, u);
+    for (int k = 0; k < 4; k++) U[(long long)k * n + i] = u[k];
+}
+
+__global__ void k_op_u2p(int n, const double *U, double gamma, double *pr, unsigned char *fl)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double u[4] = {U[i], U[n + i], U[2 * n + i], U[3 * n + i]};
+    double rho, u1, u2, p;
+    fl[i] = (unsigned char)u2p(u, gamma, rho, u1, u2, p);
+    pr[i] = rho;
+    pr[n + i] = u1;
+    pr[2 * n + i] = u2;
+    pr[3 * n + i] = p;
+}
+
+// kinetics.py:71-106 through the same device split flux the solver uses
+// (state primitives -> beta = rho/(2p) as the reference recomputes it)
+__global__ void k_op_split_flux(int n, const double *pr, int yaxis, double sg, double gamma, double *G)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    EState s;
+    s.rho = pr[i];
+    s.u1 = pr[n + i];
+    s.u2 = pr[2 * n + i];
+    const double p = pr[3 * n + i];
+    s.beta = s.rho / (2.0 * p);
+    s.r = __drcp_rn(2.0 * s.beta);
+    EShared h;
+    shared_of(s, (2.0 - gamma) / (gamma - 1.0), h);
+    double g[4];
+    sflux(s, h, yaxis != 0, sg, g);
+    for (int k = 0; k < 4; k++) G[(long long)k * n + i] = g[k];
+}
+
+// kinetics.py:59-68
+__global__ void k_op_full_flux(int n, const double *pr, int yaxis, double gamma, double *F)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double rho = pr[i], u1 = pr[n + i], u2 = pr[2 * n + i], p = pr[3 * n + i];
+    const double e = ADD(DIV(p, MUL(rho, SUB(gamma, 1.0))), MUL(0.5, ADD(MUL(u1, u1), MUL(u2, u2))));
+    const double h = ADD(p, MUL(rho, e));
+    double f[4];
+    if (!yaxis) {
+        f[0] = MUL(rho, u1);
+        f[1] = ADD(p, MUL(MUL(rho, u1), u1));
+        f[2] = MUL(MUL(rho, u1), u2);
+        f[3] = MUL(h, u1);
+    } else {
+        f[0] = MUL(rho, u2);
+        f[1] = MUL(MUL(rho, u1), u2);
+        f[2] = ADD(p, MUL(MUL(rho, u2), u2));
+        f[3] = MUL(h, u2);
+    }
+    for (int k = 0; k < 4; k++) F[(long long)k * n + i] = f[k];
+}
+
+__global__ void k_op_update(int n, const double *Uo, const double *Us, int stage, const double *dt,
+                            const double *R, double *Un)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double d = dt[i];
+    for (int k = 0; k < 4; k++) {
+        const long long x = (long long)k * n + i;
+        if (stage == 3)
+            Un[x] = SUB(ADD(MUL(2.0 / 3.0, Uo[x]), MUL(1.0 / 3.0, Us[x])), MUL(DIV(d, 6.0), R[x]));
+        else
+            Un[x] = SUB(Us[x], MUL(MUL(0.5, d), R[x]));
+    }
+}
+
+__global__ void k_op_residue(int n, const double *Un, const double *Uold, unsigned long long *limbs)
+{
+    __shared__ unsigned long long sl[kLimbs];
+    for (int t = threadIdx.x; t < kLimbs; t += blockDim.x) sl[t] = 0ull;
+    __syncthreads();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        const double d = SUB(Un[i], Uold[i]);
+        accum_add(sl, MUL(d, d));
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < kLimbs; t += blockDim.x)
+        if (sl[t]) atomicAdd(&limbs[t], sl[t]);
+}
+
+__global__ void k_op_residue_fin(int n, const unsigned long long *limbs, double *out)
+{
+    *out = sqrt(accum_round(limbs) / (double)n);
+}
+
+__global__ void k_op_timestep(DG g, const double *__restrict__ pr_dev, double cfl, double gamma,
+                              double *__restrict__ dt_dev)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= g.n) return;
+    const int ld = g.ld;
+    dt_dev[i] = timestep(pr_dev[i], pr_dev[ld + i], pr_dev[2 * ld + i], pr_dev[3 * ld + i], gamma, cfl,
+                         g.dmin[i]);
+}
+
+}  // namespace kmf

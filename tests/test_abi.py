@@ -1,0 +1,70 @@
+"""The C-ABI library loads and exports every entry point include/kmf_b200.h
+declares; without a GPU every product operation fails loudly (no CPU
+fallback).  CPU only (no compute calls)."""
+
+import ctypes
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+from paper_2108_07031_b200 import _lib
+
+
+def declared_functions():
+    text = (ROOT / "include" / "kmf_b200.h").read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(kmf_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_and_binding_agree():
+    declared = declared_functions()
+    assert len(declared) >= 25
+    assert set(declared) == set(_lib.EXPORTED)
+
+
+def test_library_exports_every_symbol():
+    so = ctypes.CDLL(str(_lib.LIB_PATH))
+    for name in declared_functions():
+        assert hasattr(so, name), name
+
+
+def test_abi_version():
+    assert _lib.lib().kmf_abi_version() == 1
+
+
+def test_structs_match_header_sizes():
+    # kmf_stencil: 2 int64 + 8 pointers; kmf_frame: int64 + 5 pointers + 3 stencils
+    assert ctypes.sizeof(_lib.Stencil) == 2 * 8 + 8 * 8
+    assert ctypes.sizeof(_lib.Frame) == 8 + 5 * 8 + 3 * ctypes.sizeof(_lib.Stencil)
+
+
+def _no_gpu():
+    return _lib.lib().kmf_device_count() == 0
+
+
+@pytest.mark.skipif(not _no_gpu(), reason="checks the no-GPU behaviour")
+def test_no_silent_cpu_fallback(small_naca, small_naca_conn):
+    from paper_2108_07031_b200 import primitives_to_q, free_stream, solve, SolverConfig
+
+    prims = free_stream(0.63, 2.0, n=10)
+    with pytest.raises(_lib.DeviceError):
+        primitives_to_q(prims)
+    with pytest.raises(_lib.DeviceError):
+        solve(SolverConfig(mach=0.63, n_outer=1), small_naca, small_naca_conn)
+
+
+def test_oracle_library_builds_and_is_separate():
+    from oracle import oracle as O
+
+    O.lib()
+    # the product library must not depend on the oracle
+    so = (ROOT / "paper_2108_07031_b200" / "libkmf_b200.so").read_bytes()
+    assert b"orc_" not in so and b"kmf_oracle" not in so
+    import paper_2108_07031_b200 as pkg
+
+    for mod in ("solver", "lsq", "state", "kinetics", "geometry", "_device", "_lib"):
+        src = (ROOT / "paper_2108_07031_b200" / f"{mod}.py").read_text()
+        assert not re.search(r"^\s*(from|import)\s+oracle", src, flags=re.M), mod
+    assert pkg.__version__

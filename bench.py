@@ -1,0 +1,349 @@
+#!/usr/bin/env python
+"""Benchmark: q-LSKUM outer iterations on B200 (driver contract, one JSON line).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
+
+A step is one outer iteration of the solver (local time step + 4 SSP-RK
+stages of q-variables, q-derivatives with 3 inner sweeps, flux residual with
+wall/outer closures, state update + exact residue) over the whole synthetic
+NACA 0012 cloud.  The default workload is BASELINE.json configs[1]:
+160,000 points, M 0.63, AoA 2 deg, second order, n_inner 3, fused.
+
+Reported (ours):
+  value          point-iterations/s with the state resident in HBM, each step
+                 one CUDA-graph launch timed by CUDA events on the solver
+                 stream, L2 flushed (256 MiB memset) between timed steps;
+  e2e            the same metric through the C ABI with host buffers: per
+                 step kmf_set_state (pinned H2D of the primitives) +
+                 kmf_run(1) + kmf_get_state (D2H primitives + residue);
+  roofline       flux_residual interior kernel (the dominant kernel) against
+                 HBM (MEASURED_PEAKS.json) -- it is FP64-bound, so
+                 roofline_fp64 reports it against the FP64 pipe peak measured
+                 in the same run (DFMA probe);
+  cpu_baseline   the CPU oracle (C restatement of the reference, OpenMP over
+                 all host cores) on a bounded 2-iteration sample.
+``--impl reference`` times that CPU oracle alone on the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    # name: (chord_points, layers, growth, mach, aoa, description)
+    "c1": (400, 100, 1.06, 0.63, 2.0, "NACA0012 40K (400x100, g=1.06) M0.63 AoA2 second order"),
+    "c2": (800, 200, 1.03, 0.63, 2.0, "NACA0012 160K (800x200, g=1.03) M0.63 AoA2 second order n_inner=3"),
+    "c3": (3160, 790, 1.00734, 0.85, 1.0, "NACA0012 2.5M (3160x790, g=1.00734) M0.85 AoA1 second order"),
+}
+METRIC = "point-iterations/sec (RDP = 1/value s/point/iter), NACA0012 q-LSKUM"
+UNIT = "point-iterations/s"
+# algorithmic work of flux_residual interior per point-stage
+FLUX_BYTES_PER_POINT = 337
+FLUX_DP_OPS_PER_POINT = 13214
+L2_FLUSH_BYTES = 256 << 20
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def dist_init(ws):
+    if ws <= 1:
+        return None
+    import torch.distributed as dist
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    dist.init_process_group("gloo")
+    return dist
+
+
+def allreduce_max(dist, v: float) -> float:
+    if dist is None:
+        return v
+    import torch
+
+    t = torch.tensor([v], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+def setup(name):
+    from paper_2108_07031_b200 import SolverConfig, build_stencils, generate_naca_cloud, initial_primitives
+
+    m, L, g, mach, aoa, _ = CONFIGS[name]
+    cloud = generate_naca_cloud(m, L, g, 20.0)
+    conn = build_stencils(cloud)
+    cfg = SolverConfig(mach=mach, aoa_deg=aoa, cfl=0.2, n_inner=3, mode="fused")
+    return cloud, conn, cfg, initial_primitives(cfg, cloud)
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.2)
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        if not self.path or not os.path.exists(self.path):
+            return None
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.path)
+        if not sm:
+            return None
+        busy = [s for s in sm if s > 400] or sm
+        return {"sm_mhz": statistics.median(busy), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_baseline(conn, cfg, init, target_s=12.0):
+    """Oracle (CPU restatement of the reference) on a bounded sample of
+    ~target_s seconds of whole outer iterations."""
+    from oracle import oracle as O
+    from paper_2108_07031_b200 import free_stream
+
+    threads = os.cpu_count() or 1
+    O.set_threads(threads)
+    pk = O.Packed(conn)
+    fs = free_stream(cfg.mach, cfg.aoa_deg, cfg.gamma)
+    fsv = [fs.rho[0], fs.u1[0], fs.u2[0], fs.p[0]]
+    t = time.perf_counter()
+    O.solve(pk, init.as_array(), fsv, 1, gamma=cfg.gamma, cfl=cfg.cfl, n_inner=cfg.n_inner)
+    one = time.perf_counter() - t
+    iters = int(min(200, max(2, target_s / max(one, 1e-3))))
+    t = time.perf_counter()
+    O.solve(pk, init.as_array(), fsv, iters, gamma=cfg.gamma, cfl=cfg.cfl, n_inner=cfg.n_inner)
+    sec = time.perf_counter() - t
+    n = conn.cloud.n_points
+    return {"value": n * iters / sec, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{iters} full outer iterations of the same {n}-point workload ({sec:.1f} s), "
+                      f"oracle/kmf_oracle.c with OpenMP over {threads} threads"}
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return json.loads(p.read_text()), "measured"
+    return {"hbm_gbs": 6650.0}, "fallback"
+
+
+def run_ours(args):
+    ws, rank, local = dist_env()
+    dist = dist_init(ws)
+    from paper_2108_07031_b200 import _lib
+    from paper_2108_07031_b200._device import DeviceConnectivity
+    from paper_2108_07031_b200.solver import _params
+    import ctypes as C
+
+    L = _lib.lib()
+    _lib.require_device()
+    cloud, conn, cfg, init = setup(args.config)
+    n = cloud.n_points
+    dev = DeviceConnectivity(conn, device=local)
+    params = _params(cfg)
+    peak_fp64 = C.c_double(0.0)
+    _lib.check(L.kmf_fp64_peak(C.byref(peak_fp64)), "kmf_fp64_peak")
+
+    # ---- device-resident value --------------------------------------------
+    dev.set_state(init.as_array())
+    W, K = max(args.warmup, 0), args.steps
+    step_ms = np.zeros(max(K, W, 1))
+    flux_ms = np.zeros_like(step_ms)
+    lps = C.c_int(0)
+    if W:
+        _lib.check(L.kmf_bench_steps(dev.handle, C.byref(params), W, L2_FLUSH_BYTES, _lib.dptr(step_ms),
+                                     _lib.dptr(flux_ms), C.byref(lps)), "warm-up")
+    barrier(dist)
+    with Clocks(local) as clk:
+        _lib.check(L.kmf_bench_steps(dev.handle, C.byref(params), K, L2_FLUSH_BYTES, _lib.dptr(step_ms),
+                                     _lib.dptr(flux_ms), C.byref(lps)), "timed steps")
+    barrier(dist)
+    total_s = allreduce_max(dist, float(step_ms[:K].sum()) * 1e-3)
+    value = n * K * ws / total_s
+    flux_launch_s = float(flux_ms[:K].sum()) * 1e-3 / (4 * K)
+    stage_share = float(flux_ms[:K].sum() / step_ms[:K].sum())
+
+    # ---- end to end through the C ABI with pinned host buffers ------------
+    host_in = _lib.pinned((4, n))
+    host_out = _lib.pinned((4, n))
+    host_in[...] = init.as_array()
+    hist = np.zeros(1)
+    done, conv = C.c_int(0), C.c_int(0)
+    e2e_params = _params(cfg)
+
+    def e2e_step():
+        _lib.check(L.kmf_set_state(dev.handle, _lib.dptr(host_in)), "set_state")
+        _lib.check(L.kmf_run(dev.handle, C.byref(e2e_params), 1, _lib.dptr(hist), C.byref(done), C.byref(conv)),
+                   "run")
+        _lib.check(L.kmf_get_state(dev.handle, _lib.dptr(host_out), None), "get_state")
+
+    for _ in range(max(W, 1)):
+        e2e_step()
+    barrier(dist)
+    t0 = time.perf_counter()
+    for _ in range(K):
+        e2e_step()
+    e2e_s = allreduce_max(dist, time.perf_counter() - t0)
+    e2e = {"value": n * K * ws / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 4 * n * 8,
+           "d2h_bytes_per_step": 4 * n * 8 + 8, "ms_per_step": 1e3 * e2e_s / K,
+           "path": "kmf_set_state(pinned) + kmf_run(1 iteration) + kmf_get_state(pinned)"}
+
+    if rank != 0:
+        return
+    peaks, peak_kind = measured_peaks()
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    achieved_gbs = FLUX_BYTES_PER_POINT * n / flux_launch_s / 1e9
+    dfma_rate = peak_fp64.value / 2.0  # DP-pipe instructions/s (TFLOP/s / 2)
+    achieved_ops = FLUX_DP_OPS_PER_POINT * n / flux_launch_s / 1e12
+    traffic = None
+    tf = ROOT / "profiles" / f"flux_traffic_{args.config}.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch")
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": ws,
+        "steps": K,
+        "warmup": W,
+        "ms_per_step": 1e3 * total_s / K,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (procedurally generated NACA 0012 O-cloud, reference generator restated bit-exactly)",
+        "config": {"workload": CONFIGS[args.config][5], "config_key": args.config, "n_points": n,
+                   "n_edges": int(conn.full.idx.size), "n_inner": cfg.n_inner, "mode": cfg.mode,
+                   "l2": "flushed between timed steps (256 MiB memset on the solver stream)",
+                   "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"},
+        "rdp_s_per_point_iter": 1.0 / (value / ws),
+        "e2e": e2e,
+        "gpu_launches": int(lps.value) * K,
+        "roofline": {"bound": "hbm", "kernel": "k_flux<fused> (flux_residual interior)",
+                     "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": achieved_gbs / hbm_peak,
+                     "traffic": traffic, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+                     "bytes_per_point": FLUX_BYTES_PER_POINT, "launch_us": flux_launch_s * 1e6,
+                     "share_of_step": stage_share,
+                     "note": "the flux kernel is FP64-pipe bound (SURVEY.md 8(d)); see roofline_fp64"},
+        "roofline_fp64": {"bound": "fp64", "achieved": achieved_ops, "peak": dfma_rate,
+                          "unit": "T DP-pipe ops/s", "frac": achieved_ops / dfma_rate,
+                          "ops_per_point": FLUX_DP_OPS_PER_POINT,
+                          "peak_source": f"DFMA probe in this run: {peak_fp64.value:.2f} TFLOP/s"},
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline and ws == 1:
+        line["cpu_baseline"] = cpu_baseline(conn, cfg, init)
+    print(json.dumps(line), flush=True)
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    from paper_2108_07031_b200 import free_stream
+
+    cloud, conn, cfg, init = setup(args.config)
+    n = cloud.n_points
+    threads = os.cpu_count() or 1
+    O.set_threads(threads)
+    pk = O.Packed(conn)
+    fs = free_stream(cfg.mach, cfg.aoa_deg, cfg.gamma)
+    fsv = [fs.rho[0], fs.u1[0], fs.u2[0], fs.p[0]]
+    W, K = max(args.warmup, 0), args.steps
+    prims = init.as_array()
+    if W:
+        _, prims, _, _, _ = O.solve(pk, prims, fsv, W, gamma=cfg.gamma, cfl=cfg.cfl, n_inner=cfg.n_inner)
+    t = time.perf_counter()
+    O.solve(pk, prims, fsv, K, gamma=cfg.gamma, cfl=cfg.cfl, n_inner=cfg.n_inner)
+    sec = time.perf_counter() - t
+    value = n * K / sec
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": W,
+        "ms_per_step": 1e3 * sec / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (procedurally generated NACA 0012 O-cloud)",
+        "config": {"workload": CONFIGS[args.config][5], "config_key": args.config, "n_points": n},
+        "rdp_s_per_point_iter": 1.0 / value,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{K} timed outer iterations after {W} warm-up, full {n}-point workload; the "
+                                   "reference is pure Python (numpy), so its restatement oracle/kmf_oracle.c "
+                                   "is timed"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", choices=tuple(CONFIGS), default="c2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -214,6 +214,20 @@ int kmf_op_residue(int64_t n, const double *U_new, const double *U_old, double *
 /* last global (context-free) error string */
 const char *kmf_strerror(void);
 
+/* ---- measurement support (bench.py) -------------------------------------- */
+
+/* n_steps outer iterations, each one CUDA-graph launch bracketed by CUDA
+ * events on the context stream (step_ms[i]); a flush_bytes memset between
+ * steps evicts L2 outside the timed region; flux_ms[i] sums the four
+ * interior flux_residual launches of step i, timed on their own stream. */
+int kmf_bench_steps(kmf_ctx *ctx, const kmf_params *p, int n_steps, int64_t flush_bytes, double *step_ms,
+                    double *flux_ms, int *launches_per_step);
+/* measured FP64 (DFMA) pipe peak of the current device, TFLOP/s */
+int kmf_fp64_peak(double *tflops);
+/* pinned host memory for host-buffer (end-to-end) transfers */
+void *kmf_host_alloc(int64_t bytes);
+void kmf_host_free(void *p);
+
 #ifdef __cplusplus
 }
 #endif

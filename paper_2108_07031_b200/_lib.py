@@ -114,6 +114,10 @@ def lib():
         "kmf_op_full_flux": (C.c_int, [C.c_int64, _dp, C.c_int, C.c_double, _dp]),
         "kmf_op_state_update": (C.c_int, [C.c_int64, _dp, _dp, C.c_int, _dp, _dp, _dp]),
         "kmf_op_residue": (C.c_int, [C.c_int64, _dp, _dp, _dp]),
+        "kmf_bench_steps": (C.c_int, [vp, C.POINTER(Params), C.c_int, C.c_int64, _dp, _dp, C.POINTER(C.c_int)]),
+        "kmf_fp64_peak": (C.c_int, [_dp]),
+        "kmf_host_alloc": (C.c_void_p, [C.c_int64]),
+        "kmf_host_free": (None, [C.c_void_p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -130,8 +134,25 @@ EXPORTED = (
     "kmf_op_timestep", "kmf_op_first_order", "kmf_op_q_derivatives", "kmf_op_flux_residual",
     "kmf_op_boundary", "kmf_op_primitives_to_q", "kmf_op_q_to_primitives",
     "kmf_op_primitives_to_conserved", "kmf_op_conserved_to_primitives", "kmf_op_split_flux",
-    "kmf_op_full_flux", "kmf_op_state_update", "kmf_op_residue",
+    "kmf_op_full_flux", "kmf_op_state_update", "kmf_op_residue", "kmf_bench_steps", "kmf_fp64_peak",
+    "kmf_host_alloc", "kmf_host_free",
 )
+
+
+def pinned(shape, dtype=np.float64):
+    """numpy view of pinned (page-locked) host memory; freed with the array."""
+    count = int(np.prod(shape))
+    nbytes = count * np.dtype(dtype).itemsize
+    L = lib()
+    ptr = L.kmf_host_alloc(nbytes)
+    if not ptr:
+        raise DeviceError("kmf_host_alloc failed")
+    buf = (C.c_char * nbytes).from_address(ptr)
+    arr = np.frombuffer(buf, dtype=dtype, count=count).reshape(shape)
+    import weakref
+
+    weakref.finalize(buf, L.kmf_host_free, ptr)  # arr.base keeps buf alive
+    return arr
 
 
 class DeviceError(RuntimeError):

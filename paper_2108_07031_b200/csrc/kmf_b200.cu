@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -81,6 +82,8 @@ struct kmf_ctx {
     int device = 0;
     int n = 0, ld = 0;
     bool xy = true;  // offsets recomputed from coordinates
+    int qg_nc = 2;   // q-gradient components per thread (KMF_QG_NC)
+    int flux_minb = 4;  // interior flux kernel blocks per SM (KMF_FLUX_MINB)
     bool has_perm = false;
     cudaStream_t s0 = nullptr, s1 = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
@@ -113,7 +116,12 @@ struct kmf_ctx {
 
     // instrumentation
     double stage_sec[6] = {0, 0, 0, 0, 0, 0};
-    cudaEvent_t ev[8] = {};
+    cudaEvent_t ev[18] = {};
+    cudaEvent_t evb[8] = {};   // bench: around the 4 interior flux launches
+    cudaEvent_t evs[2] = {};   // bench: around one step
+    cudaGraphExec_t execB = nullptr;
+    GraphKey keyB{};
+    DBuf<unsigned char> flush;
 
     // last error
     kmf_error_info err{};
@@ -159,7 +167,12 @@ struct kmf_ctx {
     {
         if (exec1) cudaGraphExecDestroy(exec1);
         if (execU) cudaGraphExecDestroy(execU);
+        if (execB) cudaGraphExecDestroy(execB);
         for (auto &e : ev)
+            if (e) cudaEventDestroy(e);
+        for (auto &e : evb)
+            if (e) cudaEventDestroy(e);
+        for (auto &e : evs)
             if (e) cudaEventDestroy(e);
         if (fork) cudaEventDestroy(fork);
         if (join) cudaEventDestroy(join);
@@ -444,60 +457,99 @@ int build_context(kmf_ctx *c, const kmf_geometry *g)
     CK(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
     for (auto &e : c->ev) CK(cudaEventCreate(&e));
+    for (auto &e : c->evb) CK(cudaEventCreate(&e));
+    for (auto &e : c->evs) CK(cudaEventCreate(&e));
     return KMF_OK;
 }
 
 // ------------------------------------------------------------ stage launch
 
+template <bool XY, int NC>
+void launch_fo_t(kmf_ctx *c, cudaStream_t s, double *G, Ctrl *ctl, int stage)
+{
+    const int nb = nblk(c->n, qg_points_per_block<NC>());
+    k_first_order<XY, NC><<<nb, kTB, 0, s>>>(c->dg(), c->q.p, G, ctl, stage);
+}
+
+template <bool XY, int NC>
+void launch_sw_t(kmf_ctx *c, cudaStream_t s, const double *Gin, double *Gout, Ctrl *ctl, int stage, int slot,
+                 int want_res)
+{
+    const int nb = nblk(c->n, qg_points_per_block<NC>());
+    k_sweep<XY, NC><<<nb, kTB, 0, s>>>(c->dg(), c->q.p, Gin, Gout, ctl, stage, slot, want_res);
+}
+
+// components per thread of the q-gradient kernels (KMF_QG_NC = 1, 2 or 4)
+void launch_first_order(kmf_ctx *c, cudaStream_t s, double *G, Ctrl *ctl, int stage)
+{
+    switch ((c->xy ? 8 : 0) + c->qg_nc) {
+    case 9: launch_fo_t<true, 1>(c, s, G, ctl, stage); break;
+    case 10: launch_fo_t<true, 2>(c, s, G, ctl, stage); break;
+    case 12: launch_fo_t<true, 4>(c, s, G, ctl, stage); break;
+    case 1: launch_fo_t<false, 1>(c, s, G, ctl, stage); break;
+    case 2: launch_fo_t<false, 2>(c, s, G, ctl, stage); break;
+    default: launch_fo_t<false, 4>(c, s, G, ctl, stage); break;
+    }
+}
+
+void launch_sweep(kmf_ctx *c, cudaStream_t s, const double *Gin, double *Gout, Ctrl *ctl, int stage, int slot,
+                  int want_res)
+{
+    switch ((c->xy ? 8 : 0) + c->qg_nc) {
+    case 9: launch_sw_t<true, 1>(c, s, Gin, Gout, ctl, stage, slot, want_res); break;
+    case 10: launch_sw_t<true, 2>(c, s, Gin, Gout, ctl, stage, slot, want_res); break;
+    case 12: launch_sw_t<true, 4>(c, s, Gin, Gout, ctl, stage, slot, want_res); break;
+    case 1: launch_sw_t<false, 1>(c, s, Gin, Gout, ctl, stage, slot, want_res); break;
+    case 2: launch_sw_t<false, 2>(c, s, Gin, Gout, ctl, stage, slot, want_res); break;
+    default: launch_sw_t<false, 4>(c, s, Gin, Gout, ctl, stage, slot, want_res); break;
+    }
+}
+
 // q-derivatives of one stage: first order into GA, sweeps ping-pong;
 // returns the buffer holding the result (0 = GA, 1 = GB).
-int launch_qgrad(kmf_ctx *c, cudaStream_t s, int stage, int n_inner, Ctrl *ctl, int want_res,
-                 double *res_host_dev_unused = nullptr)
+int launch_qgrad(kmf_ctx *c, cudaStream_t s, int stage, int n_inner, Ctrl *ctl, int want_res)
 {
-    (void)res_host_dev_unused;
-    DG g = c->dg();
-    const int nb = nblk(c->n);
-    if (c->xy)
-        k_first_order<true><<<nb, kTB, 0, s>>>(g, c->q.p, c->GA.p, ctl, stage);
-    else
-        k_first_order<false><<<nb, kTB, 0, s>>>(g, c->q.p, c->GA.p, ctl, stage);
+    launch_first_order(c, s, c->GA.p, ctl, stage);
     double *cur = c->GA.p, *nxt = c->GB.p;
     int which = 0;
     for (int it = 0; it < n_inner; it++) {
-        if (c->xy)
-            k_sweep<true><<<nb, kTB, 0, s>>>(g, c->q.p, cur, nxt, ctl, stage, 1 + it, want_res);
-        else
-            k_sweep<false><<<nb, kTB, 0, s>>>(g, c->q.p, cur, nxt, ctl, stage, 1 + it, want_res);
+        launch_sweep(c, s, cur, nxt, ctl, stage, 1 + it, want_res);
         std::swap(cur, nxt);
         which ^= 1;
     }
     return which;
 }
 
-template <bool XY>
-void launch_flux_xy(kmf_ctx *c, cudaStream_t s, const double *G, int mode, double gamma, int zero_bnd,
-                    Ctrl *ctl, int stage)
+template <bool XY, int MINB>
+void launch_flux_t(kmf_ctx *c, cudaStream_t s, const double *G, int mode, double gamma, int zero_bnd, Ctrl *ctl,
+                   int stage)
 {
     DG g = c->dg();
     const int nb = nblk(c->n);
     const double inv_gm1 = 1.0 / (gamma - 1.0), c_i0 = (2.0 - gamma) / (gamma - 1.0);
     if (mode == 0) {
-        k_flux<XY, -1><<<nb, kTB, 0, s>>>(g, c->q.p, G, c->R.p, inv_gm1, c_i0, zero_bnd, ctl, stage);
+        k_flux<XY, -1, MINB><<<nb, kTB, 0, s>>>(g, c->q.p, G, c->R.p, inv_gm1, c_i0, zero_bnd, ctl, stage);
     } else {
-        k_flux<XY, 0><<<nb, kTB, 0, s>>>(g, c->q.p, G, c->R.p, inv_gm1, c_i0, zero_bnd, ctl, stage);
-        k_flux<XY, 1><<<nb, kTB, 0, s>>>(g, c->q.p, G, c->R.p, inv_gm1, c_i0, zero_bnd, ctl, stage);
-        k_flux<XY, 2><<<nb, kTB, 0, s>>>(g, c->q.p, G, c->R.p, inv_gm1, c_i0, zero_bnd, ctl, stage);
-        k_flux<XY, 3><<<nb, kTB, 0, s>>>(g, c->q.p, G, c->R.p, inv_gm1, c_i0, zero_bnd, ctl, stage);
+        k_flux<XY, 0, MINB><<<nb, kTB, 0, s>>>(g, c->q.p, G, c->R.p, inv_gm1, c_i0, zero_bnd, ctl, stage);
+        k_flux<XY, 1, MINB><<<nb, kTB, 0, s>>>(g, c->q.p, G, c->R.p, inv_gm1, c_i0, zero_bnd, ctl, stage);
+        k_flux<XY, 2, MINB><<<nb, kTB, 0, s>>>(g, c->q.p, G, c->R.p, inv_gm1, c_i0, zero_bnd, ctl, stage);
+        k_flux<XY, 3, MINB><<<nb, kTB, 0, s>>>(g, c->q.p, G, c->R.p, inv_gm1, c_i0, zero_bnd, ctl, stage);
     }
 }
 
+// occupancy of the interior flux kernel: KMF_FLUX_MINB = 3 (<=168 regs) or
+// 4 (<=128 regs) resident 128-thread blocks per SM
 void launch_flux(kmf_ctx *c, cudaStream_t s, const double *G, int mode, double gamma, int zero_bnd, Ctrl *ctl,
                  int stage)
 {
-    if (c->xy)
-        launch_flux_xy<true>(c, s, G, mode, gamma, zero_bnd, ctl, stage);
-    else
-        launch_flux_xy<false>(c, s, G, mode, gamma, zero_bnd, ctl, stage);
+    const bool m4 = c->flux_minb == 4;
+    if (c->xy) {
+        if (m4) launch_flux_t<true, 4>(c, s, G, mode, gamma, zero_bnd, ctl, stage);
+        else launch_flux_t<true, 3>(c, s, G, mode, gamma, zero_bnd, ctl, stage);
+    } else {
+        if (m4) launch_flux_t<false, 4>(c, s, G, mode, gamma, zero_bnd, ctl, stage);
+        else launch_flux_t<false, 3>(c, s, G, mode, gamma, zero_bnd, ctl, stage);
+    }
 }
 
 void launch_boundary(kmf_ctx *c, cudaStream_t s, const double *G, const double fs[4], double gamma, Ctrl *ctl,
@@ -510,63 +562,70 @@ void launch_boundary(kmf_ctx *c, cudaStream_t s, const double *G, const double f
         c->dg(), c->db(), c->q.p, G, c->R.p, inv_gm1, c_i0, fs[0], fs[1], fs[2], fs[3], ctl, stage);
 }
 
-void launch_update(kmf_ctx *c, cudaStream_t s, int stage, double gamma, double cfl)
+void launch_update(kmf_ctx *c, cudaStream_t s, int stage, double gamma, double cfl, IterOut io)
 {
     DG g = c->dg();
     const int nb = nblk(c->n);
     Ctrl *ctl = c->ctrl.p;
+    double *Uo = c->Uo.p, *Us = c->Us.p, *dt = c->dt.p, *q = c->q.p;
+    const double *R = c->R.p;
     switch (stage) {
-    case 1: k_update<1><<<nb, kTB, 0, s>>>(g, c->Uo.p, c->Us.p, c->R.p, c->dt.p, c->q.p, gamma, cfl, ctl); break;
-    case 2: k_update<2><<<nb, kTB, 0, s>>>(g, c->Uo.p, c->Us.p, c->R.p, c->dt.p, c->q.p, gamma, cfl, ctl); break;
-    case 3: k_update<3><<<nb, kTB, 0, s>>>(g, c->Uo.p, c->Us.p, c->R.p, c->dt.p, c->q.p, gamma, cfl, ctl); break;
-    default: k_update<4><<<nb, kTB, 0, s>>>(g, c->Uo.p, c->Us.p, c->R.p, c->dt.p, c->q.p, gamma, cfl, ctl); break;
+    case 1: k_update<1><<<nb, kTB, 0, s>>>(g, Uo, Us, R, dt, q, gamma, cfl, ctl, io); break;
+    case 2: k_update<2><<<nb, kTB, 0, s>>>(g, Uo, Us, R, dt, q, gamma, cfl, ctl, io); break;
+    case 3: k_update<3><<<nb, kTB, 0, s>>>(g, Uo, Us, R, dt, q, gamma, cfl, ctl, io); break;
+    default: k_update<4><<<nb, kTB, 0, s>>>(g, Uo, Us, R, dt, q, gamma, cfl, ctl, io); break;
     }
 }
 
 // One outer iteration (solver.py:515-559) enqueued on s0; the boundary
 // closure runs on a forked branch concurrently with the interior flux.
-void enqueue_iteration(kmf_ctx *c, const kmf_params *p, double *hist, int hist_base, int cap, bool timed)
+enum { ITER_PLAIN = 0, ITER_INSTRUMENT = 1, ITER_BENCH = 2 };
+
+// ITER_INSTRUMENT: eager launches with events around every group, one sync
+// per iteration, per-stage seconds accumulated (solver.py:461-474).
+// ITER_BENCH: captured into a graph with external event-record nodes around
+// each interior flux launch (the roofline kernel, timed on its own stream).
+void enqueue_iteration(kmf_ctx *c, const kmf_params *p, double *hist, int hist_base, int cap, int how)
 {
     Ctrl *ctl = c->ctrl.p;
+    const bool inst = how == ITER_INSTRUMENT, bench = how == ITER_BENCH;
     for (int stage = 1; stage <= 4; stage++) {
-        if (timed) cudaEventRecord(c->ev[0], c->s0);
+        cudaEvent_t *e = &c->ev[4 * (stage - 1)];
+        if (inst) cudaEventRecord(e[0], c->s0);
         int which = launch_qgrad(c, c->s0, stage, p->n_inner, ctl, 0);
         const double *G = which ? c->GB.p : c->GA.p;
         c->last_G = which;
-        if (timed) cudaEventRecord(c->ev[1], c->s0);
+        if (inst) cudaEventRecord(e[1], c->s0);
         cudaEventRecord(c->fork, c->s0);
         cudaStreamWaitEvent(c->s1, c->fork, 0);
         launch_boundary(c, c->s1, G, p->fs, p->gamma, ctl, stage);
         cudaEventRecord(c->join, c->s1);
+        if (bench) cudaEventRecordWithFlags(c->evb[2 * (stage - 1)], c->s0, cudaEventRecordExternal);
         launch_flux(c, c->s0, G, p->mode, p->gamma, 0, ctl, stage);
+        if (bench) cudaEventRecordWithFlags(c->evb[2 * (stage - 1) + 1], c->s0, cudaEventRecordExternal);
         cudaStreamWaitEvent(c->s0, c->join, 0);
-        if (timed) cudaEventRecord(c->ev[2], c->s0);
-        launch_update(c, c->s0, stage, p->gamma, p->cfl);
-        if (timed) {
-            cudaEventRecord(c->ev[3], c->s0);
-            cudaEventSynchronize(c->ev[3]);
+        if (inst) cudaEventRecord(e[2], c->s0);
+        IterOut io{hist, hist_base, cap, p->convergence_tol};
+        launch_update(c, c->s0, stage, p->gamma, p->cfl, io);
+        if (inst) cudaEventRecord(e[3], c->s0);
+    }
+    if (inst) {
+        // residue_norm and the iteration close run inside the stage-4 update
+        cudaEventSynchronize(c->ev[15]);
+        for (int s = 0; s < 4; s++) {
             float a = 0, b = 0, d = 0;
-            cudaEventElapsedTime(&a, c->ev[0], c->ev[1]);
-            cudaEventElapsedTime(&b, c->ev[1], c->ev[2]);
-            cudaEventElapsedTime(&d, c->ev[2], c->ev[3]);
+            cudaEventElapsedTime(&a, c->ev[4 * s], c->ev[4 * s + 1]);
+            cudaEventElapsedTime(&b, c->ev[4 * s + 1], c->ev[4 * s + 2]);
+            cudaEventElapsedTime(&d, c->ev[4 * s + 2], c->ev[4 * s + 3]);
             c->stage_sec[2] += a * 1e-3;
             c->stage_sec[3] += b * 1e-3;
             c->stage_sec[4] += d * 1e-3;
         }
     }
-    if (timed) cudaEventRecord(c->ev[4], c->s0);
-    k_finalize<<<1, 1, 0, c->s0>>>(ctl, c->n, hist, hist_base, cap, p->convergence_tol);
-    if (timed) {
-        cudaEventRecord(c->ev[5], c->s0);
-        cudaEventSynchronize(c->ev[5]);
-        float a = 0;
-        cudaEventElapsedTime(&a, c->ev[4], c->ev[5]);
-        c->stage_sec[5] += a * 1e-3;
-    }
 }
 
 int get_graph(kmf_ctx *c, const kmf_params *p, int unroll, double *hist, int hist_base, int cap,
-              cudaGraphExec_t *exec, GraphKey *key)
+              cudaGraphExec_t *exec, GraphKey *key, int how = ITER_PLAIN)
 {
     GraphKey k;
     std::memset(&k, 0, sizeof k);
@@ -587,7 +646,7 @@ int get_graph(kmf_ctx *c, const kmf_params *p, int unroll, double *hist, int his
     }
     cudaGraph_t graph;
     CK(cudaStreamBeginCapture(c->s0, cudaStreamCaptureModeThreadLocal));
-    for (int u = 0; u < unroll; u++) enqueue_iteration(c, p, hist, hist_base, cap, false);
+    for (int u = 0; u < unroll; u++) enqueue_iteration(c, p, hist, hist_base, cap, how);
     CK(cudaStreamEndCapture(c->s0, &graph));
     cudaError_t e = cudaGraphInstantiate(exec, graph, 0);
     cudaGraphDestroy(graph);
@@ -637,6 +696,14 @@ int kmf_create(kmf_ctx **out, const kmf_geometry *g, int device)
     CK(cudaSetDevice(device));
     kmf_ctx *c = new kmf_ctx();
     c->device = device;
+    if (const char *e = std::getenv("KMF_QG_NC")) {
+        int v = std::atoi(e);
+        if (v == 1 || v == 2 || v == 4) c->qg_nc = v;
+    }
+    if (const char *e = std::getenv("KMF_FLUX_MINB")) {
+        int v = std::atoi(e);
+        if (v == 3 || v == 4) c->flux_minb = v;
+    }
     int rc = build_context(c, g);
     if (rc != KMF_OK) {
         delete c;
@@ -708,6 +775,7 @@ int kmf_run(kmf_ctx *c, const kmf_params *p, int n_iter, double *history, int *i
     Ctrl init;
     std::memset(&init, 0, sizeof init);
     init.iter = 1;
+    init.epoch = 1;
     CK(cudaMemcpyAsync(c->ctrl.p, &init, sizeof init, cudaMemcpyHostToDevice, c->s0));
     for (double &s : c->stage_sec) s = 0.0;
 
@@ -716,7 +784,7 @@ int kmf_run(kmf_ctx *c, const kmf_params *p, int n_iter, double *history, int *i
     if (p->instrument) {
         // timed iterations launch eagerly with events around every group
         for (int it = 0; it < n_iter; it++) {
-            enqueue_iteration(c, p, c->history.p, 1, n_iter, it >= skip);
+            enqueue_iteration(c, p, c->history.p, 1, n_iter, it >= skip ? ITER_INSTRUMENT : ITER_PLAIN);
         }
         done = n_iter;
     } else {
@@ -863,11 +931,7 @@ int kmf_op_first_order(kmf_ctx *c, const double *q, double *qx, double *qy)
     int rc = upload_fields(c, q, 4, c->q.p);
     if (rc) return rc;
     if ((rc = reset_ctrl(c))) return rc;
-    const int nb = nblk(c->n);
-    if (c->xy)
-        k_first_order<true><<<nb, kTB, 0, c->s0>>>(c->dg(), c->q.p, c->GA.p, c->ctrl.p, 0);
-    else
-        k_first_order<false><<<nb, kTB, 0, c->s0>>>(c->dg(), c->q.p, c->GA.p, c->ctrl.p, 0);
+    launch_first_order(c, c->s0, c->GA.p, c->ctrl.p, 0);
     CK(cudaGetLastError());
     if ((rc = download_fields(c, c->GA.p, 4, qx))) return rc;
     return download_fields(c, c->GA.p + 4 * (size_t)c->ld, 4, qy);
@@ -890,18 +954,13 @@ int kmf_op_q_derivatives(kmf_ctx *c, const double *q, int n_inner, const double 
     if (pqx && pqy) {
         if ((rc = upload_fields(c, pqx, 4, c->GA.p))) return rc;
         if ((rc = upload_fields(c, pqy, 4, c->GA.p + 4 * (size_t)c->ld))) return rc;
-    } else if (c->xy) {
-        k_first_order<true><<<nb, kTB, 0, c->s0>>>(g, c->q.p, c->GA.p, c->ctrl.p, 0);
     } else {
-        k_first_order<false><<<nb, kTB, 0, c->s0>>>(g, c->q.p, c->GA.p, c->ctrl.p, 0);
+        launch_first_order(c, c->s0, c->GA.p, c->ctrl.p, 0);
     }
     double *cur = c->GA.p, *nxt = c->GB.p;
     for (int it = 0; it < n_inner; it++) {
         CK(cudaMemsetAsync(&c->ctrl.p->resmax, 0, sizeof(unsigned long long), c->s0));
-        if (c->xy)
-            k_sweep<true><<<nb, kTB, 0, c->s0>>>(g, c->q.p, cur, nxt, c->ctrl.p, 0, 1 + it, 1);
-        else
-            k_sweep<false><<<nb, kTB, 0, c->s0>>>(g, c->q.p, cur, nxt, c->ctrl.p, 0, 1 + it, 1);
+        launch_sweep(c, c->s0, cur, nxt, c->ctrl.p, 0, 1 + it, 1);
         CK(cudaGetLastError());
         if (inner_residuals) {
             unsigned long long b = 0;
@@ -1198,6 +1257,110 @@ int kmf_op_residue(int64_t n, const double *Un, const double *Uold, double *out)
     CK(cudaGetLastError());
     CK(cudaMemcpy(out, o, sizeof(double), cudaMemcpyDeviceToHost));
     return KMF_OK;
+}
+
+}  // extern "C"
+
+// ================================================================ bench ABI
+
+extern "C" {
+
+// Timed outer iterations for bench.py: each step = one graph launch of one
+// outer iteration on the context stream, bracketed by CUDA events; between
+// steps a `flush_bytes` memset on the same stream evicts L2 (outside the
+// timed events).  flux_ms[i] = summed duration of the 4 interior flux
+// launches of step i (events on the flux kernel's own stream).
+int kmf_bench_steps(kmf_ctx *c, const kmf_params *p, int n_steps, int64_t flush_bytes, double *step_ms,
+                    double *flux_ms, int *launches_per_step)
+{
+    if (!c || !p || n_steps < 1 || !step_ms || !flux_ms) return KMF_EINVAL;
+    if (!c->have_state) {
+        set_msg("kmf_bench_steps: no state");
+        return KMF_EINVAL;
+    }
+    CK(cudaSetDevice(c->device));
+    if (int rc = seed_state(c, p->gamma, p->cfl)) return rc;
+    if ((int)c->history.n < n_steps) CK(c->history.alloc(n_steps));
+    if (flush_bytes > 0 && (int64_t)c->flush.n < flush_bytes) CK(c->flush.alloc((size_t)flush_bytes));
+    Ctrl init;
+    std::memset(&init, 0, sizeof init);
+    init.iter = 1;
+    init.epoch = 1;
+    CK(cudaMemcpyAsync(c->ctrl.p, &init, sizeof init, cudaMemcpyHostToDevice, c->s0));
+    kmf_params q = *p;
+    q.convergence_tol = 0.0;
+    if (int rc = get_graph(c, &q, 1, c->history.p, 1, n_steps, &c->execB, &c->keyB, ITER_BENCH)) return rc;
+    for (int i = 0; i < n_steps; i++) {
+        if (flush_bytes > 0) CK(cudaMemsetAsync(c->flush.p, i & 0xff, (size_t)flush_bytes, c->s0));
+        CK(cudaEventRecord(c->evs[0], c->s0));
+        CK(cudaGraphLaunch(c->execB, c->s0));
+        CK(cudaEventRecord(c->evs[1], c->s0));
+        CK(cudaEventSynchronize(c->evs[1]));
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, c->evs[0], c->evs[1]));
+        step_ms[i] = ms;
+        double f = 0;
+        for (int s = 0; s < 4; s++) {
+            float a = 0;
+            CK(cudaEventElapsedTime(&a, c->evb[2 * s], c->evb[2 * s + 1]));
+            f += a;
+        }
+        flux_ms[i] = f;
+    }
+    Ctrl fin;
+    CK(cudaMemcpy(&fin, c->ctrl.p, sizeof fin, cudaMemcpyDeviceToHost));
+    if (launches_per_step)
+        *launches_per_step = 4 * (1 + p->n_inner + (p->mode ? 4 : 1) + (c->nb > 0 ? 1 : 0) + 1);  // the iteration close is fused into update<4>
+    if ((fin.state & 3ull) == 1ull) {
+        set_msg("kmf_bench_steps: positivity failure at iteration %d", fin.err_iter);
+        return KMF_EPOSITIVITY;
+    }
+    return KMF_OK;
+}
+
+// FP64 pipe peak of this device (DFMA chains on every SM), TFLOP/s.
+int kmf_fp64_peak(double *tflops)
+{
+    if (!tflops) return KMF_EINVAL;
+    if (int rc = ensure_device()) return rc;
+    int dev = 0, sms = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    Tmp tmp;
+    TMP_OR_FAIL(o, double, 1);
+    const int blocks = sms * 8, threads = 256, iters = 16384;
+    k_fp64_peak<<<blocks, threads>>>(64, 1.0, o);  // warm-up
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    double best = 0.0;
+    for (int rep = 0; rep < 3; rep++) {
+        CK(cudaEventRecord(a));
+        k_fp64_peak<<<blocks, threads>>>(iters, 1.0, o);
+        CK(cudaEventRecord(b));
+        CK(cudaEventSynchronize(b));
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, a, b));
+        double fl = 2.0 * 8.0 * iters * (double)blocks * threads;
+        best = std::max(best, fl / (ms * 1e-3) / 1e12);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    *tflops = best;
+    return KMF_OK;
+}
+
+// pinned host buffers for the end-to-end (host-buffer) measurement
+void *kmf_host_alloc(int64_t bytes)
+{
+    void *p = nullptr;
+    if (cudaMallocHost(&p, (size_t)bytes) != cudaSuccess) return nullptr;
+    return p;
+}
+
+void kmf_host_free(void *p)
+{
+    if (p) cudaFreeHost(p);
 }
 
 }  // extern "C"

@@ -29,34 +29,39 @@ constexpr int kStageFinal = 7;
 // number of the launch that set it: 0 running, (seq<<2)|1 positivity error,
 // (seq<<2)|2 converged.  Kernels skip their work once state != 0 unless they
 // carry the very same seq (so every block of the failing launch, and the
-// boundary kernel that shares its seq, still completes).
+// boundary kernel that shares its seq, still completes).  The seq is built
+// from `epoch`, which the end-of-iteration kernel advances on EVERY replayed
+// iteration (also skipped ones), so no later launch can share a seq with the
+// failing one; `iter` advances only on completed iterations.
 struct Ctrl {
     unsigned long long state;
     int iter;
+    int epoch;
     int err_iter;
     int err_stage;
     unsigned int ctx_mask;
+    unsigned int blocks_done;   // last-block detection of the stage-4 update
     unsigned long long resmax;  // inner-residual max (bits of a nonnegative double)
     unsigned long long limbs[kLimbs];
 };
 
-KMF_HD long long seq_of(int iter, int stage, int slot)
+KMF_HD long long seq_of(int epoch, int stage, int slot)
 {
-    return ((long long)iter << 16) | ((long long)stage << 12) | (long long)slot;
+    return ((long long)epoch << 16) | ((long long)stage << 12) | (long long)slot;
 }
 
 KMF_HD bool should_skip(const Ctrl *c, int stage, int slot)
 {
     unsigned long long st = *(volatile const unsigned long long *)&c->state;
     if (st == 0ull) return false;
-    long long me = seq_of(*(volatile const int *)&c->iter, stage, slot);
+    long long me = seq_of(*(volatile const int *)&c->epoch, stage, slot);
     return (long long)(st >> 2) != me;
 }
 
 __device__ __forceinline__ void raise_err(Ctrl *c, int stage, int slot, int ctx)
 {
     atomicOr(&c->ctx_mask, 1u << ctx);
-    unsigned long long want = ((unsigned long long)seq_of(c->iter, stage, slot) << 2) | 1ull;
+    unsigned long long want = ((unsigned long long)seq_of(c->epoch, stage, slot) << 2) | 1ull;
     if (atomicCAS(&c->state, 0ull, want) == 0ull) {
         c->err_iter = c->iter;
         c->err_stage = stage;
@@ -108,19 +113,39 @@ KMF_HD void edge_offsets(const DG &g, int ent, int j, double xi, double yi, doub
 KMF_HD int ell_base(const DG &g, int i) { return g.eoff[i >> 5] + (i & 31); }
 
 // ---------------------------------------------------------------------------
+// q-gradient kernels: NC components of one point per thread (NC = 1, 2, 4).
+// The four components of q are independent in every LS sum, so splitting
+// them over 4/NC threads keeps each sum sequential in CSR order (bitwise)
+// while multiplying the threads in flight.  A 128-thread block covers
+// 128*NC/4 points; warp w handles component group w % (4/NC) of the
+// 32-point SELL slice w / (4/NC), so slice-local ELL offsets stay coalesced.
+template <int NC>
+KMF_HD void qg_thread(int &i, int &k0)
+{
+    constexpr int CG = 4 / NC;            // component groups per point
+    constexpr int P = kTB / CG;           // points per block
+    const int w = threadIdx.x >> 5;
+    i = blockIdx.x * P + (w / CG) * 32 + (threadIdx.x & 31);
+    k0 = (w % CG) * NC;
+}
+
+template <int NC>
+constexpr int qg_points_per_block() { return kTB * NC / 4; }
+
 // lsq.py:164-175 first_order_q_gradients -- bitwise (CSR-order sums, no FMA)
-template <bool XY>
+template <bool XY, int NC>
 __global__ void __launch_bounds__(kTB) k_first_order(DG g, const double *__restrict__ q,
                                                      double *__restrict__ G, Ctrl *c, int stage)
 {
     if (c && should_skip(c, stage, 0)) return;
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    int i, k0;
+    qg_thread<NC>(i, k0);
     if (i >= g.n) return;
     const int ld = g.ld;
-    double qi[4], sx[4], sy[4];
+    double qi[NC], sx[NC], sy[NC];
 #pragma unroll
-    for (int k = 0; k < 4; k++) {
-        qi[k] = q[k * ld + i];
+    for (int k = 0; k < NC; k++) {
+        qi[k] = q[(k0 + k) * ld + i];
         sx[k] = 0.0;
         sy[k] = 0.0;
     }
@@ -132,38 +157,39 @@ __global__ void __launch_bounds__(kTB) k_first_order(DG g, const double *__restr
         double dx, dy;
         edge_offsets<XY>(g, ent, j, xi, yi, dx, dy);
 #pragma unroll
-        for (int k = 0; k < 4; k++) {
-            double dq = SUB(q[k * ld + j], qi[k]);
+        for (int k = 0; k < NC; k++) {
+            double dq = SUB(q[(k0 + k) * ld + j], qi[k]);
             sx[k] = ADD(sx[k], MUL(dx, dq));
             sy[k] = ADD(sy[k], MUL(dy, dq));
         }
     }
     const double sxx = g.fsum[i], sxy = g.fsum[ld + i], syy = g.fsum[2 * ld + i], det = g.fsum[3 * ld + i];
 #pragma unroll
-    for (int k = 0; k < 4; k++) {
-        G[k * ld + i] = DIV(SUB(MUL(syy, sx[k]), MUL(sxy, sy[k])), det);
-        G[(4 + k) * ld + i] = DIV(SUB(MUL(sxx, sy[k]), MUL(sxy, sx[k])), det);
+    for (int k = 0; k < NC; k++) {
+        G[(k0 + k) * ld + i] = DIV(SUB(MUL(syy, sx[k]), MUL(sxy, sy[k])), det);
+        G[(4 + k0 + k) * ld + i] = DIV(SUB(MUL(sxx, sy[k]), MUL(sxy, sx[k])), det);
     }
 }
 
 // lsq.py:214-227 one Jacobi sweep of the defect-corrected gradients --
-// bitwise.  With `resmax` the max |new - old| (lsq.py:238-243) is reduced.
-template <bool XY>
+// bitwise.  With want_res the max |new - old| (lsq.py:238-243) is reduced.
+template <bool XY, int NC>
 __global__ void __launch_bounds__(kTB) k_sweep(DG g, const double *__restrict__ q,
                                                const double *__restrict__ Gin, double *__restrict__ Gout,
                                                Ctrl *c, int stage, int slot, int want_res)
 {
     if (c && should_skip(c, stage, slot)) return;
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    int i, k0;
+    qg_thread<NC>(i, k0);
     double rmax = 0.0;
     if (i < g.n) {
         const int ld = g.ld;
-        double qi[4], gxi[4], gyi[4], sx[4], sy[4];
+        double qi[NC], gxi[NC], gyi[NC], sx[NC], sy[NC];
 #pragma unroll
-        for (int k = 0; k < 4; k++) {
-            qi[k] = q[k * ld + i];
-            gxi[k] = Gin[k * ld + i];
-            gyi[k] = Gin[(4 + k) * ld + i];
+        for (int k = 0; k < NC; k++) {
+            qi[k] = q[(k0 + k) * ld + i];
+            gxi[k] = Gin[(k0 + k) * ld + i];
+            gyi[k] = Gin[(4 + k0 + k) * ld + i];
             sx[k] = 0.0;
             sy[k] = 0.0;
         }
@@ -175,8 +201,8 @@ __global__ void __launch_bounds__(kTB) k_sweep(DG g, const double *__restrict__ 
             double dx, dy;
             edge_offsets<XY>(g, ent, j, xi, yi, dx, dy);
 #pragma unroll
-            for (int k = 0; k < 4; k++) {
-                double ti = qtilde(q[k * ld + j], Gin[k * ld + j], Gin[(4 + k) * ld + j], dx, dy);
+            for (int k = 0; k < NC; k++) {
+                double ti = qtilde(q[(k0 + k) * ld + j], Gin[(k0 + k) * ld + j], Gin[(4 + k0 + k) * ld + j], dx, dy);
                 double t0 = qtilde(qi[k], gxi[k], gyi[k], dx, dy);
                 double dq = SUB(ti, t0);
                 sx[k] = ADD(sx[k], MUL(dx, dq));
@@ -186,11 +212,11 @@ __global__ void __launch_bounds__(kTB) k_sweep(DG g, const double *__restrict__ 
         const double sxx = g.fsum[i], sxy = g.fsum[ld + i], syy = g.fsum[2 * ld + i],
                      det = g.fsum[3 * ld + i];
 #pragma unroll
-        for (int k = 0; k < 4; k++) {
+        for (int k = 0; k < NC; k++) {
             double nx_ = DIV(SUB(MUL(syy, sx[k]), MUL(sxy, sy[k])), det);
             double ny_ = DIV(SUB(MUL(sxx, sy[k]), MUL(sxy, sx[k])), det);
-            Gout[k * ld + i] = nx_;
-            Gout[(4 + k) * ld + i] = ny_;
+            Gout[(k0 + k) * ld + i] = nx_;
+            Gout[(4 + k0 + k) * ld + i] = ny_;
             if (want_res) {
                 rmax = fmax(rmax, fabs(nx_ - gxi[k]));
                 rmax = fmax(rmax, fabs(ny_ - gyi[k]));
@@ -220,8 +246,8 @@ __global__ void __launch_bounds__(kTB) k_sweep(DG g, const double *__restrict__ 
 // w_f(e) = cx_f*dx + cy_f*dy (cx, cy = rows of the inverse 2x2 matrix,
 // solver.py:192-195), in CSR order per family.  Fused and split4 run the
 // same per-edge code and add families in the same order: bitwise equal.
-template <bool XY, int FAM>
-__global__ void __launch_bounds__(kTB) k_flux(DG g, const double *__restrict__ q,
+template <bool XY, int FAM, int MINB>
+__global__ void __launch_bounds__(kTB, MINB) k_flux(DG g, const double *__restrict__ q,
                                               const double *__restrict__ G, double *__restrict__ R,
                                               double inv_gm1, double c_i0, int zero_boundary, Ctrl *c,
                                               int stage)
@@ -484,20 +510,69 @@ __global__ void __launch_bounds__(kTB) k_boundary(DG g, DB b, const double *__re
 // fused with primitives_to_q for the next stage (state.py:132-138) and, at
 // stage 4, local_timestep for the next iteration (solver.py:154-159) and the
 // exact residue partial sum (solver.py:412-421).
+// Exact warp-aggregated residue accumulation: lanes whose 85-bit shifted
+// mantissas start in the same 32-bit limb are summed with __reduce_add_sync
+// on 16-bit pieces (exact: 32 * 2^16 < 2^21), and one lane per group adds
+// the three limb sums to shared memory.  Every lane of the warp must call.
+__device__ __forceinline__ void accum_add_warp(unsigned long long *limbs, double v)
+{
+    int L = -1;
+    unsigned long long lo = 0, hi = 0;
+    if (v > 0.0) {
+        unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+        int be = (int)(bits >> 52);
+        unsigned long long m = bits & ((1ull << 52) - 1);
+        int e2 = 0;
+        if (be) {
+            m |= 1ull << 52;
+            e2 = be - 1;
+        }
+        L = e2 >> 5;
+        const int sh = e2 & 31;
+        lo = m << sh;
+        hi = sh ? (m >> (64 - sh)) : 0ull;
+    }
+    const unsigned grp = __match_any_sync(0xffffffffu, L);
+    unsigned piece[6] = {(unsigned)(lo & 0xffff), (unsigned)((lo >> 16) & 0xffff), (unsigned)((lo >> 32) & 0xffff),
+                         (unsigned)(lo >> 48), (unsigned)(hi & 0xffff), (unsigned)(hi >> 16)};
+    unsigned s[6];
+#pragma unroll
+    for (int t = 0; t < 6; t++) s[t] = __reduce_add_sync(grp, piece[t]);
+    const int lane = threadIdx.x & 31;
+    if (L >= 0 && lane == __ffs(grp) - 1) {
+        atomicAdd(&limbs[L], (unsigned long long)s[0] + ((unsigned long long)s[1] << 16));
+        atomicAdd(&limbs[L + 1], (unsigned long long)s[2] + ((unsigned long long)s[3] << 16));
+        const unsigned long long top = (unsigned long long)s[4] + ((unsigned long long)s[5] << 16);
+        if (top) atomicAdd(&limbs[L + 2], top);
+    }
+}
+
+KMF_HD double accum_round(const unsigned long long *limbs);
+
+struct IterOut {
+    double *history;
+    int hist_base, cap;
+    double tol;
+};
+
 template <int STAGE>
 __global__ void __launch_bounds__(kTB) k_update(DG g, double *__restrict__ Uo, double *__restrict__ Us,
                                                 const double *__restrict__ R, double *__restrict__ dt,
-                                                double *__restrict__ q, double gamma, double cfl, Ctrl *c)
+                                                double *__restrict__ q, double gamma, double cfl, Ctrl *c,
+                                                IterOut io)
 {
     __shared__ unsigned long long sl[kLimbs];
-    if (should_skip(c, STAGE, kSlotUpdate)) return;
+    __shared__ bool last;
+    const bool skip = should_skip(c, STAGE, kSlotUpdate);
+    if (STAGE != 4 && skip) return;
     if (STAGE == 4) {
         for (int t = threadIdx.x; t < kLimbs; t += blockDim.x) sl[t] = 0ull;
         __syncthreads();
     }
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int ld = g.ld;
-    if (i < g.n) {
+    double dr2 = 0.0;
+    if (!skip && i < g.n) {
         double uo[4], us[4], un[4];
         const double d = dt[i];
 #pragma unroll
@@ -523,13 +598,45 @@ __global__ void __launch_bounds__(kTB) k_update(DG g, double *__restrict__ Uo, d
         if (STAGE == 4) {
             dt[i] = timestep(rho, u1, u2, p, gamma, cfl, g.dmin[i]);
             const double dr = SUB(un[0], uo[0]);
-            accum_add(sl, MUL(dr, dr));
+            dr2 = MUL(dr, dr);
         }
     }
     if (STAGE == 4) {
+        // exact residue sum (solver.py:418-420), then the last block to
+        // finish closes the iteration (residue_norm, history, convergence,
+        // counters) -- no separate finalize launch
+        accum_add_warp(sl, dr2);
         __syncthreads();
         for (int t = threadIdx.x; t < kLimbs; t += blockDim.x)
             if (sl[t]) atomicAdd(&c->limbs[t], sl[t]);
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) last = atomicAdd(&c->blocks_done, 1u) == gridDim.x - 1;
+        __syncthreads();
+        if (last && threadIdx.x == 0) {
+            __threadfence();
+            volatile unsigned long long *vl = c->limbs;
+            unsigned long long lm[kLimbs];
+            for (int l = 0; l < kLimbs; l++) {
+                lm[l] = vl[l];
+                vl[l] = 0ull;
+            }
+            const int ep = c->epoch;
+            const unsigned long long st = *(volatile unsigned long long *)&c->state;
+            if (st == 0ull) {
+                // residue_norm finish: sqrt(fsum(drho^2)/n) (solver.py:418-421)
+                const double res = sqrt(accum_round(lm) / (double)g.n);
+                const int it = c->iter;
+                const int h = it - io.hist_base;
+                if (h >= 0 && h < io.cap) io.history[h] = res;
+                if (io.tol > 0.0 && res <= io.tol)  // solver.py:557-559
+                    c->state = ((unsigned long long)seq_of(ep, kStageFinal, 0) << 2) | 2ull;
+                c->iter = it + 1;
+            }
+            c->blocks_done = 0u;
+            c->epoch = ep + 1;
+            __threadfence();
+        }
     }
 }
 
@@ -592,21 +699,6 @@ KMF_HD double accum_round(const unsigned long long *limbs)
     return scalbn((double)mant, e - 1074);
 }
 
-// residue_norm finish: sqrt(fsum(drho^2)/n) (solver.py:418-421), history,
-// convergence test (solver.py:557-559), advance the iteration counter.
-__global__ void k_finalize(Ctrl *c, int n, double *history, int hist_base, int cap, double tol)
-{
-    if (should_skip(c, kStageFinal, 0)) return;
-    const double total = accum_round(c->limbs);
-    for (int l = 0; l < kLimbs; l++) c->limbs[l] = 0ull;
-    const double res = sqrt(total / (double)n);
-    const int it = c->iter;
-    const int h = it - hist_base;
-    if (h >= 0 && h < cap) history[h] = res;
-    if (tol > 0.0 && res <= tol)
-        c->state = ((unsigned long long)seq_of(it, kStageFinal, 0) << 2) | 2ull;
-    c->iter = it + 1;
-}
 
 // ---------------------------------------------------------------- set/get
 
@@ -856,10 +948,12 @@ __global__ void k_op_residue(int n, const double *Un, const double *Uold, unsign
     for (int t = threadIdx.x; t < kLimbs; t += blockDim.x) sl[t] = 0ull;
     __syncthreads();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    double d2 = 0.0;
     if (i < n) {
         const double d = SUB(Un[i], Uold[i]);
-        accum_add(sl, MUL(d, d));
+        d2 = MUL(d, d);
     }
+    accum_add_warp(sl, d2);
     __syncthreads();
     for (int t = threadIdx.x; t < kLimbs; t += blockDim.x)
         if (sl[t]) atomicAdd(&limbs[t], sl[t]);
@@ -880,4 +974,23 @@ __global__ void k_op_timestep(DG g, const double *__restrict__ pr_dev, double cf
                          g.dmin[i]);
 }
 
+}  // namespace kmf
+
+namespace kmf {
+// FP64 pipe peak probe: 8 independent DFMA chains per thread.
+__global__ void k_fp64_peak(int iters, double seed, double *out)
+{
+    double a[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) a[k] = seed + k * 1e-3 + threadIdx.x * 1e-9;
+    const double b = 0.999999, cc = 1e-7;
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int k = 0; k < 8; k++) a[k] = fma(a[k], b, cc);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) s += a[k];
+    if (s == 12345.678) out[0] = s;  // keep the chains alive
+}
 }  // namespace kmf

@@ -83,7 +83,9 @@ struct kmf_ctx {
     int n = 0, ld = 0;
     bool xy = true;  // offsets recomputed from coordinates
     int qg_nc = 2;   // q-gradient components per thread (KMF_QG_NC)
-    int flux_minb = 4;  // interior flux kernel blocks per SM (KMF_FLUX_MINB)
+    int qg_unroll = 1;  // q-gradient edge unroll (KMF_QG_UNROLL)
+    int flux_impl = 1;  // interior flux kernel shape (KMF_FLUX_IMPL)
+    int flux_minb = 4;  // pair-kernel blocks per SM (KMF_FLUX_MINB)
     bool has_perm = false;
     cudaStream_t s0 = nullptr, s1 = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
@@ -464,45 +466,52 @@ int build_context(kmf_ctx *c, const kmf_geometry *g)
 
 // ------------------------------------------------------------ stage launch
 
-template <bool XY, int NC>
+template <bool XY, int NC, int U>
 void launch_fo_t(kmf_ctx *c, cudaStream_t s, double *G, Ctrl *ctl, int stage)
 {
     const int nb = nblk(c->n, qg_points_per_block<NC>());
-    k_first_order<XY, NC><<<nb, kTB, 0, s>>>(c->dg(), c->q.p, G, ctl, stage);
+    k_first_order<XY, NC, U><<<nb, kTB, 0, s>>>(c->dg(), c->q.p, G, ctl, stage);
 }
 
-template <bool XY, int NC>
+template <bool XY, int NC, int U>
 void launch_sw_t(kmf_ctx *c, cudaStream_t s, const double *Gin, double *Gout, Ctrl *ctl, int stage, int slot,
                  int want_res)
 {
     const int nb = nblk(c->n, qg_points_per_block<NC>());
-    k_sweep<XY, NC><<<nb, kTB, 0, s>>>(c->dg(), c->q.p, Gin, Gout, ctl, stage, slot, want_res);
+    k_sweep<XY, NC, U><<<nb, kTB, 0, s>>>(c->dg(), c->q.p, Gin, Gout, ctl, stage, slot, want_res);
 }
 
-// components per thread of the q-gradient kernels (KMF_QG_NC = 1, 2 or 4)
+// q-gradient launch shape: KMF_QG_NC components per thread (1, 2, 4) and
+// KMF_QG_UNROLL edge unroll (1, 2, 4); connectivities whose offsets are not
+// x[j]-x[i] use the stored-offset variant (NC 2, U 1).
+#define KMF_QG_DISPATCH(CALL, ...)                                          \
+    do {                                                                    \
+        if (!c->xy) {                                                       \
+            CALL<false, 2, 1>(__VA_ARGS__);                                 \
+            break;                                                          \
+        }                                                                   \
+        switch (c->qg_nc * 10 + c->qg_unroll) {                             \
+        case 11: CALL<true, 1, 1>(__VA_ARGS__); break;                      \
+        case 12: CALL<true, 1, 2>(__VA_ARGS__); break;                      \
+        case 14: CALL<true, 1, 4>(__VA_ARGS__); break;                      \
+        case 21: CALL<true, 2, 1>(__VA_ARGS__); break;                      \
+        case 22: CALL<true, 2, 2>(__VA_ARGS__); break;                      \
+        case 24: CALL<true, 2, 4>(__VA_ARGS__); break;                      \
+        case 41: CALL<true, 4, 1>(__VA_ARGS__); break;                      \
+        case 42: CALL<true, 4, 2>(__VA_ARGS__); break;                      \
+        default: CALL<true, 4, 4>(__VA_ARGS__); break;                      \
+        }                                                                   \
+    } while (0)
+
 void launch_first_order(kmf_ctx *c, cudaStream_t s, double *G, Ctrl *ctl, int stage)
 {
-    switch ((c->xy ? 8 : 0) + c->qg_nc) {
-    case 9: launch_fo_t<true, 1>(c, s, G, ctl, stage); break;
-    case 10: launch_fo_t<true, 2>(c, s, G, ctl, stage); break;
-    case 12: launch_fo_t<true, 4>(c, s, G, ctl, stage); break;
-    case 1: launch_fo_t<false, 1>(c, s, G, ctl, stage); break;
-    case 2: launch_fo_t<false, 2>(c, s, G, ctl, stage); break;
-    default: launch_fo_t<false, 4>(c, s, G, ctl, stage); break;
-    }
+    KMF_QG_DISPATCH(launch_fo_t, c, s, G, ctl, stage);
 }
 
 void launch_sweep(kmf_ctx *c, cudaStream_t s, const double *Gin, double *Gout, Ctrl *ctl, int stage, int slot,
                   int want_res)
 {
-    switch ((c->xy ? 8 : 0) + c->qg_nc) {
-    case 9: launch_sw_t<true, 1>(c, s, Gin, Gout, ctl, stage, slot, want_res); break;
-    case 10: launch_sw_t<true, 2>(c, s, Gin, Gout, ctl, stage, slot, want_res); break;
-    case 12: launch_sw_t<true, 4>(c, s, Gin, Gout, ctl, stage, slot, want_res); break;
-    case 1: launch_sw_t<false, 1>(c, s, Gin, Gout, ctl, stage, slot, want_res); break;
-    case 2: launch_sw_t<false, 2>(c, s, Gin, Gout, ctl, stage, slot, want_res); break;
-    default: launch_sw_t<false, 4>(c, s, Gin, Gout, ctl, stage, slot, want_res); break;
-    }
+    KMF_QG_DISPATCH(launch_sw_t, c, s, Gin, Gout, ctl, stage, slot, want_res);
 }
 
 // q-derivatives of one stage: first order into GA, sweeps ping-pong;
@@ -520,13 +529,25 @@ int launch_qgrad(kmf_ctx *c, cudaStream_t s, int stage, int n_inner, Ctrl *ctl, 
     return which;
 }
 
-template <bool XY, int MINB>
+template <bool XY, int MINB, bool PAIR>
 void launch_flux_t(kmf_ctx *c, cudaStream_t s, const double *G, int mode, double gamma, int zero_bnd, Ctrl *ctl,
                    int stage)
 {
     DG g = c->dg();
-    const int nb = nblk(c->n);
     const double inv_gm1 = 1.0 / (gamma - 1.0), c_i0 = (2.0 - gamma) / (gamma - 1.0);
+    if (PAIR) {
+        const int nb = nblk(c->n, kTB / 2);
+        if (mode == 0) {
+            k_flux2<XY, -1, MINB><<<nb, kTB, 0, s>>>(g, c->q.p, G, c->R.p, inv_gm1, c_i0, zero_bnd, ctl, stage);
+        } else {
+            k_flux2<XY, 0, MINB><<<nb, kTB, 0, s>>>(g, c->q.p, G, c->R.p, inv_gm1, c_i0, zero_bnd, ctl, stage);
+            k_flux2<XY, 1, MINB><<<nb, kTB, 0, s>>>(g, c->q.p, G, c->R.p, inv_gm1, c_i0, zero_bnd, ctl, stage);
+            k_flux2<XY, 2, MINB><<<nb, kTB, 0, s>>>(g, c->q.p, G, c->R.p, inv_gm1, c_i0, zero_bnd, ctl, stage);
+            k_flux2<XY, 3, MINB><<<nb, kTB, 0, s>>>(g, c->q.p, G, c->R.p, inv_gm1, c_i0, zero_bnd, ctl, stage);
+        }
+        return;
+    }
+    const int nb = nblk(c->n);
     if (mode == 0) {
         k_flux<XY, -1, MINB><<<nb, kTB, 0, s>>>(g, c->q.p, G, c->R.p, inv_gm1, c_i0, zero_bnd, ctl, stage);
     } else {
@@ -537,19 +558,26 @@ void launch_flux_t(kmf_ctx *c, cudaStream_t s, const double *G, int mode, double
     }
 }
 
-// occupancy of the interior flux kernel: KMF_FLUX_MINB = 3 (<=168 regs) or
-// 4 (<=128 regs) resident 128-thread blocks per SM
+// interior flux kernel shape: KMF_FLUX_IMPL 1 (thread per point, <=168 regs,
+// 3 blocks/SM) or 2 (thread pair per point, KMF_FLUX_MINB 4/5/6 blocks/SM)
 void launch_flux(kmf_ctx *c, cudaStream_t s, const double *G, int mode, double gamma, int zero_bnd, Ctrl *ctl,
                  int stage)
 {
-    const bool m4 = c->flux_minb == 4;
-    if (c->xy) {
-        if (m4) launch_flux_t<true, 4>(c, s, G, mode, gamma, zero_bnd, ctl, stage);
-        else launch_flux_t<true, 3>(c, s, G, mode, gamma, zero_bnd, ctl, stage);
-    } else {
-        if (m4) launch_flux_t<false, 4>(c, s, G, mode, gamma, zero_bnd, ctl, stage);
-        else launch_flux_t<false, 3>(c, s, G, mode, gamma, zero_bnd, ctl, stage);
+#define KMF_FLUX_ARGS c, s, G, mode, gamma, zero_bnd, ctl, stage
+    if (!c->xy) {
+        launch_flux_t<false, 3, false>(KMF_FLUX_ARGS);
+        return;
     }
+    if (c->flux_impl == 1) {
+        launch_flux_t<true, 3, false>(KMF_FLUX_ARGS);
+        return;
+    }
+    switch (c->flux_minb) {
+    case 6: launch_flux_t<true, 6, true>(KMF_FLUX_ARGS); break;
+    case 5: launch_flux_t<true, 5, true>(KMF_FLUX_ARGS); break;
+    default: launch_flux_t<true, 4, true>(KMF_FLUX_ARGS); break;
+    }
+#undef KMF_FLUX_ARGS
 }
 
 void launch_boundary(kmf_ctx *c, cudaStream_t s, const double *G, const double fs[4], double gamma, Ctrl *ctl,
@@ -700,9 +728,17 @@ int kmf_create(kmf_ctx **out, const kmf_geometry *g, int device)
         int v = std::atoi(e);
         if (v == 1 || v == 2 || v == 4) c->qg_nc = v;
     }
+    if (const char *e = std::getenv("KMF_QG_UNROLL")) {
+        int v = std::atoi(e);
+        if (v == 1 || v == 2 || v == 4) c->qg_unroll = v;
+    }
     if (const char *e = std::getenv("KMF_FLUX_MINB")) {
         int v = std::atoi(e);
-        if (v == 3 || v == 4) c->flux_minb = v;
+        if (v >= 4 && v <= 6) c->flux_minb = v;
+    }
+    if (const char *e = std::getenv("KMF_FLUX_IMPL")) {
+        int v = std::atoi(e);
+        if (v == 1 || v == 2) c->flux_impl = v;
     }
     int rc = build_context(c, g);
     if (rc != KMF_OK) {

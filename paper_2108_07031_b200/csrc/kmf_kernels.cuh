@@ -132,8 +132,13 @@ KMF_HD void qg_thread(int &i, int &k0)
 template <int NC>
 constexpr int qg_points_per_block() { return kTB * NC / 4; }
 
+// The edge loop is unrolled by U: the U neighbour indices, then all their
+// gathers, are issued before any arithmetic (U-fold memory-level
+// parallelism); the accumulation itself stays strictly in slot order and
+// tail slots are predicated off, so the result is unchanged bit for bit.
+
 // lsq.py:164-175 first_order_q_gradients -- bitwise (CSR-order sums, no FMA)
-template <bool XY, int NC>
+template <bool XY, int NC, int U>
 __global__ void __launch_bounds__(kTB) k_first_order(DG g, const double *__restrict__ q,
                                                      double *__restrict__ G, Ctrl *c, int stage)
 {
@@ -151,16 +156,30 @@ __global__ void __launch_bounds__(kTB) k_first_order(DG g, const double *__restr
     }
     const double xi = g.x[i], yi = g.y[i];
     const int base = ell_base(g, i), d = g.deg[i];
-    for (int s = 0; s < d; s++) {
-        const int ent = base + s * 32;
-        const int j = g.eidx[ent];
-        double dx, dy;
-        edge_offsets<XY>(g, ent, j, xi, yi, dx, dy);
+    for (int s0 = 0; s0 < d; s0 += U) {
+        int jj[U], ent[U];
 #pragma unroll
-        for (int k = 0; k < NC; k++) {
-            double dq = SUB(q[(k0 + k) * ld + j], qi[k]);
-            sx[k] = ADD(sx[k], MUL(dx, dq));
-            sy[k] = ADD(sy[k], MUL(dy, dq));
+        for (int u = 0; u < U; u++) {
+            ent[u] = base + min(s0 + u, d - 1) * 32;
+            jj[u] = g.eidx[ent[u]];
+        }
+        double dx[U], dy[U], qj[U][NC];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            edge_offsets<XY>(g, ent[u], jj[u], xi, yi, dx[u], dy[u]);
+#pragma unroll
+            for (int k = 0; k < NC; k++) qj[u][k] = q[(k0 + k) * ld + jj[u]];
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            if (s0 + u < d) {
+#pragma unroll
+                for (int k = 0; k < NC; k++) {
+                    double dq = SUB(qj[u][k], qi[k]);
+                    sx[k] = ADD(sx[k], MUL(dx[u], dq));
+                    sy[k] = ADD(sy[k], MUL(dy[u], dq));
+                }
+            }
         }
     }
     const double sxx = g.fsum[i], sxy = g.fsum[ld + i], syy = g.fsum[2 * ld + i], det = g.fsum[3 * ld + i];
@@ -173,7 +192,7 @@ __global__ void __launch_bounds__(kTB) k_first_order(DG g, const double *__restr
 
 // lsq.py:214-227 one Jacobi sweep of the defect-corrected gradients --
 // bitwise.  With want_res the max |new - old| (lsq.py:238-243) is reduced.
-template <bool XY, int NC>
+template <bool XY, int NC, int U>
 __global__ void __launch_bounds__(kTB) k_sweep(DG g, const double *__restrict__ q,
                                                const double *__restrict__ Gin, double *__restrict__ Gout,
                                                Ctrl *c, int stage, int slot, int want_res)
@@ -195,18 +214,36 @@ __global__ void __launch_bounds__(kTB) k_sweep(DG g, const double *__restrict__ 
         }
         const double xi = g.x[i], yi = g.y[i];
         const int base = ell_base(g, i), d = g.deg[i];
-        for (int s = 0; s < d; s++) {
-            const int ent = base + s * 32;
-            const int j = g.eidx[ent];
-            double dx, dy;
-            edge_offsets<XY>(g, ent, j, xi, yi, dx, dy);
+        for (int s0 = 0; s0 < d; s0 += U) {
+            int jj[U], ent[U];
 #pragma unroll
-            for (int k = 0; k < NC; k++) {
-                double ti = qtilde(q[(k0 + k) * ld + j], Gin[(k0 + k) * ld + j], Gin[(4 + k0 + k) * ld + j], dx, dy);
-                double t0 = qtilde(qi[k], gxi[k], gyi[k], dx, dy);
-                double dq = SUB(ti, t0);
-                sx[k] = ADD(sx[k], MUL(dx, dq));
-                sy[k] = ADD(sy[k], MUL(dy, dq));
+            for (int u = 0; u < U; u++) {
+                ent[u] = base + min(s0 + u, d - 1) * 32;
+                jj[u] = g.eidx[ent[u]];
+            }
+            double dx[U], dy[U], qj[U][NC], gxj[U][NC], gyj[U][NC];
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                edge_offsets<XY>(g, ent[u], jj[u], xi, yi, dx[u], dy[u]);
+#pragma unroll
+                for (int k = 0; k < NC; k++) {
+                    qj[u][k] = q[(k0 + k) * ld + jj[u]];
+                    gxj[u][k] = Gin[(k0 + k) * ld + jj[u]];
+                    gyj[u][k] = Gin[(4 + k0 + k) * ld + jj[u]];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                if (s0 + u < d) {
+#pragma unroll
+                    for (int k = 0; k < NC; k++) {
+                        double ti = qtilde(qj[u][k], gxj[u][k], gyj[u][k], dx[u], dy[u]);
+                        double t0 = qtilde(qi[k], gxi[k], gyi[k], dx[u], dy[u]);
+                        double dq = SUB(ti, t0);
+                        sx[k] = ADD(sx[k], MUL(dx[u], dq));
+                        sy[k] = ADD(sy[k], MUL(dy[u], dq));
+                    }
+                }
             }
         }
         const double sxx = g.fsum[i], sxy = g.fsum[ld + i], syy = g.fsum[2 * ld + i],
@@ -366,6 +403,162 @@ __global__ void __launch_bounds__(kTB, MINB) k_flux(DG g, const double *__restri
             else
                 r = ADD(R[k * ld + i], acc[FAM][k]);
             R[k * ld + i] = r;
+        }
+    } else if (zero_boundary && FAM <= 0) {
+#pragma unroll
+        for (int k = 0; k < 4; k++) R[k * ld + i] = 0.0;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// flux_residual, pair layout: TWO threads per point, one per edge END.
+// Lane 2p+0 ("A") builds q~_i from the neighbour's data, lane 2p+1 ("B")
+// q~_0 from the owner's; each decodes ONE state and evaluates the x- and
+// y-family split fluxes of it; one xor-1 shuffle of four values gives A the
+// x-family difference dG = G(q~_i) - G(q~_0) and B the y-family one.  A
+// accumulates x+/x-, B y+/y-, each in CSR order.  Per-thread state is
+// halved (one decoded state, eight accumulators), so twice the threads are
+// resident.  Per-edge arithmetic is exactly k_flux's (same device
+// functions), fused == split4 bitwise as before.
+template <bool XY, int FAM, int MINB>
+__global__ void __launch_bounds__(kTB, MINB) k_flux2(DG g, const double *__restrict__ q,
+                                                     const double *__restrict__ G, double *__restrict__ R,
+                                                     double inv_gm1, double c_i0, int zero_boundary, Ctrl *c,
+                                                     int stage)
+{
+    if (c && should_skip(c, stage, kSlotFlux)) return;
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const bool roleA = (lane & 1) == 0;  // A: neighbour end (x families); B: owner end (y families)
+    const int i = blockIdx.x * (kTB / 2) + (threadIdx.x >> 1);
+    const bool valid = i < g.n;
+    const int ld = g.ld;
+    const int ii = valid ? i : 0;
+    const bool interior = valid && g.flag[ii] == 0;
+    const int d = valid ? g.deg[ii] : 0;
+    const int dmax = __reduce_max_sync(FULL, d);
+    // owner data (used by B for q~_0; A keeps the same registers idle)
+    double qi[4], gxi[4], gyi[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        qi[k] = q[k * ld + ii];
+        gxi[k] = G[k * ld + ii];
+        gyi[k] = G[(4 + k) * ld + ii];
+    }
+    // this lane's two families: A -> (x+, x-), B -> (y+, y-)
+    const double cP_x = interior ? g.fcoef[(roleA ? 0 : 4) * ld + ii] : 0.0;
+    const double cP_y = interior ? g.fcoef[(roleA ? 1 : 5) * ld + ii] : 0.0;
+    const double cM_x = interior ? g.fcoef[(roleA ? 2 : 6) * ld + ii] : 0.0;
+    const double cM_y = interior ? g.fcoef[(roleA ? 3 : 7) * ld + ii] : 0.0;
+    double accP[4] = {0.0, 0.0, 0.0, 0.0}, accM[4] = {0.0, 0.0, 0.0, 0.0};
+    const double xi = g.x[ii], yi = g.y[ii];
+    const int base = ell_base(g, ii);
+    bool bad = false;
+    for (int s = 0; s < dmax; s++) {
+        const bool live = s < d;
+        const int ent = base + min(s, d > 0 ? d - 1 : 0) * 32;
+        const int j = valid ? g.eidx[ent] : 0;
+        double dx, dy;
+        edge_offsets<XY>(g, ent, j, xi, yi, dx, dy);
+        bool member = live;
+        if (FAM == 0) member = member && (dx <= 0.0);
+        if (FAM == 1) member = member && (dx >= 0.0);
+        if (FAM == 2) member = member && (dy <= 0.0);
+        if (FAM == 3) member = member && (dy >= 0.0);
+        const int p = roleA ? j : ii;  // which end this lane perturbs
+        double t[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const double qq = roleA ? q[k * ld + p] : qi[k];
+            const double gx = roleA ? G[k * ld + p] : gxi[k];
+            const double gy = roleA ? G[(4 + k) * ld + p] : gyi[k];
+            t[k] = qtilde(qq, gx, gy, dx, dy);  // solver.py:184-185, bitwise
+        }
+        const double t4o = __shfl_xor_sync(FULL, t[3], 1);
+        const bool ok = (t[3] < 0.0) && (t4o < 0.0);
+        if (member && !ok) bad = true;
+        const bool work = member && ok && interior;
+        EState st;
+        EShared sh;
+        decode(t[0], t[1], t[2], t[3], inv_gm1, st);
+        shared_of(st, c_i0, sh);
+        double gxf[4], gyf[4], snd[4], rcv[4];
+        const bool px = dx <= 0.0, py = dy <= 0.0;
+        if (FAM < 2) sflux(st, sh, false, (FAM < 0 ? px : FAM == 0) ? 1.0 : -1.0, gxf);
+        if (FAM < 0 || FAM >= 2) sflux(st, sh, true, (FAM < 0 ? py : FAM == 2) ? 1.0 : -1.0, gyf);
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            if (FAM < 0) snd[k] = roleA ? gyf[k] : gxf[k];
+            else snd[k] = FAM < 2 ? gxf[k] : gyf[k];
+            rcv[k] = __shfl_xor_sync(FULL, snd[k], 1);
+        }
+        // A owns the x families, B the y families
+        const bool mine = FAM < 0 ? true : (FAM < 2 ? roleA : !roleA);
+        if (work && mine) {
+            const bool plus = FAM < 0 ? (roleA ? px : py) : (FAM == 0 || FAM == 2);
+            const double w = plus ? fma(cP_x, dx, cP_y * dy) : fma(cM_x, dx, cM_y * dy);
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                // dG = G(q~_i) - G(q~_0): A holds the i end, B the 0 end
+                const double own = (FAM < 0 ? (roleA ? gxf[k] : gyf[k]) : snd[k]);
+                const double dG = roleA ? own - rcv[k] : rcv[k] - own;
+                if (plus)
+                    accP[k] = fma(w, dG, accP[k]);
+                else
+                    accM[k] = fma(w, dG, accM[k]);
+            }
+        }
+        if (FAM < 0) {
+            // ties join both families of an axis (geometry.py:544-549)
+            const bool tie = live && ok && interior && (roleA ? dx == 0.0 : dy == 0.0);
+            if (__any_sync(FULL, live && (dx == 0.0 || dy == 0.0))) {
+                double gm[4];
+                const bool tx = dx == 0.0, ty = dy == 0.0;
+                // lanes evaluate the '-' flux of the axis their PAIR needs:
+                // the x- exchange serves A, the y- exchange serves B
+                if (__any_sync(FULL, tx)) {
+                    sflux(st, sh, false, -1.0, gm);
+#pragma unroll
+                    for (int k = 0; k < 4; k++) {
+                        const double o = __shfl_xor_sync(FULL, gm[k], 1);
+                        if (roleA && tie && tx) accM[k] = fma(fma(cM_x, dx, cM_y * dy), gm[k] - o, accM[k]);
+                    }
+                }
+                if (__any_sync(FULL, ty)) {
+                    sflux(st, sh, true, -1.0, gm);
+#pragma unroll
+                    for (int k = 0; k < 4; k++) {
+                        const double o = __shfl_xor_sync(FULL, gm[k], 1);
+                        if (!roleA && tie && ty) accM[k] = fma(fma(cM_x, dx, cM_y * dy), o - gm[k], accM[k]);
+                    }
+                }
+            }
+        }
+    }
+    if (__any_sync(FULL, bad) && c && lane == 0) raise_err(c, stage, kSlotFlux, 2);
+    // combine: R = ((x+ + x-) + y+) + y-, computed on the B lane
+    double r[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        const double mine = (FAM < 0) ? accP[k] + accM[k] : 0.0;  // A: x+ + x-
+        const double fromA = __shfl_xor_sync(FULL, mine, 1);
+        if (FAM < 0)
+            r[k] = (fromA + accP[k]) + accM[k];  // on B: ((x+ + x-) + y+) + y-
+        else if (FAM == 0 || FAM == 1)
+            r[k] = __shfl_xor_sync(FULL, FAM == 0 ? accP[k] : accM[k], 1);  // A's value onto B
+        else
+            r[k] = FAM == 2 ? accP[k] : accM[k];
+    }
+    if (!valid || roleA) return;
+    if (interior) {
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            double v;
+            if (FAM < 0 || FAM == 0)
+                v = r[k];
+            else
+                v = ADD(R[k * ld + i], r[k]);
+            R[k * ld + i] = v;
         }
     } else if (zero_boundary && FAM <= 0) {
 #pragma unroll

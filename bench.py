@@ -194,9 +194,11 @@ def run_ours(args):
 
     L = _lib.lib()
     _lib.require_device()
+    from paper_2108_07031_b200 import reorder
+
     cloud, conn, cfg, init = setup(args.config)
     n = cloud.n_points
-    dev = DeviceConnectivity(conn, device=local)
+    dev = DeviceConnectivity(conn, device=local, perm=reorder.permutation(cloud, args.order))
     params = _params(cfg)
     peak_fp64 = C.c_double(0.0)
     _lib.check(L.kmf_fp64_peak(C.byref(peak_fp64)), "kmf_fp64_peak")
@@ -272,7 +274,8 @@ def run_ours(args):
         "config": {"workload": CONFIGS[args.config][5], "config_key": args.config, "n_points": n,
                    "n_edges": int(conn.full.idx.size), "n_inner": cfg.n_inner, "mode": cfg.mode,
                    "l2": "flushed between timed steps (256 MiB memset on the solver stream)",
-                   "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"},
+                   "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
+                   "point_order": args.order},
         "rdp_s_per_point_iter": 1.0 / (value / ws),
         "e2e": e2e,
         "gpu_launches": int(lps.value) * K,
@@ -338,6 +341,8 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", choices=tuple(CONFIGS), default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--order", choices=("natural", "hilbert"), default=os.environ.get("KMF_ORDER", "natural"),
+                    help="device point order (bitwise neutral, locality only)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

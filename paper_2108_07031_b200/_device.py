@@ -8,12 +8,13 @@ context and indices of solver.py:164-170, :260-265, state.py:110-128).
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 import weakref
 
 import numpy as np
 
-from . import _lib
+from . import _lib, reorder
 from .geometry import SPLIT_KINDS, Connectivity
 from .state import PositivityError, raise_decode_flags
 
@@ -229,18 +230,35 @@ class DeviceConnectivity:
 
 _cache: dict = {}
 _cache_lock = threading.Lock()
+_order = os.environ.get("KMF_ORDER", "natural")
 
 
-def device_for(conn: Connectivity, perm=None) -> DeviceConnectivity:
-    """Cached device context for this Connectivity object (and permutation)."""
-    key = (id(conn), None if perm is None else id(perm))
+def set_point_order(order: str) -> None:
+    """Device slot order for contexts created from now on: "natural" (the
+    caller's numbering) or "hilbert" (reorder.py).  Results are bitwise
+    identical either way; only memory locality changes."""
+    global _order
+    if order not in reorder.ORDERS:
+        raise ValueError(f"order must be one of {reorder.ORDERS}")
+    _order = order
+
+
+def point_order() -> str:
+    return _order
+
+
+def device_for(conn: Connectivity, order: str | None = None) -> DeviceConnectivity:
+    """Cached device context for this Connectivity object in the given (or
+    current default) point order."""
+    order = order or _order
+    key = (id(conn), order)
     with _cache_lock:
         hit = _cache.get(key)
         if hit is not None:
             ref, dev = hit
             if ref() is conn:
                 return dev
-        dev = DeviceConnectivity(conn, perm=perm)
+        dev = DeviceConnectivity(conn, perm=reorder.permutation(conn.cloud, order))
         _cache[key] = (weakref.ref(conn), dev)
         weakref.finalize(conn, _cache.pop, key, None)
         return dev

@@ -116,6 +116,7 @@ def lib():
         "kmf_op_residue": (C.c_int, [C.c_int64, _dp, _dp, _dp]),
         "kmf_bench_steps": (C.c_int, [vp, C.POINTER(Params), C.c_int, C.c_int64, _dp, _dp, C.POINTER(C.c_int)]),
         "kmf_fp64_peak": (C.c_int, [_dp]),
+        "kmf_fastmath_probe": (C.c_int, [C.c_int64, _dp, C.c_int, _dp]),
         "kmf_host_alloc": (C.c_void_p, [C.c_int64]),
         "kmf_host_free": (None, [C.c_void_p]),
     }
@@ -134,7 +135,7 @@ EXPORTED = (
     "kmf_op_timestep", "kmf_op_first_order", "kmf_op_q_derivatives", "kmf_op_flux_residual",
     "kmf_op_boundary", "kmf_op_primitives_to_q", "kmf_op_q_to_primitives",
     "kmf_op_primitives_to_conserved", "kmf_op_conserved_to_primitives", "kmf_op_split_flux",
-    "kmf_op_full_flux", "kmf_op_state_update", "kmf_op_residue", "kmf_bench_steps", "kmf_fp64_peak",
+    "kmf_op_full_flux", "kmf_op_state_update", "kmf_op_residue", "kmf_bench_steps", "kmf_fp64_peak", "kmf_fastmath_probe",
     "kmf_host_alloc", "kmf_host_free",
 )
 

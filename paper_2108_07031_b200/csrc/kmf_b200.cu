@@ -85,7 +85,7 @@ struct kmf_ctx {
     int qg_nc = 2;   // q-gradient components per thread (KMF_QG_NC)
     int qg_unroll = 1;  // q-gradient edge unroll (KMF_QG_UNROLL)
     int flux_impl = 1;  // interior flux kernel shape (KMF_FLUX_IMPL)
-    int flux_minb = 4;  // pair-kernel blocks per SM (KMF_FLUX_MINB)
+    int flux_minb = 3;  // interior flux blocks per SM (KMF_FLUX_MINB)
     bool has_perm = false;
     cudaStream_t s0 = nullptr, s1 = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
@@ -529,54 +529,72 @@ int launch_qgrad(kmf_ctx *c, cudaStream_t s, int stage, int n_inner, Ctrl *ctl, 
     return which;
 }
 
-template <bool XY, int MINB, bool PAIR>
+// beta^(-1/(gamma-1)) evaluation of the fast decode (kmf_fastmath.cuh):
+// 1 for gamma = 7/5, 2 for gamma = 5/3, 0 otherwise (log/exp)
+inline int gamma_kind(double gamma)
+{
+    if (gamma == 1.4) return 1;
+    if (gamma == 5.0 / 3.0) return 2;
+    return 0;
+}
+
+template <bool XY, int MINB, bool PAIR, int GK>
 void launch_flux_t(kmf_ctx *c, cudaStream_t s, const double *G, int mode, double gamma, int zero_bnd, Ctrl *ctl,
                    int stage)
 {
     DG g = c->dg();
     const double inv_gm1 = 1.0 / (gamma - 1.0), c_i0 = (2.0 - gamma) / (gamma - 1.0);
+    double *R = c->R.p;
+    const double *q = c->q.p;
     if (PAIR) {
         const int nb = nblk(c->n, kTB / 2);
         if (mode == 0) {
-            k_flux2<XY, -1, MINB><<<nb, kTB, 0, s>>>(g, c->q.p, G, c->R.p, inv_gm1, c_i0, zero_bnd, ctl, stage);
+            k_flux2<XY, -1, MINB, GK><<<nb, kTB, 0, s>>>(g, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage);
         } else {
-            k_flux2<XY, 0, MINB><<<nb, kTB, 0, s>>>(g, c->q.p, G, c->R.p, inv_gm1, c_i0, zero_bnd, ctl, stage);
-            k_flux2<XY, 1, MINB><<<nb, kTB, 0, s>>>(g, c->q.p, G, c->R.p, inv_gm1, c_i0, zero_bnd, ctl, stage);
-            k_flux2<XY, 2, MINB><<<nb, kTB, 0, s>>>(g, c->q.p, G, c->R.p, inv_gm1, c_i0, zero_bnd, ctl, stage);
-            k_flux2<XY, 3, MINB><<<nb, kTB, 0, s>>>(g, c->q.p, G, c->R.p, inv_gm1, c_i0, zero_bnd, ctl, stage);
+            k_flux2<XY, 0, MINB, GK><<<nb, kTB, 0, s>>>(g, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage);
+            k_flux2<XY, 1, MINB, GK><<<nb, kTB, 0, s>>>(g, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage);
+            k_flux2<XY, 2, MINB, GK><<<nb, kTB, 0, s>>>(g, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage);
+            k_flux2<XY, 3, MINB, GK><<<nb, kTB, 0, s>>>(g, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage);
         }
         return;
     }
     const int nb = nblk(c->n);
     if (mode == 0) {
-        k_flux<XY, -1, MINB><<<nb, kTB, 0, s>>>(g, c->q.p, G, c->R.p, inv_gm1, c_i0, zero_bnd, ctl, stage);
+        k_flux<XY, -1, MINB, GK><<<nb, kTB, 0, s>>>(g, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage);
     } else {
-        k_flux<XY, 0, MINB><<<nb, kTB, 0, s>>>(g, c->q.p, G, c->R.p, inv_gm1, c_i0, zero_bnd, ctl, stage);
-        k_flux<XY, 1, MINB><<<nb, kTB, 0, s>>>(g, c->q.p, G, c->R.p, inv_gm1, c_i0, zero_bnd, ctl, stage);
-        k_flux<XY, 2, MINB><<<nb, kTB, 0, s>>>(g, c->q.p, G, c->R.p, inv_gm1, c_i0, zero_bnd, ctl, stage);
-        k_flux<XY, 3, MINB><<<nb, kTB, 0, s>>>(g, c->q.p, G, c->R.p, inv_gm1, c_i0, zero_bnd, ctl, stage);
+        k_flux<XY, 0, MINB, GK><<<nb, kTB, 0, s>>>(g, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage);
+        k_flux<XY, 1, MINB, GK><<<nb, kTB, 0, s>>>(g, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage);
+        k_flux<XY, 2, MINB, GK><<<nb, kTB, 0, s>>>(g, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage);
+        k_flux<XY, 3, MINB, GK><<<nb, kTB, 0, s>>>(g, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage);
     }
 }
 
-// interior flux kernel shape: KMF_FLUX_IMPL 1 (thread per point, <=168 regs,
-// 3 blocks/SM) or 2 (thread pair per point, KMF_FLUX_MINB 4/5/6 blocks/SM)
+// interior flux kernel shape: KMF_FLUX_IMPL 1 (thread per point) or 2
+// (thread pair per point); KMF_FLUX_MINB 3 or 4 resident 128-thread blocks/SM
 void launch_flux(kmf_ctx *c, cudaStream_t s, const double *G, int mode, double gamma, int zero_bnd, Ctrl *ctl,
                  int stage)
 {
 #define KMF_FLUX_ARGS c, s, G, mode, gamma, zero_bnd, ctl, stage
+    const int gk = gamma_kind(gamma);
     if (!c->xy) {
-        launch_flux_t<false, 3, false>(KMF_FLUX_ARGS);
+        launch_flux_t<false, 3, false, 0>(KMF_FLUX_ARGS);
         return;
     }
-    if (c->flux_impl == 1) {
-        launch_flux_t<true, 3, false>(KMF_FLUX_ARGS);
+    if (c->flux_impl == 2) {
+        if (gk == 1) launch_flux_t<true, 4, true, 1>(KMF_FLUX_ARGS);
+        else if (gk == 2) launch_flux_t<true, 4, true, 2>(KMF_FLUX_ARGS);
+        else launch_flux_t<true, 4, true, 0>(KMF_FLUX_ARGS);
         return;
     }
-    switch (c->flux_minb) {
-    case 6: launch_flux_t<true, 6, true>(KMF_FLUX_ARGS); break;
-    case 5: launch_flux_t<true, 5, true>(KMF_FLUX_ARGS); break;
-    default: launch_flux_t<true, 4, true>(KMF_FLUX_ARGS); break;
+    if (c->flux_minb == 3) {
+        if (gk == 1) launch_flux_t<true, 3, false, 1>(KMF_FLUX_ARGS);
+        else if (gk == 2) launch_flux_t<true, 3, false, 2>(KMF_FLUX_ARGS);
+        else launch_flux_t<true, 3, false, 0>(KMF_FLUX_ARGS);
+        return;
     }
+    if (gk == 1) launch_flux_t<true, 4, false, 1>(KMF_FLUX_ARGS);
+    else if (gk == 2) launch_flux_t<true, 4, false, 2>(KMF_FLUX_ARGS);
+    else launch_flux_t<true, 4, false, 0>(KMF_FLUX_ARGS);
 #undef KMF_FLUX_ARGS
 }
 
@@ -586,8 +604,20 @@ void launch_boundary(kmf_ctx *c, cudaStream_t s, const double *G, const double f
     if (c->nb == 0) return;
     const double inv_gm1 = 1.0 / (gamma - 1.0), c_i0 = (2.0 - gamma) / (gamma - 1.0);
     const int warps_per_block = kTB / 32;
-    k_boundary<<<(c->nb + warps_per_block - 1) / warps_per_block, kTB, 0, s>>>(
-        c->dg(), c->db(), c->q.p, G, c->R.p, inv_gm1, c_i0, fs[0], fs[1], fs[2], fs[3], ctl, stage);
+    const int nbk = (c->nb + warps_per_block - 1) / warps_per_block;
+    switch (gamma_kind(gamma)) {
+    case 1:
+        k_boundary<1><<<nbk, kTB, 0, s>>>(c->dg(), c->db(), c->q.p, G, c->R.p, inv_gm1, c_i0, fs[0], fs[1], fs[2],
+                                          fs[3], ctl, stage);
+        break;
+    case 2:
+        k_boundary<2><<<nbk, kTB, 0, s>>>(c->dg(), c->db(), c->q.p, G, c->R.p, inv_gm1, c_i0, fs[0], fs[1], fs[2],
+                                          fs[3], ctl, stage);
+        break;
+    default:
+        k_boundary<0><<<nbk, kTB, 0, s>>>(c->dg(), c->db(), c->q.p, G, c->R.p, inv_gm1, c_i0, fs[0], fs[1], fs[2],
+                                          fs[3], ctl, stage);
+    }
 }
 
 void launch_update(kmf_ctx *c, cudaStream_t s, int stage, double gamma, double cfl, IterOut io)
@@ -734,7 +764,7 @@ int kmf_create(kmf_ctx **out, const kmf_geometry *g, int device)
     }
     if (const char *e = std::getenv("KMF_FLUX_MINB")) {
         int v = std::atoi(e);
-        if (v >= 4 && v <= 6) c->flux_minb = v;
+        if (v == 3 || v == 4) c->flux_minb = v;
     }
     if (const char *e = std::getenv("KMF_FLUX_IMPL")) {
         int v = std::atoi(e);
@@ -1400,3 +1430,17 @@ void kmf_host_free(void *p)
 }
 
 }  // extern "C"
+
+extern "C" int kmf_fastmath_probe(int64_t n, const double *x, int which, double *out)
+{
+    if (n <= 0 || !x || !out || which < 0 || which > 3) return KMF_EINVAL;
+    if (int rc = ensure_device()) return rc;
+    Tmp tmp;
+    TMP_OR_FAIL(dx, double, n);
+    TMP_OR_FAIL(dout, double, n);
+    CK(cudaMemcpy(dx, x, sizeof(double) * n, cudaMemcpyHostToDevice));
+    k_fastmath_probe<<<nblk(n), kTB>>>((int)n, dx, which, dout);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(out, dout, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    return KMF_OK;
+}

@@ -16,6 +16,7 @@
 // One thread per point everywhere except the boundary closure (one warp
 // per boundary point, lanes over frame edges).
 #pragma once
+#include "kmf_fastmath.cuh"
 #include "kmf_math.cuh"
 
 namespace kmf {
@@ -283,7 +284,7 @@ __global__ void __launch_bounds__(kTB) k_sweep(DG g, const double *__restrict__ 
 // w_f(e) = cx_f*dx + cy_f*dy (cx, cy = rows of the inverse 2x2 matrix,
 // solver.py:192-195), in CSR order per family.  Fused and split4 run the
 // same per-edge code and add families in the same order: bitwise equal.
-template <bool XY, int FAM, int MINB>
+template <bool XY, int FAM, int MINB, int GK>
 __global__ void __launch_bounds__(kTB, MINB) k_flux(DG g, const double *__restrict__ q,
                                               const double *__restrict__ G, double *__restrict__ R,
                                               double inv_gm1, double c_i0, int zero_boundary, Ctrl *c,
@@ -294,16 +295,9 @@ __global__ void __launch_bounds__(kTB, MINB) k_flux(DG g, const double *__restri
     if (i >= g.n) return;
     const int ld = g.ld;
     const bool interior = g.flag[i] == 0;
-    double qi[4], gxi[4], gyi[4];
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-        qi[k] = q[k * ld + i];
-        gxi[k] = G[k * ld + i];
-        gyi[k] = G[(4 + k) * ld + i];
-    }
-    double cf[8];
-#pragma unroll
-    for (int k = 0; k < 8; k++) cf[k] = interior ? g.fcoef[k * ld + i] : 0.0;
+    // The owner's q, gradients and family weights are re-read from L1 per
+    // edge (through a laundered index the compiler cannot hoist) instead of
+    // being pinned in 40 registers: the kernel is occupancy-bound.
     double acc[4][4];
 #pragma unroll
     for (int f = 0; f < 4; f++)
@@ -322,33 +316,33 @@ __global__ void __launch_bounds__(kTB, MINB) k_flux(DG g, const double *__restri
         if (FAM == 1 && !(dx >= 0.0)) continue;
         if (FAM == 2 && !(dy <= 0.0)) continue;
         if (FAM == 3 && !(dy >= 0.0)) continue;
+        int io;
+        asm volatile("mov.b32 %0, %1;" : "=r"(io) : "r"(i));
         double ti[4], t0[4];
 #pragma unroll
         for (int k = 0; k < 4; k++) {
             ti[k] = qtilde(q[k * ld + j], G[k * ld + j], G[(4 + k) * ld + j], dx, dy);
-            t0[k] = qtilde(qi[k], gxi[k], gyi[k], dx, dy);
+            t0[k] = qtilde(q[k * ld + io], G[k * ld + io], G[(4 + k) * ld + io], dx, dy);
         }
+        const double *cf = g.fcoef + io;  // cf[k * ld]: (cx, cy) of x+, x-, y+, y-
         // solver.py:164 positivity (q4 >= 0, NaN caught by q_to_primitives)
         if (!(ti[3] < 0.0) || !(t0[3] < 0.0)) {
             bad = true;
             continue;
         }
         if (!interior) continue;  // rows zeroed (solver.py:233-234)
-        EState si, s0;
-        decode(ti[0], ti[1], ti[2], ti[3], inv_gm1, si);
-        decode(t0[0], t0[1], t0[2], t0[3], inv_gm1, s0);
-        EShared hi, h0;
-        shared_of(si, c_i0, hi);
-        shared_of(s0, c_i0, h0);
+        FState si, s0;
+        fdecode<GK>(ti[0], ti[1], ti[2], ti[3], inv_gm1, c_i0, si);
+        fdecode<GK>(t0[0], t0[1], t0[2], t0[3], inv_gm1, c_i0, s0);
         double gi[4], g0[4];
         if (FAM < 2) {
             // x family: x+ holds dx <= 0 (tie in both), x- dx >= 0
             const bool primary_p = FAM < 0 ? (dx <= 0.0) : (FAM == 0);
             const double sg = primary_p ? 1.0 : -1.0;
-            const double cx = primary_p ? cf[0] : cf[2];
-            const double cy = primary_p ? cf[1] : cf[3];
-            sflux(si, hi, false, sg, gi);
-            sflux(s0, h0, false, sg, g0);
+            const double cx = primary_p ? cf[0 * ld] : cf[2 * ld];
+            const double cy = primary_p ? cf[1 * ld] : cf[3 * ld];
+            fsflux(si, false, sg, gi);
+            fsflux(s0, false, sg, g0);
             const double w = fma(cx, dx, cy * dy);
 #pragma unroll
             for (int k = 0; k < 4; k++) {
@@ -359,9 +353,9 @@ __global__ void __launch_bounds__(kTB, MINB) k_flux(DG g, const double *__restri
                     acc[1][k] = a;
             }
             if (FAM < 0 && dx == 0.0) {  // tie: also in x-
-                sflux(si, hi, false, -1.0, gi);
-                sflux(s0, h0, false, -1.0, g0);
-                const double w2 = fma(cf[2], dx, cf[3] * dy);
+                fsflux(si, false, -1.0, gi);
+                fsflux(s0, false, -1.0, g0);
+                const double w2 = fma(cf[2 * ld], dx, cf[3 * ld] * dy);
 #pragma unroll
                 for (int k = 0; k < 4; k++) acc[1][k] = fma(w2, gi[k] - g0[k], acc[1][k]);
             }
@@ -369,10 +363,10 @@ __global__ void __launch_bounds__(kTB, MINB) k_flux(DG g, const double *__restri
         if (FAM < 0 || FAM >= 2) {
             const bool primary_p = FAM < 0 ? (dy <= 0.0) : (FAM == 2);
             const double sg = primary_p ? 1.0 : -1.0;
-            const double cx = primary_p ? cf[4] : cf[6];
-            const double cy = primary_p ? cf[5] : cf[7];
-            sflux(si, hi, true, sg, gi);
-            sflux(s0, h0, true, sg, g0);
+            const double cx = primary_p ? cf[4 * ld] : cf[6 * ld];
+            const double cy = primary_p ? cf[5 * ld] : cf[7 * ld];
+            fsflux(si, true, sg, gi);
+            fsflux(s0, true, sg, g0);
             const double w = fma(cx, dx, cy * dy);
 #pragma unroll
             for (int k = 0; k < 4; k++) {
@@ -383,9 +377,9 @@ __global__ void __launch_bounds__(kTB, MINB) k_flux(DG g, const double *__restri
                     acc[3][k] = a;
             }
             if (FAM < 0 && dy == 0.0) {
-                sflux(si, hi, true, -1.0, gi);
-                sflux(s0, h0, true, -1.0, g0);
-                const double w2 = fma(cf[6], dx, cf[7] * dy);
+                fsflux(si, true, -1.0, gi);
+                fsflux(s0, true, -1.0, g0);
+                const double w2 = fma(cf[6 * ld], dx, cf[7 * ld] * dy);
 #pragma unroll
                 for (int k = 0; k < 4; k++) acc[3][k] = fma(w2, gi[k] - g0[k], acc[3][k]);
             }
@@ -420,7 +414,7 @@ __global__ void __launch_bounds__(kTB, MINB) k_flux(DG g, const double *__restri
 // halved (one decoded state, eight accumulators), so twice the threads are
 // resident.  Per-edge arithmetic is exactly k_flux's (same device
 // functions), fused == split4 bitwise as before.
-template <bool XY, int FAM, int MINB>
+template <bool XY, int FAM, int MINB, int GK>
 __global__ void __launch_bounds__(kTB, MINB) k_flux2(DG g, const double *__restrict__ q,
                                                      const double *__restrict__ G, double *__restrict__ R,
                                                      double inv_gm1, double c_i0, int zero_boundary, Ctrl *c,
@@ -478,14 +472,12 @@ __global__ void __launch_bounds__(kTB, MINB) k_flux2(DG g, const double *__restr
         const bool ok = (t[3] < 0.0) && (t4o < 0.0);
         if (member && !ok) bad = true;
         const bool work = member && ok && interior;
-        EState st;
-        EShared sh;
-        decode(t[0], t[1], t[2], t[3], inv_gm1, st);
-        shared_of(st, c_i0, sh);
+        FState st;
+        fdecode<GK>(t[0], t[1], t[2], t[3], inv_gm1, c_i0, st);
         double gxf[4], gyf[4], snd[4], rcv[4];
         const bool px = dx <= 0.0, py = dy <= 0.0;
-        if (FAM < 2) sflux(st, sh, false, (FAM < 0 ? px : FAM == 0) ? 1.0 : -1.0, gxf);
-        if (FAM < 0 || FAM >= 2) sflux(st, sh, true, (FAM < 0 ? py : FAM == 2) ? 1.0 : -1.0, gyf);
+        if (FAM < 2) fsflux(st, false, (FAM < 0 ? px : FAM == 0) ? 1.0 : -1.0, gxf);
+        if (FAM < 0 || FAM >= 2) fsflux(st, true, (FAM < 0 ? py : FAM == 2) ? 1.0 : -1.0, gyf);
 #pragma unroll
         for (int k = 0; k < 4; k++) {
             if (FAM < 0) snd[k] = roleA ? gyf[k] : gxf[k];
@@ -517,7 +509,7 @@ __global__ void __launch_bounds__(kTB, MINB) k_flux2(DG g, const double *__restr
                 // lanes evaluate the '-' flux of the axis their PAIR needs:
                 // the x- exchange serves A, the y- exchange serves B
                 if (__any_sync(FULL, tx)) {
-                    sflux(st, sh, false, -1.0, gm);
+                    fsflux(st, false, -1.0, gm);
 #pragma unroll
                     for (int k = 0; k < 4; k++) {
                         const double o = __shfl_xor_sync(FULL, gm[k], 1);
@@ -525,7 +517,7 @@ __global__ void __launch_bounds__(kTB, MINB) k_flux2(DG g, const double *__restr
                     }
                 }
                 if (__any_sync(FULL, ty)) {
-                    sflux(st, sh, true, -1.0, gm);
+                    fsflux(st, true, -1.0, gm);
 #pragma unroll
                     for (int k = 0; k < 4; k++) {
                         const double o = __shfl_xor_sync(FULL, gm[k], 1);
@@ -577,6 +569,7 @@ __device__ __forceinline__ double warp_sum(double v)
     return v;
 }
 
+template <int GK>
 __global__ void __launch_bounds__(kTB) k_boundary(DG g, DB b, const double *__restrict__ q,
                                                   const double *__restrict__ G, double *__restrict__ R,
                                                   double inv_gm1, double c_i0, double fsr, double fsu,
@@ -601,15 +594,16 @@ __global__ void __launch_bounds__(kTB) k_boundary(DG g, DB b, const double *__re
     // free-stream Maxwellian in this point's frame (solver.py:365-369)
     double gfs[4] = {0, 0, 0, 0};
     if (!wall) {
-        EState fs;
+        FState fs;
+        const double beta = fsr / (2.0 * fsp);
         fs.rho = fsr;
         fs.u1 = ADD(MUL(fsu, tx), MUL(fsv, ty));
         fs.u2 = ADD(MUL(fsu, nx), MUL(fsv, ny));
-        fs.beta = fsr / (2.0 * fsp);
-        fs.r = __drcp_rn(2.0 * fs.beta);
-        EShared h;
-        shared_of(fs, c_i0, h);
-        sflux(fs, h, true, -1.0, gfs);
+        fs.r = 1.0 / (2.0 * beta);
+        fs.sb = sqrt(beta);
+        fs.bc = rsqrt(beta) * kInv2SqrtPi;
+        fs.i0 = c_i0 * fs.r;
+        fsflux(fs, true, -1.0, gfs);
     }
     double acc[3][4];
 #pragma unroll
@@ -638,31 +632,28 @@ __global__ void __launch_bounds__(kTB) k_boundary(DG g, DB b, const double *__re
                 continue;
             }
             // _frame_q (solver.py:238-242): rotate the velocity pair
-            EState si, s0;
-            decode(ti[0], ADD(MUL(tx, ti[1]), MUL(ty, ti[2])), ADD(MUL(nx, ti[1]), MUL(ny, ti[2])), ti[3],
-                   inv_gm1, si);
-            decode(t0[0], ADD(MUL(tx, t0[1]), MUL(ty, t0[2])), ADD(MUL(nx, t0[1]), MUL(ny, t0[2])), t0[3],
-                   inv_gm1, s0);
-            EShared hi, h0;
-            shared_of(si, c_i0, hi);
-            shared_of(s0, c_i0, h0);
+            FState si, s0;
+            fdecode<GK>(ti[0], ADD(MUL(tx, ti[1]), MUL(ty, ti[2])), ADD(MUL(nx, ti[1]), MUL(ny, ti[2])), ti[3],
+                        inv_gm1, c_i0, si);
+            fdecode<GK>(t0[0], ADD(MUL(tx, t0[1]), MUL(ty, t0[2])), ADD(MUL(nx, t0[1]), MUL(ny, t0[2])), t0[3],
+                        inv_gm1, c_i0, s0);
             double gi[4], g0[4], dg[4];
             if (f < 2) {
                 const double sg = f == 0 ? 1.0 : -1.0;
-                sflux(si, hi, false, sg, gi);
-                sflux(s0, h0, false, sg, g0);
+                fsflux(si, false, sg, gi);
+                fsflux(s0, false, sg, g0);
 #pragma unroll
                 for (int k = 0; k < 4; k++) dg[k] = gi[k] - g0[k];
             } else if (wall) {
-                sflux(si, hi, true, -1.0, gi);
-                sflux(s0, h0, true, -1.0, g0);
+                fsflux(si, true, -1.0, gi);
+                fsflux(s0, true, -1.0, g0);
 #pragma unroll
                 for (int k = 0; k < 4; k++) dg[k] = gi[k] - g0[k];
             } else {
                 double gm[4];
-                sflux(si, hi, true, 1.0, gi);
-                sflux(s0, h0, true, 1.0, g0);
-                sflux(si, hi, true, -1.0, gm);
+                fsflux(si, true, 1.0, gi);
+                fsflux(s0, true, 1.0, g0);
+                fsflux(si, true, -1.0, gm);
 #pragma unroll
                 for (int k = 0; k < 4; k++) dg[k] = (gi[k] - g0[k]) + (gm[k] - gfs[k]);
             }
@@ -748,6 +739,27 @@ struct IterOut {
     double tol;
 };
 
+// End of an outer iteration, run by one thread of the last stage-4 block:
+// residue_norm = sqrt(fsum(drho^2)/n) (solver.py:418-421), history,
+// convergence test (solver.py:557-559), counters.  Out of line so the
+// per-point update keeps its small register footprint.
+__device__ __noinline__ void close_iteration(Ctrl *c, const unsigned long long *limbs, int n, IterOut io)
+{
+    const int ep = c->epoch;
+    const unsigned long long st = *(volatile unsigned long long *)&c->state;
+    if (st == 0ull) {
+        const double res = sqrt(accum_round(limbs) / (double)n);
+        const int it = c->iter;
+        const int h = it - io.hist_base;
+        if (h >= 0 && h < io.cap) io.history[h] = res;
+        if (io.tol > 0.0 && res <= io.tol) c->state = ((unsigned long long)seq_of(ep, kStageFinal, 0) << 2) | 2ull;
+        c->iter = it + 1;
+    }
+    c->blocks_done = 0u;
+    c->epoch = ep + 1;
+    __threadfence();
+}
+
 template <int STAGE>
 __global__ void __launch_bounds__(kTB) k_update(DG g, double *__restrict__ Uo, double *__restrict__ Us,
                                                 const double *__restrict__ R, double *__restrict__ dt,
@@ -806,29 +818,11 @@ __global__ void __launch_bounds__(kTB) k_update(DG g, double *__restrict__ Uo, d
         __syncthreads();
         if (threadIdx.x == 0) last = atomicAdd(&c->blocks_done, 1u) == gridDim.x - 1;
         __syncthreads();
-        if (last && threadIdx.x == 0) {
+        if (last) {
             __threadfence();
-            volatile unsigned long long *vl = c->limbs;
-            unsigned long long lm[kLimbs];
-            for (int l = 0; l < kLimbs; l++) {
-                lm[l] = vl[l];
-                vl[l] = 0ull;
-            }
-            const int ep = c->epoch;
-            const unsigned long long st = *(volatile unsigned long long *)&c->state;
-            if (st == 0ull) {
-                // residue_norm finish: sqrt(fsum(drho^2)/n) (solver.py:418-421)
-                const double res = sqrt(accum_round(lm) / (double)g.n);
-                const int it = c->iter;
-                const int h = it - io.hist_base;
-                if (h >= 0 && h < io.cap) io.history[h] = res;
-                if (io.tol > 0.0 && res <= io.tol)  // solver.py:557-559
-                    c->state = ((unsigned long long)seq_of(ep, kStageFinal, 0) << 2) | 2ull;
-                c->iter = it + 1;
-            }
-            c->blocks_done = 0u;
-            c->epoch = ep + 1;
-            __threadfence();
+            for (int t = threadIdx.x; t < kLimbs; t += blockDim.x) sl[t] = atomicExch(&c->limbs[t], 0ull);
+            __syncthreads();
+            if (threadIdx.x == 0) close_iteration(c, sl, g.n, io);
         }
     }
 }
@@ -1083,17 +1077,18 @@ __global__ void k_op_split_flux(int n, const double *pr, int yaxis, double sg, d
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    EState s;
+    FState s;
     s.rho = pr[i];
     s.u1 = pr[n + i];
     s.u2 = pr[2 * n + i];
     const double p = pr[3 * n + i];
-    s.beta = s.rho / (2.0 * p);
-    s.r = __drcp_rn(2.0 * s.beta);
-    EShared h;
-    shared_of(s, (2.0 - gamma) / (gamma - 1.0), h);
+    const double beta = s.rho / (2.0 * p);
+    s.r = 1.0 / (2.0 * beta);
+    s.sb = sqrt(beta);
+    s.bc = rsqrt(beta) * kInv2SqrtPi;
+    s.i0 = ((2.0 - gamma) / (gamma - 1.0)) * s.r;
     double g[4];
-    sflux(s, h, yaxis != 0, sg, g);
+    fsflux(s, yaxis != 0, sg, g);
     for (int k = 0; k < 4; k++) G[(long long)k * n + i] = g[k];
 }
 
@@ -1185,5 +1180,23 @@ __global__ void k_fp64_peak(int iters, double seed, double *out)
 #pragma unroll
     for (int k = 0; k < 8; k++) s += a[k];
     if (s == 12345.678) out[0] = s;  // keep the chains alive
+}
+}  // namespace kmf
+
+namespace kmf {
+// accuracy probe of the flux-path transcendentals (tests/test_gpu_fastmath.py)
+__global__ void k_fastmath_probe(int n, const double *x, int which, double *out)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double v = x[i];
+    double r;
+    switch (which) {
+    case 0: r = fexp(v); break;
+    case 1: r = ferf(v, fexp(-(v * v))); break;
+    case 2: r = frcp(v); break;
+    default: r = frsqrt(v); break;
+    }
+    out[i] = r;
 }
 }  // namespace kmf

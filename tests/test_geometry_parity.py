@@ -146,3 +146,15 @@ def test_text_grid_errors():
         read_point_cloud(b"2\n0 0 0\n")
     with pytest.raises(ValueError):
         read_point_cloud(b"1\n0 0 1\n")
+
+
+def test_hilbert_permutation_is_local_and_deterministic(small_naca):
+    from paper_2108_07031_b200 import reorder
+
+    p = reorder.permutation(small_naca, "hilbert")
+    assert np.array_equal(np.sort(p), np.arange(small_naca.n_points))
+    assert np.array_equal(p, reorder.permutation(small_naca, "hilbert"))
+    assert reorder.permutation(small_naca, "natural") is None
+    # the 2x2 grid in Hilbert order visits (0,0),(0,1),(1,1),(1,0)
+    k = reorder.hilbert_keys(np.array([0.0, 0.0, 1.0, 1.0]), np.array([0.0, 1.0, 1.0, 0.0]), bits=1)
+    assert list(k) == [0, 1, 2, 3]

@@ -1,8 +1,8 @@
-run() { echo "== $*" >> gpurun_out/sweep2.log; env "$@" timeout 120 python tools/quick_perf.py 800 200 1.03 50 2>&1 | grep -E "instrument|stage" >> gpurun_out/sweep2.log; }
-run KMF_FLUX_IMPL=1 KMF_QG_NC=2 KMF_QG_UNROLL=1
-run KMF_FLUX_IMPL=2 KMF_FLUX_MINB=4 KMF_QG_NC=2 KMF_QG_UNROLL=2
-run KMF_FLUX_IMPL=2 KMF_FLUX_MINB=5 KMF_QG_NC=1 KMF_QG_UNROLL=2
-run KMF_FLUX_IMPL=2 KMF_FLUX_MINB=6 KMF_QG_NC=1 KMF_QG_UNROLL=4
-run KMF_FLUX_IMPL=2 KMF_FLUX_MINB=4 KMF_QG_NC=2 KMF_QG_UNROLL=4
-run KMF_FLUX_IMPL=2 KMF_FLUX_MINB=4 KMF_QG_NC=4 KMF_QG_UNROLL=2
-run KMF_FLUX_IMPL=2 KMF_FLUX_MINB=4 KMF_QG_NC=1 KMF_QG_UNROLL=1
+# development sweep of launch shapes / orders (not part of the bench)
+run() { echo "== $*" >> gpurun_out/sweep4.log; env "$@" timeout 120 python tools/quick_perf.py 800 200 1.03 50 2>&1 | grep -E "instrument=False|stage" >> gpurun_out/sweep4.log; }
+run KMF_ORDER=natural
+run KMF_ORDER=hilbert
+run KMF_ORDER=hilbert KMF_QG_NC=4
+run KMF_ORDER=hilbert KMF_QG_NC=1
+run KMF_ORDER=hilbert KMF_QG_UNROLL=2
+run KMF_ORDER=hilbert KMF_FLUX_MINB=4

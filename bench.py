@@ -341,7 +341,8 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", choices=tuple(CONFIGS), default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--order", choices=("natural", "hilbert"), default=os.environ.get("KMF_ORDER", "natural"),
+    ap.add_argument("--order", choices=("natural", "hilbert", "ringtile2", "ringtile4", "ringtile8"),
+                    default=os.environ.get("KMF_ORDER", "natural"),
                     help="device point order (bitwise neutral, locality only)")
     args = ap.parse_args()
     if args.impl == "reference":

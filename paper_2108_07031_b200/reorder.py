@@ -17,7 +17,7 @@ from __future__ import annotations
 
 import numpy as np
 
-ORDERS = ("natural", "hilbert")
+ORDERS = ("natural", "hilbert", "ringtile2", "ringtile4", "ringtile8")
 BITS = 21
 
 
@@ -49,11 +49,32 @@ def hilbert_keys(x: np.ndarray, y: np.ndarray, bits: int = BITS) -> np.ndarray:
     return d
 
 
-def permutation(cloud, order: str = "hilbert") -> np.ndarray | None:
-    """perm[k] = caller point stored in device slot k (None for natural)."""
+def ring_tiles(n: int, m: int, tile_rings: int = 4, width: int = 32) -> np.ndarray:
+    """Tile order for ring-structured clouds (point r*m + a is angle a of
+    ring r, as generate_naca_cloud numbers them): bands of `tile_rings`
+    rings, each cut into `width`-point angular tiles stored ring by ring.
+    A warp still owns `width` angularly consecutive points (so its slot-s
+    neighbours stay consecutive and coalesced) while a block's warps stack
+    radially and share their neighbour rings in L1."""
+    if n % m:
+        raise ValueError("ring tiling needs n to be a multiple of the ring size m")
+    k = np.arange(n, dtype=np.int64)
+    r, a = k // m, k % m
+    return np.lexsort((a % width, r % tile_rings, a // width, r // tile_rings)).astype(np.int64)
+
+
+def permutation(cloud, order: str = "hilbert", ring_size: int | None = None) -> np.ndarray | None:
+    """perm[k] = caller point stored in device slot k (None for natural).
+
+    "ringtile" needs the ring size m of a generator cloud (ring_size, or the
+    number of wall points when the cloud has one wall ring)."""
     if order not in ORDERS:
         raise ValueError(f"order must be one of {ORDERS}")
     if order == "natural":
         return None
+    if order.startswith("ringtile"):
+        m = ring_size or int((cloud.flag == 1).sum())
+        rows = int(order[len("ringtile"):] or 4)
+        return ring_tiles(cloud.n_points, m, rows)
     keys = hilbert_keys(cloud.x, cloud.y)
     return np.lexsort((np.arange(keys.size), keys)).astype(np.int64)

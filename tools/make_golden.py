@@ -64,6 +64,7 @@ from kmf.solver import (
 )
 from kmf.state import (
     FlowState,
+    PositivityError,
     Primitives,
     conserved_to_primitives,
     free_stream,
@@ -334,7 +335,16 @@ def _big(name, params, mach, aoa, iters, store_final=True):
     meta["digests"]["init"] = digest(prims_arr(init))
     print(f"{name}: n={cloud.n_points} built in {t_build:.1f}s", flush=True)
     t0 = time.perf_counter()
-    res = solve(cfg, cloud, conn, instrument=False)
+    try:
+        res = solve(cfg, cloud, conn, instrument=False)
+    except PositivityError as exc:
+        # the reference itself breaks down (config 1 does at iteration 407):
+        # record the failure, then the state just before it
+        meta["failure"] = {"message": str(exc), "indices": [int(i) for i in exc.indices]}
+        it = int(str(exc).split(":")[0].split()[1])
+        meta["iters"] = it - 1
+        cfg = SolverConfig(mach=mach, aoa_deg=aoa, cfl=0.2, n_outer=it - 1, threads=8)
+        res = solve(cfg, cloud, conn, instrument=False)
     meta["solve_seconds"] = time.perf_counter() - t0
     arrays = {"history": res.residue_history}
     fin = prims_arr(res.primitives)

@@ -214,6 +214,28 @@ int kmf_op_residue(int64_t n, const double *U_new, const double *U_old, double *
 /* last global (context-free) error string */
 const char *kmf_strerror(void);
 
+/* ---- multi-GPU partition (paper_2108_07031_b200/partition.py) ------------ *
+ * A partitioned context holds its rank's owned points (local slots
+ * 0..n_owned-1) followed by an (n_inner+2)-layer halo.  Flux, boundary and
+ * update launches cover the owned points; the q-gradient launches the whole
+ * local set; after every stage the halo q is refreshed from its owners;
+ * the residue limbs are summed across ranks before the iteration close, so
+ * every rank's arithmetic -- and the history -- is bitwise the single-GPU
+ * one.  send_slots/recv_slots are concatenated per peer (peer_ranks order):
+ * owned local slots to send, halo local slots to fill. */
+int kmf_set_partition(kmf_ctx *ctx, int64_t n_owned, int64_t n_global, int rank, int nranks, int npeers,
+                      const int *peer_ranks, const int64_t *send_counts, const int64_t *send_slots,
+                      const int64_t *recv_counts, const int64_t *recv_slots);
+/* NCCL transport (one process per GPU): halo send/recv and the limb
+ * all-reduce are captured in the iteration graph; kmf_run then works as for
+ * a single domain.  libnccl.so.2 is loaded at run time. */
+int kmf_nccl_get_unique_id(void *out128);
+int kmf_nccl_init(kmf_ctx *ctx, const void *id128, int rank, int nranks);
+/* one process driving all ranks' contexts (same or peer GPUs): halo moves
+ * by device/peer copies, limbs summed on the host */
+int kmf_run_group(kmf_ctx **ctxs, int nctx, const kmf_params *p, int n_iter, double *history, int *iters_done,
+                  int *converged);
+
 /* ---- measurement support (bench.py) -------------------------------------- */
 
 /* n_steps outer iterations, each one CUDA-graph launch bracketed by CUDA

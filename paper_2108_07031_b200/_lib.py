@@ -117,6 +117,12 @@ def lib():
         "kmf_bench_steps": (C.c_int, [vp, C.POINTER(Params), C.c_int, C.c_int64, _dp, _dp, C.POINTER(C.c_int)]),
         "kmf_fp64_peak": (C.c_int, [_dp]),
         "kmf_fastmath_probe": (C.c_int, [C.c_int64, _dp, C.c_int, _dp]),
+        "kmf_set_partition": (C.c_int, [vp, C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int),
+                                        _i64p, _i64p, _i64p, _i64p]),
+        "kmf_nccl_get_unique_id": (C.c_int, [C.c_void_p]),
+        "kmf_nccl_init": (C.c_int, [vp, C.c_void_p, C.c_int, C.c_int]),
+        "kmf_run_group": (C.c_int, [C.POINTER(vp), C.c_int, C.POINTER(Params), C.c_int, _dp, C.POINTER(C.c_int),
+                                    C.POINTER(C.c_int)]),
         "kmf_host_alloc": (C.c_void_p, [C.c_int64]),
         "kmf_host_free": (None, [C.c_void_p]),
     }
@@ -136,7 +142,8 @@ EXPORTED = (
     "kmf_op_boundary", "kmf_op_primitives_to_q", "kmf_op_q_to_primitives",
     "kmf_op_primitives_to_conserved", "kmf_op_conserved_to_primitives", "kmf_op_split_flux",
     "kmf_op_full_flux", "kmf_op_state_update", "kmf_op_residue", "kmf_bench_steps", "kmf_fp64_peak", "kmf_fastmath_probe",
-    "kmf_host_alloc", "kmf_host_free",
+    "kmf_host_alloc", "kmf_host_free", "kmf_set_partition", "kmf_nccl_get_unique_id", "kmf_nccl_init",
+    "kmf_run_group",
 )
 
 

@@ -6,6 +6,8 @@
 #include "kmf_kernels.cuh"
 
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: the library dlopens libnccl at run time
 
 #include <algorithm>
 #include <cmath>
@@ -130,11 +132,25 @@ struct kmf_ctx {
     std::vector<long long> err_idx;
     int last_G = 0;  // which gradient buffer holds the final gradients of the last stage
 
+    // partition (multi-GPU, partition.py): owned points first, halo after
+    bool dist_on = false;
+    int n_owned = 0, rank = 0, nranks = 1;
+    long long n_global = 0;
+    std::vector<int> peer_rank;
+    std::vector<long long> send_off, send_cnt, recv_off, recv_cnt;  // points, per peer
+    long long send_total = 0, recv_total = 0;
+    DBuf<int> ps_slot, ps_base, ps_stride, pr_slot, pr_base, pr_stride;
+    DBuf<double> sendbuf, recvbuf;
+    void *nccl = nullptr;  // ncclComm_t when the NCCL transport is initialised
+    void (*nccl_destroy)(void *) = nullptr;
+
     DG dg() const
     {
         DG g;
         g.n = n;
         g.ld = ld;
+        g.n_act = dist_on ? n_owned : n;
+        g.n_norm = dist_on ? (int)n_global : n;
         g.x = x.p;
         g.y = y.p;
         g.flag = flag.p;
@@ -167,6 +183,7 @@ struct kmf_ctx {
     }
     ~kmf_ctx()
     {
+        if (nccl && nccl_destroy) nccl_destroy(nccl);
         if (exec1) cudaGraphExecDestroy(exec1);
         if (execU) cudaGraphExecDestroy(execU);
         if (execB) cudaGraphExecDestroy(execB);
@@ -643,30 +660,125 @@ enum { ITER_PLAIN = 0, ITER_INSTRUMENT = 1, ITER_BENCH = 2 };
 // per iteration, per-stage seconds accumulated (solver.py:461-474).
 // ITER_BENCH: captured into a graph with external event-record nodes around
 // each interior flux launch (the roofline kernel, timed on its own stream).
-void enqueue_iteration(kmf_ctx *c, const kmf_params *p, double *hist, int hist_base, int cap, int how)
+// ------------------------------------------------------------- NCCL (dlopen)
+// The library does not link NCCL: the multi-process transport resolves it at
+// run time (libnccl.so.2, torch's or the system's), so single-GPU use never
+// needs it.
+struct NcclApi {
+    bool ok = false;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char *(*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi &nccl_api()
+{
+    static NcclApi api;
+    static bool tried = false;
+    if (tried) return api;
+    tried = true;
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return api;
+#define KMF_SYM(field, name) api.field = reinterpret_cast<decltype(api.field)>(dlsym(h, name))
+    KMF_SYM(GetUniqueId, "ncclGetUniqueId");
+    KMF_SYM(CommInitRank, "ncclCommInitRank");
+    KMF_SYM(CommDestroy, "ncclCommDestroy");
+    KMF_SYM(Send, "ncclSend");
+    KMF_SYM(Recv, "ncclRecv");
+    KMF_SYM(AllReduce, "ncclAllReduce");
+    KMF_SYM(GroupStart, "ncclGroupStart");
+    KMF_SYM(GroupEnd, "ncclGroupEnd");
+    KMF_SYM(GetErrorString, "ncclGetErrorString");
+#undef KMF_SYM
+    api.ok = api.GetUniqueId && api.CommInitRank && api.Send && api.Recv && api.AllReduce && api.GroupStart &&
+             api.GroupEnd;
+    return api;
+}
+
+// halo pack on the owner side: q of the points each peer needs
+void enqueue_pack(kmf_ctx *c, cudaStream_t s)
+{
+    if (c->send_total)
+        k_halo_pack<<<nblk(c->send_total), kTB, 0, s>>>((int)c->send_total, c->ps_slot.p, c->ps_base.p,
+                                                        c->ps_stride.p, c->q.p, c->ld, c->sendbuf.p);
+}
+
+void enqueue_unpack(kmf_ctx *c, cudaStream_t s)
+{
+    if (c->recv_total)
+        k_halo_unpack<<<nblk(c->recv_total), kTB, 0, s>>>((int)c->recv_total, c->pr_slot.p, c->pr_base.p,
+                                                          c->pr_stride.p, c->recvbuf.p, c->q.p, c->ld);
+}
+
+// NCCL transport: one grouped send/recv per peer of each rank's halo q, and
+// the exact residue limbs all-reduced before the iteration close; all on the
+// solver stream, so the whole iteration stays one graph.
+void enqueue_exchange_nccl(kmf_ctx *c)
+{
+    NcclApi &api = nccl_api();
+    ncclComm_t comm = (ncclComm_t)c->nccl;
+    enqueue_pack(c, c->s0);
+    api.GroupStart();
+    for (size_t k = 0; k < c->peer_rank.size(); k++) {
+        if (c->send_cnt[k])
+            api.Send(c->sendbuf.p + 4 * c->send_off[k], 4 * c->send_cnt[k], ncclDouble, c->peer_rank[k], comm, c->s0);
+        if (c->recv_cnt[k])
+            api.Recv(c->recvbuf.p + 4 * c->recv_off[k], 4 * c->recv_cnt[k], ncclDouble, c->peer_rank[k], comm, c->s0);
+    }
+    api.GroupEnd();
+    enqueue_unpack(c, c->s0);
+}
+
+void enqueue_close_nccl(kmf_ctx *c, IterOut io)
+{
+    NcclApi &api = nccl_api();
+    api.AllReduce(c->ctrl.p->limbs, c->ctrl.p->limbs, kLimbs, ncclUint64, ncclSum, (ncclComm_t)c->nccl, c->s0);
+    k_close<<<1, kTB, 0, c->s0>>>(c->ctrl.p, (int)c->n_global, io);
+}
+
+// One RK stage (solver.py:524-549) on s0 (boundary on a forked branch).
+void enqueue_stage(kmf_ctx *c, const kmf_params *p, int stage, IterOut io, int how)
 {
     Ctrl *ctl = c->ctrl.p;
     const bool inst = how == ITER_INSTRUMENT, bench = how == ITER_BENCH;
+    cudaEvent_t *e = &c->ev[4 * (stage - 1)];
+    if (inst) cudaEventRecord(e[0], c->s0);
+    int which = launch_qgrad(c, c->s0, stage, p->n_inner, ctl, 0);
+    const double *G = which ? c->GB.p : c->GA.p;
+    c->last_G = which;
+    if (inst) cudaEventRecord(e[1], c->s0);
+    cudaEventRecord(c->fork, c->s0);
+    cudaStreamWaitEvent(c->s1, c->fork, 0);
+    launch_boundary(c, c->s1, G, p->fs, p->gamma, ctl, stage);
+    cudaEventRecord(c->join, c->s1);
+    if (bench) cudaEventRecordWithFlags(c->evb[2 * (stage - 1)], c->s0, cudaEventRecordExternal);
+    launch_flux(c, c->s0, G, p->mode, p->gamma, 0, ctl, stage);
+    if (bench) cudaEventRecordWithFlags(c->evb[2 * (stage - 1) + 1], c->s0, cudaEventRecordExternal);
+    cudaStreamWaitEvent(c->s0, c->join, 0);
+    if (inst) cudaEventRecord(e[2], c->s0);
+    io.close_in_kernel = c->dist_on ? 0 : 1;
+    launch_update(c, c->s0, stage, p->gamma, p->cfl, io);
+    if (inst) cudaEventRecord(e[3], c->s0);
+}
+
+void enqueue_iteration(kmf_ctx *c, const kmf_params *p, double *hist, int hist_base, int cap, int how)
+{
+    const bool inst = how == ITER_INSTRUMENT;
+    IterOut io{hist, hist_base, cap, p->convergence_tol, 1};
+    const bool nccl = c->dist_on && c->nccl;
     for (int stage = 1; stage <= 4; stage++) {
-        cudaEvent_t *e = &c->ev[4 * (stage - 1)];
-        if (inst) cudaEventRecord(e[0], c->s0);
-        int which = launch_qgrad(c, c->s0, stage, p->n_inner, ctl, 0);
-        const double *G = which ? c->GB.p : c->GA.p;
-        c->last_G = which;
-        if (inst) cudaEventRecord(e[1], c->s0);
-        cudaEventRecord(c->fork, c->s0);
-        cudaStreamWaitEvent(c->s1, c->fork, 0);
-        launch_boundary(c, c->s1, G, p->fs, p->gamma, ctl, stage);
-        cudaEventRecord(c->join, c->s1);
-        if (bench) cudaEventRecordWithFlags(c->evb[2 * (stage - 1)], c->s0, cudaEventRecordExternal);
-        launch_flux(c, c->s0, G, p->mode, p->gamma, 0, ctl, stage);
-        if (bench) cudaEventRecordWithFlags(c->evb[2 * (stage - 1) + 1], c->s0, cudaEventRecordExternal);
-        cudaStreamWaitEvent(c->s0, c->join, 0);
-        if (inst) cudaEventRecord(e[2], c->s0);
-        IterOut io{hist, hist_base, cap, p->convergence_tol};
-        launch_update(c, c->s0, stage, p->gamma, p->cfl, io);
-        if (inst) cudaEventRecord(e[3], c->s0);
+        enqueue_stage(c, p, stage, io, how);
+        if (nccl) enqueue_exchange_nccl(c);
     }
+    if (nccl) enqueue_close_nccl(c, io);
     if (inst) {
         // residue_norm and the iteration close run inside the stage-4 update
         cudaEventSynchronize(c->ev[15]);
@@ -828,6 +940,10 @@ int kmf_run(kmf_ctx *c, const kmf_params *p, int n_iter, double *history, int *i
     if (p->n_inner < 1 || !(p->gamma > 1.0 && p->gamma < 2.0) || !(p->cfl > 0.0 && p->cfl <= 1.0) ||
         (p->mode != 0 && p->mode != 1)) {
         set_msg("kmf_run: invalid parameters");
+        return KMF_EINVAL;
+    }
+    if (c->dist_on && !c->nccl) {
+        set_msg("kmf_run: partitioned context without NCCL (use kmf_nccl_init or kmf_run_group)");
         return KMF_EINVAL;
     }
     CK(cudaSetDevice(c->device));
@@ -1376,7 +1492,8 @@ int kmf_bench_steps(kmf_ctx *c, const kmf_params *p, int n_steps, int64_t flush_
     Ctrl fin;
     CK(cudaMemcpy(&fin, c->ctrl.p, sizeof fin, cudaMemcpyDeviceToHost));
     if (launches_per_step)
-        *launches_per_step = 4 * (1 + p->n_inner + (p->mode ? 4 : 1) + (c->nb > 0 ? 1 : 0) + 1);  // the iteration close is fused into update<4>
+        *launches_per_step = 4 * (1 + p->n_inner + (p->mode ? 4 : 1) + (c->nb > 0 ? 1 : 0) + 1) +  // the iteration close is fused into update<4>
+                             ((c->dist_on && c->nccl) ? 4 * ((c->send_total ? 1 : 0) + (c->recv_total ? 1 : 0)) + 1 : 0);
     if ((fin.state & 3ull) == 1ull) {
         set_msg("kmf_bench_steps: positivity failure at iteration %d", fin.err_iter);
         return KMF_EPOSITIVITY;
@@ -1442,5 +1559,243 @@ extern "C" int kmf_fastmath_probe(int64_t n, const double *x, int which, double 
     k_fastmath_probe<<<nblk(n), kTB>>>((int)n, dx, which, dout);
     CK(cudaGetLastError());
     CK(cudaMemcpy(out, dout, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    return KMF_OK;
+}
+
+// ============================================================ multi-GPU ABI
+
+extern "C" int kmf_set_partition(kmf_ctx *c, int64_t n_owned, int64_t n_global, int rank, int nranks, int npeers,
+                                 const int *peer_ranks, const int64_t *send_counts, const int64_t *send_slots,
+                                 const int64_t *recv_counts, const int64_t *recv_slots)
+{
+    if (!c || n_owned <= 0 || n_owned > c->n || n_global < n_owned || npeers < 0 || rank < 0 || rank >= nranks)
+        return KMF_EINVAL;
+    if (c->has_perm) {
+        set_msg("kmf_set_partition: partitioned contexts use the natural local order");
+        return KMF_EINVAL;
+    }
+    CK(cudaSetDevice(c->device));
+    c->n_owned = (int)n_owned;
+    c->n_global = n_global;
+    c->rank = rank;
+    c->nranks = nranks;
+    c->peer_rank.assign(peer_ranks, peer_ranks + npeers);
+    c->send_off.assign(npeers, 0);
+    c->send_cnt.assign(npeers, 0);
+    c->recv_off.assign(npeers, 0);
+    c->recv_cnt.assign(npeers, 0);
+    long long so = 0, ro = 0;
+    for (int k = 0; k < npeers; k++) {
+        c->send_off[k] = so;
+        c->send_cnt[k] = send_counts[k];
+        so += send_counts[k];
+        c->recv_off[k] = ro;
+        c->recv_cnt[k] = recv_counts[k];
+        ro += recv_counts[k];
+    }
+    c->send_total = so;
+    c->recv_total = ro;
+    auto build = [&](const int64_t *slots, const std::vector<long long> &off, const std::vector<long long> &cnt,
+                     long long total, DBuf<int> &sl, DBuf<int> &ba, DBuf<int> &st, bool owned_side) -> int {
+        std::vector<int> s(std::max<long long>(total, 1)), b(s.size()), t(s.size());
+        for (int k = 0; k < npeers; k++)
+            for (long long e = 0; e < cnt[k]; e++) {
+                const long long idx = off[k] + e;
+                const long long slot = slots[idx];
+                if (slot < 0 || slot >= c->n || (owned_side && slot >= n_owned) || (!owned_side && slot < n_owned)) {
+                    set_msg("kmf_set_partition: slot %lld out of range", slot);
+                    return KMF_EINVAL;
+                }
+                s[idx] = (int)slot;
+                b[idx] = (int)(4 * off[k] + e);
+                t[idx] = (int)cnt[k];
+            }
+        CK(sl.upload(s.data(), s.size()));
+        CK(ba.upload(b.data(), b.size()));
+        CK(st.upload(t.data(), t.size()));
+        return KMF_OK;
+    };
+    if (int rc = build(send_slots, c->send_off, c->send_cnt, so, c->ps_slot, c->ps_base, c->ps_stride, true)) return rc;
+    if (int rc = build(recv_slots, c->recv_off, c->recv_cnt, ro, c->pr_slot, c->pr_base, c->pr_stride, false))
+        return rc;
+    CK(c->sendbuf.alloc(4 * (size_t)std::max<long long>(so, 1)));
+    CK(c->recvbuf.alloc(4 * (size_t)std::max<long long>(ro, 1)));
+    c->dist_on = true;
+    // graphs captured before the partition are stale
+    if (c->exec1) cudaGraphExecDestroy(c->exec1), c->exec1 = nullptr;
+    if (c->execU) cudaGraphExecDestroy(c->execU), c->execU = nullptr;
+    if (c->execB) cudaGraphExecDestroy(c->execB), c->execB = nullptr;
+    return KMF_OK;
+}
+
+extern "C" int kmf_nccl_get_unique_id(void *out128)
+{
+    if (!out128) return KMF_EINVAL;
+    NcclApi &api = nccl_api();
+    if (!api.ok) {
+        set_msg("libnccl.so.2 not loadable");
+        return KMF_ENCCL;
+    }
+    ncclUniqueId id;
+    if (api.GetUniqueId(&id) != ncclSuccess) return KMF_ENCCL;
+    std::memcpy(out128, &id, sizeof id);
+    return KMF_OK;
+}
+
+extern "C" int kmf_nccl_init(kmf_ctx *c, const void *id128, int rank, int nranks)
+{
+    if (!c || !id128 || rank < 0 || rank >= nranks) return KMF_EINVAL;
+    NcclApi &api = nccl_api();
+    if (!api.ok) {
+        set_msg("libnccl.so.2 not loadable");
+        return KMF_ENCCL;
+    }
+    CK(cudaSetDevice(c->device));
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof id);
+    ncclComm_t comm;
+    ncclResult_t r = api.CommInitRank(&comm, nranks, id, rank);
+    if (r != ncclSuccess) {
+        set_msg("ncclCommInitRank: %s", api.GetErrorString ? api.GetErrorString(r) : "error");
+        return KMF_ENCCL;
+    }
+    c->nccl = comm;
+    c->nccl_destroy = [](void *p) {
+        NcclApi &a = nccl_api();
+        if (a.CommDestroy) a.CommDestroy((ncclComm_t)p);
+    };
+    if (c->exec1) cudaGraphExecDestroy(c->exec1), c->exec1 = nullptr;
+    if (c->execU) cudaGraphExecDestroy(c->execU), c->execU = nullptr;
+    if (c->execB) cudaGraphExecDestroy(c->execB), c->execB = nullptr;
+    return KMF_OK;
+}
+
+// Single-process driver for several partitioned contexts (one per rank, on
+// the same or different GPUs): per stage every context runs its kernels,
+// then halo q moves by device-to-device / peer copies; the residue limbs
+// are summed on the host (exact integers) and every context closes the
+// iteration with the same total.  Used by the multi-rank parity tests on a
+// single GPU and as a one-process multi-GPU mode.
+extern "C" int kmf_run_group(kmf_ctx **ctxs, int nctx, const kmf_params *p, int n_iter, double *history,
+                             int *iters_done, int *converged)
+{
+    if (!ctxs || nctx < 1 || !p || n_iter < 0) return KMF_EINVAL;
+    std::vector<kmf_ctx *> byrank(nctx, nullptr);
+    for (int k = 0; k < nctx; k++) {
+        kmf_ctx *c = ctxs[k];
+        if (!c || !c->dist_on || c->nranks != nctx || byrank[c->rank] || !c->have_state) {
+            set_msg("kmf_run_group: contexts must be partitioned ranks 0..n-1 with state");
+            return KMF_EINVAL;
+        }
+        byrank[c->rank] = c;
+    }
+    if (iters_done) *iters_done = 0;
+    if (converged) *converged = 0;
+    if (n_iter == 0) return KMF_OK;
+    for (kmf_ctx *c : byrank) {
+        CK(cudaSetDevice(c->device));
+        if (int rc = seed_state(c, p->gamma, p->cfl)) return rc;
+        if ((int)c->history.n < n_iter) CK(c->history.alloc(n_iter));
+        Ctrl init;
+        std::memset(&init, 0, sizeof init);
+        init.iter = 1;
+        init.epoch = 1;
+        CK(cudaMemcpy(c->ctrl.p, &init, sizeof init, cudaMemcpyHostToDevice));
+    }
+    auto sync_all = [&]() -> int {
+        for (kmf_ctx *c : byrank) {
+            CK(cudaSetDevice(c->device));
+            CK(cudaStreamSynchronize(c->s0));
+        }
+        return KMF_OK;
+    };
+    for (int it = 0; it < n_iter; it++) {
+        for (int stage = 1; stage <= 4; stage++) {
+            for (kmf_ctx *c : byrank) {
+                CK(cudaSetDevice(c->device));
+                IterOut io{c->history.p, 1, n_iter, p->convergence_tol, 0};
+                enqueue_stage(c, p, stage, io, ITER_PLAIN);
+                enqueue_pack(c, c->s0);
+            }
+            if (int rc = sync_all()) return rc;
+            for (kmf_ctx *dst : byrank)
+                for (size_t k = 0; k < dst->peer_rank.size(); k++) {
+                    kmf_ctx *src = byrank[dst->peer_rank[k]];
+                    size_t j = 0;
+                    while (j < src->peer_rank.size() && src->peer_rank[j] != dst->rank) j++;
+                    if (j == src->peer_rank.size() || src->send_cnt[j] != dst->recv_cnt[k]) {
+                        set_msg("kmf_run_group: send/recv lists of ranks %d and %d disagree", src->rank, dst->rank);
+                        return KMF_EINVAL;
+                    }
+                    if (dst->recv_cnt[k])
+                        CK(cudaMemcpyPeer(dst->recvbuf.p + 4 * dst->recv_off[k], dst->device,
+                                          src->sendbuf.p + 4 * src->send_off[j], src->device,
+                                          sizeof(double) * 4 * dst->recv_cnt[k]));
+                }
+            for (kmf_ctx *c : byrank) {
+                CK(cudaSetDevice(c->device));
+                enqueue_unpack(c, c->s0);
+            }
+        }
+        // exact residue across ranks: integer limb sums
+        std::vector<unsigned long long> tot(kLimbs, 0ull), part(kLimbs);
+        if (int rc = sync_all()) return rc;
+        for (kmf_ctx *c : byrank) {
+            CK(cudaSetDevice(c->device));
+            CK(cudaMemcpy(part.data(), c->ctrl.p->limbs, sizeof(unsigned long long) * kLimbs, cudaMemcpyDeviceToHost));
+            for (int l = 0; l < kLimbs; l++) tot[l] += part[l];
+        }
+        for (kmf_ctx *c : byrank) {
+            CK(cudaSetDevice(c->device));
+            CK(cudaMemcpy(c->ctrl.p->limbs, tot.data(), sizeof(unsigned long long) * kLimbs, cudaMemcpyHostToDevice));
+            IterOut io{c->history.p, 1, n_iter, p->convergence_tol, 0};
+            k_close<<<1, kTB, 0, c->s0>>>(c->ctrl.p, (int)c->n_global, io);
+            CK(cudaGetLastError());
+        }
+        if (int rc = sync_all()) return rc;
+        // stop early on convergence or an error on any rank
+        int stop = 0;
+        for (kmf_ctx *c : byrank) {
+            unsigned long long st = 0;
+            CK(cudaMemcpy(&st, &c->ctrl.p->state, sizeof st, cudaMemcpyDeviceToHost));
+            if (st) stop = 1;
+        }
+        if (stop) break;
+    }
+    // outputs from rank 0 (all ranks agree on history and convergence);
+    // errors: the earliest failing rank
+    Ctrl fin;
+    int err_rank = -1, err_it = 1 << 30, err_stage = 99;
+    for (kmf_ctx *c : byrank) {
+        Ctrl f;
+        CK(cudaMemcpy(&f, c->ctrl.p, sizeof f, cudaMemcpyDeviceToHost));
+        if ((f.state & 3ull) == 1ull && (f.err_iter < err_it || (f.err_iter == err_it && f.err_stage < err_stage))) {
+            err_rank = c->rank;
+            err_it = f.err_iter;
+            err_stage = f.err_stage;
+        }
+        if (c->rank == 0) fin = f;
+    }
+    int completed = std::min(fin.iter - 1, n_iter);
+    if (history && completed > 0)
+        CK(cudaMemcpy(history, byrank[0]->history.p, sizeof(double) * completed, cudaMemcpyDeviceToHost));
+    if (iters_done) *iters_done = completed;
+    if (converged) *converged = (fin.state & 3ull) == 2ull;
+    if (err_rank >= 0) {
+        kmf_ctx *c = byrank[err_rank];
+        Ctrl f;
+        CK(cudaMemcpy(&f, c->ctrl.p, sizeof f, cudaMemcpyDeviceToHost));
+        int ctx = 0;
+        const int order[] = {KMF_CTX_FLUX_XP, KMF_CTX_WALL_TANGENT, KMF_CTX_WALL_NORMAL, KMF_CTX_OUTER_TANGENT,
+                             KMF_CTX_OUTER_NORMAL, KMF_CTX_C2P_DENSITY, KMF_CTX_C2P_PRESSURE};
+        for (int o : order)
+            if (f.ctx_mask & (1u << o)) {
+                ctx = o;
+                break;
+            }
+        record_error(c, KMF_EPOSITIVITY, f.err_iter, f.err_stage, ctx, err_rank, "positivity");
+        set_msg("positivity failure on rank %d", err_rank);
+        return KMF_EPOSITIVITY;
+    }
     return KMF_OK;
 }

@@ -72,6 +72,8 @@ __device__ __forceinline__ void raise_err(Ctrl *c, int stage, int slot, int ctx)
 // Geometry as seen by the point kernels.
 struct DG {
     int n, ld;
+    int n_act;   // points the flux / update launches cover (owned points under a partition)
+    int n_norm;  // residue normalisation (global point count under a partition)
     const double *__restrict__ x;
     const double *__restrict__ y;
     const unsigned char *__restrict__ flag;
@@ -292,7 +294,7 @@ __global__ void __launch_bounds__(kTB, MINB) k_flux(DG g, const double *__restri
 {
     if (c && should_skip(c, stage, kSlotFlux)) return;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= g.n) return;
+    if (i >= g.n_act) return;
     const int ld = g.ld;
     const bool interior = g.flag[i] == 0;
     // The owner's q, gradients and family weights are re-read from L1 per
@@ -425,7 +427,7 @@ __global__ void __launch_bounds__(kTB, MINB) k_flux2(DG g, const double *__restr
     const int lane = threadIdx.x & 31;
     const bool roleA = (lane & 1) == 0;  // A: neighbour end (x families); B: owner end (y families)
     const int i = blockIdx.x * (kTB / 2) + (threadIdx.x >> 1);
-    const bool valid = i < g.n;
+    const bool valid = i < g.n_act;
     const int ld = g.ld;
     const int ii = valid ? i : 0;
     const bool interior = valid && g.flag[ii] == 0;
@@ -737,6 +739,7 @@ struct IterOut {
     double *history;
     int hist_base, cap;
     double tol;
+    int close_in_kernel;  // 0 under a partition: limbs are all-reduced first, then k_close
 };
 
 // End of an outer iteration, run by one thread of the last stage-4 block:
@@ -777,7 +780,7 @@ __global__ void __launch_bounds__(kTB) k_update(DG g, double *__restrict__ Uo, d
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int ld = g.ld;
     double dr2 = 0.0;
-    if (!skip && i < g.n) {
+    if (!skip && i < g.n_act) {
         double uo[4], us[4], un[4];
         const double d = dt[i];
 #pragma unroll
@@ -814,6 +817,7 @@ __global__ void __launch_bounds__(kTB) k_update(DG g, double *__restrict__ Uo, d
         __syncthreads();
         for (int t = threadIdx.x; t < kLimbs; t += blockDim.x)
             if (sl[t]) atomicAdd(&c->limbs[t], sl[t]);
+        if (!io.close_in_kernel) return;  // partition: all-reduce, then k_close
         __threadfence();
         __syncthreads();
         if (threadIdx.x == 0) last = atomicAdd(&c->blocks_done, 1u) == gridDim.x - 1;
@@ -822,9 +826,44 @@ __global__ void __launch_bounds__(kTB) k_update(DG g, double *__restrict__ Uo, d
             __threadfence();
             for (int t = threadIdx.x; t < kLimbs; t += blockDim.x) sl[t] = atomicExch(&c->limbs[t], 0ull);
             __syncthreads();
-            if (threadIdx.x == 0) close_iteration(c, sl, g.n, io);
+            if (threadIdx.x == 0) close_iteration(c, sl, g.n_norm, io);
         }
     }
+}
+
+// Iteration close under a partition, after the limbs were summed across
+// ranks (ncclAllReduce or the group runner): one block.
+__global__ void k_close(Ctrl *c, int n_norm, IterOut io)
+{
+    __shared__ unsigned long long sl[kLimbs];
+    for (int t = threadIdx.x; t < kLimbs; t += blockDim.x) sl[t] = atomicExch(&c->limbs[t], 0ull);
+    __syncthreads();
+    if (threadIdx.x == 0) close_iteration(c, sl, n_norm, io);
+}
+
+// Halo exchange of q (multi-GPU): entry t moves component k of local slot
+// slot[t] to/from buf[base[t] + k * stride[t]] (per-peer component-major
+// blocks, one contiguous message per peer).
+__global__ void k_halo_pack(int total, const int *__restrict__ slot, const int *__restrict__ base,
+                            const int *__restrict__ stride, const double *__restrict__ q, int ld,
+                            double *__restrict__ buf)
+{
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= total) return;
+    const int s = slot[t], b = base[t], st = stride[t];
+#pragma unroll
+    for (int k = 0; k < 4; k++) buf[b + k * st] = q[k * ld + s];
+}
+
+__global__ void k_halo_unpack(int total, const int *__restrict__ slot, const int *__restrict__ base,
+                              const int *__restrict__ stride, const double *__restrict__ buf, double *__restrict__ q,
+                              int ld)
+{
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= total) return;
+    const int s = slot[t], b = base[t], st = stride[t];
+#pragma unroll
+    for (int k = 0; k < 4; k++) q[k * ld + s] = buf[b + k * st];
 }
 
 // 96-bit window of the normalised digit array starting at bit p

@@ -1,0 +1,151 @@
+"""Partitioned (multi-GPU) solve on top of the device contexts.
+
+Two drivers share the partition of `partition.py` and the device kernels:
+
+* `solve_group` -- one process, one context per rank (same GPU or several
+  GPUs), halo q moved by device / peer copies (`kmf_run_group`).  Used by the
+  multi-rank parity tests on a single B200 and as a one-process multi-GPU
+  mode.
+* `RankSolver` -- one process per GPU (torchrun), halo exchange and the
+  residue limb all-reduce over NCCL inside the iteration graph
+  (`kmf_nccl_init` + `kmf_run`).  torch.distributed only carries the NCCL
+  unique id and the final error / state gathers (plumbing).
+
+In both, every rank runs the single-GPU arithmetic on its owned points, so
+the residue history is bitwise identical to `solver.solve` for any rank
+count (tests/test_gpu_dist.py, tests/test_partition.py).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from ._device import DeviceConnectivity
+from .geometry import Connectivity
+from .partition import LocalPart, build_part, send_lists_for
+from .solver import SolverConfig, _params, initial_primitives
+from .state import PositivityError, Primitives
+
+
+def attach_partition(dev: DeviceConnectivity, part: LocalPart) -> None:
+    peers = sorted(set(part.send) | set(part.recv))
+    send_counts = np.array([part.send.get(p, np.empty(0)).size for p in peers], dtype=np.int64)
+    recv_counts = np.array([part.recv.get(p, np.empty(0)).size for p in peers], dtype=np.int64)
+    send = np.concatenate([part.send[p] for p in peers if p in part.send] or [np.empty(0, np.int64)]).astype(np.int64)
+    recv = np.concatenate([part.recv[p] for p in peers if p in part.recv] or [np.empty(0, np.int64)]).astype(np.int64)
+    pr = (C.c_int * max(len(peers), 1))(*peers)
+    keep = (send_counts, recv_counts, send, recv)
+    _lib.check(
+        _lib.lib().kmf_set_partition(dev.handle, part.n_owned, part.n_global, part.rank, part.nranks, len(peers), pr,
+                                     _lib.i64ptr(keep[0]), _lib.i64ptr(keep[2]), _lib.i64ptr(keep[1]),
+                                     _lib.i64ptr(keep[3])),
+        "kmf_set_partition",
+    )
+
+
+class RankPart:
+    """One rank's partition and its device context."""
+
+    def __init__(self, conn: Connectivity, rank: int, nranks: int, n_inner: int = 3, device: int | None = None,
+                 part: LocalPart | None = None):
+        depth = n_inner + 2
+        if part is None:
+            part = build_part(conn, rank, nranks, depth)
+            part.send = send_lists_for(conn, rank, nranks, depth)
+        self.part = part
+        self.dev = DeviceConnectivity(part.conn, device=device)
+        attach_partition(self.dev, part)
+
+    def set_state(self, prims_global: np.ndarray) -> None:
+        self.dev.set_state(np.ascontiguousarray(prims_global[:, self.part.global_ids]))
+
+    def owned_state(self):
+        prims, U = self.dev.get_state()
+        no = self.part.n_owned
+        return self.part.global_ids[:no], prims[:, :no], U[:, :no]
+
+
+def _raise_rank_error(rp: RankPart, params) -> None:
+    info = _lib.ErrorInfo()
+    _lib.lib().kmf_last_error(rp.dev.handle, C.byref(info))
+    try:
+        rp.dev.raise_positivity(info.context, info.stage, which=params.n_inner & 1, mode=params.mode,
+                                prefix=f"iteration {info.iteration}: ", gamma=params.gamma)
+    except PositivityError as exc:
+        idx = exc.indices
+        if idx is not None and info.context >= _lib.CTX_WALL_TANGENT:
+            idx = rp.part.global_ids[idx]  # point-level contexts: report global numbering
+        raise PositivityError(str(exc), indices=idx) from None
+
+
+def solve_group(config: SolverConfig, cloud, conn: Connectivity, nranks: int, initial_state: Primitives | None = None,
+                devices=None):
+    """Partitioned solve in one process; returns (history, prims (4,n), U (4,n))."""
+    prims0 = (initial_state.copy() if initial_state is not None else initial_primitives(config, cloud))
+    prims0.validate("initial state")
+    devices = devices or [_lib.device_index()] * nranks
+    ranks = [RankPart(conn, r, nranks, config.n_inner, devices[r]) for r in range(nranks)]
+    g = prims0.as_array()
+    for rp in ranks:
+        rp.set_state(g)
+    p = _params(config)
+    handles = (C.c_void_p * nranks)(*[rp.dev.handle.value for rp in ranks])
+    hist = np.zeros(config.n_outer)
+    done, conv = C.c_int(0), C.c_int(0)
+    rc = _lib.lib().kmf_run_group(handles, nranks, C.byref(p), config.n_outer, _lib.dptr(hist), C.byref(done),
+                                  C.byref(conv))
+    if rc == _lib.KMF_EPOSITIVITY:
+        for rp in ranks:
+            info = _lib.ErrorInfo()
+            _lib.lib().kmf_last_error(rp.dev.handle, C.byref(info))
+            if info.code == _lib.KMF_EPOSITIVITY:
+                _raise_rank_error(rp, p)
+    _lib.check(rc, "kmf_run_group")
+    n = cloud.n_points
+    prims, U = np.empty((4, n)), np.empty((4, n))
+    for rp in ranks:
+        gid, pr, u = rp.owned_state()
+        prims[:, gid] = pr
+        U[:, gid] = u
+    return hist[: done.value], prims, U, bool(conv.value)
+
+
+class RankSolver:
+    """This process's rank of an NCCL-partitioned solve (torchrun, one GPU
+    per process).  `dist` is an initialised torch.distributed module."""
+
+    def __init__(self, conn: Connectivity, dist, n_inner: int = 3, device: int | None = None):
+        self.rank, self.nranks = dist.get_rank(), dist.get_world_size()
+        self.dist = dist
+        self.rp = RankPart(conn, self.rank, self.nranks, n_inner, device)
+        uid = (C.c_char * 128)()
+        if self.rank == 0:
+            _lib.check(_lib.lib().kmf_nccl_get_unique_id(uid), "kmf_nccl_get_unique_id")
+        box = [bytes(uid)]
+        dist.broadcast_object_list(box, src=0)
+        uid = (C.c_char * 128).from_buffer_copy(box[0])
+        _lib.check(_lib.lib().kmf_nccl_init(self.rp.dev.handle, uid, self.rank, self.nranks), "kmf_nccl_init")
+
+    @property
+    def dev(self) -> DeviceConnectivity:
+        return self.rp.dev
+
+    def run(self, config: SolverConfig, prims_global: np.ndarray, n_iter: int):
+        """Set the state and run; history is identical on every rank."""
+        self.rp.set_state(prims_global)
+        p = _params(config)
+        hist = np.zeros(max(n_iter, 1))
+        done, conv = C.c_int(0), C.c_int(0)
+        rc = _lib.lib().kmf_run(self.rp.dev.handle, C.byref(p), n_iter, _lib.dptr(hist), C.byref(done),
+                                C.byref(conv))
+        flags = [None] * self.nranks
+        self.dist.all_gather_object(flags, rc)
+        if any(f == _lib.KMF_EPOSITIVITY for f in flags):
+            if rc == _lib.KMF_EPOSITIVITY:
+                _raise_rank_error(self.rp, p)
+            raise PositivityError("positivity failure on another rank")
+        _lib.check(rc, "kmf_run")
+        return hist[: done.value], bool(conv.value)

@@ -1,0 +1,187 @@
+"""Multi-GPU domain decomposition, checked on the CPU with the oracle.
+
+A partitioned solve -- every rank runs the single-GPU arithmetic on its
+owned points plus an (n_inner + 2)-layer halo, exchanging q for the halo
+once per RK stage and summing the residue exactly -- must reproduce the
+global solve bit for bit.  The exchange runs in-process and, for
+world_size 2, over torch.distributed gloo (the same protocol the NCCL
+transport implements on the GPUs).
+"""
+
+import math
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from conftest import fs_vec, perturbed_state
+from oracle import oracle as O
+from paper_2108_07031_b200.geometry import Connectivity, StencilSet, _select
+from paper_2108_07031_b200.partition import build_part, build_parts, halo_layers, owner_ranges, send_lists_for
+
+DEPTH = 5  # n_inner 3 + 2
+
+
+def flux_view(conn: Connectivity, n_owned: int) -> Connectivity:
+    """Same local connectivity with stencils only on owned rows (what the
+    device kernels restrict the flux / boundary / update launches to)."""
+    f = conn.full
+    keep = np.arange(f.n_owners) < n_owned
+    cnt = np.where(keep, np.diff(f.ptr), 0)
+    ptr = np.concatenate([[0], np.cumsum(cnt)])
+    e = np.arange(ptr[-1]) + np.repeat(f.ptr[:-1][keep] - ptr[:-1][keep], cnt[keep])
+    full = StencilSet(ptr=ptr, idx=f.idx[e], dx=f.dx[e], dy=f.dy[e])
+    split = {"x+": _select(full, full.dx <= 0.0), "x-": _select(full, full.dx >= 0.0),
+             "y+": _select(full, full.dy <= 0.0), "y-": _select(full, full.dy >= 0.0)}
+    det_safe = {k: np.where(conn.cloud.flag == 0, s.det, 1.0) for k, s in split.items()}
+    for k in det_safe:
+        det_safe[k][~keep] = 1.0
+    return Connectivity(cloud=conn.cloud, full=full, split=split, d_min=conn.d_min, d_mean=conn.d_mean,
+                        wall_frame=conn.wall_frame, outer_frame=conn.outer_frame, det_safe=det_safe)
+
+
+class RankState:
+    def __init__(self, part, init_global, fs):
+        self.p = part
+        self.pk = O.Packed(part.conn)
+        self.pkf = O.Packed(flux_view(part.conn, part.n_owned))
+        self.fs = fs
+        self.prims = init_global[:, part.global_ids].copy()
+        self.q = O.primitives_to_q(self.prims)
+        self.U = O.primitives_to_conserved(self.prims)
+
+    def owned(self, a):
+        return a[:, : self.p.n_owned]
+
+    def stage(self, stage, U_outer, dt):
+        qx, qy, _ = O.q_derivatives(self.pk, self.q, 3)
+        R = O.flux_residual(self.pkf, self.q, qx, qy)
+        R = O.apply_boundary(self.pkf, self.q, qx, qy, self.fs, R)
+        no = self.p.n_owned
+        Un = O.state_update_rk(U_outer[:, :no], self.U[:, :no], stage, dt[:no], R[:, :no])
+        self.U[:, :no] = Un
+        self.prims[:, :no] = O.conserved_to_primitives(Un)
+        self.q[:, :no] = O.primitives_to_q(self.prims[:, :no])
+
+
+def global_reference(conn, init, fs, iters):
+    hist, prims, U, _, _ = O.solve(O.Packed(conn), init, fs, iters)
+    return hist, prims
+
+
+def test_layers_cover_the_dependency_cone(small_naca_conn):
+    n = small_naca_conn.cloud.n_points
+    b = owner_ranges(n, 3)
+    layers = halo_layers(small_naca_conn.full, np.arange(b[1], b[2]), DEPTH)
+    allpts = np.concatenate(layers)
+    assert np.unique(allpts).size == allpts.size
+    # every neighbour of layers 0..DEPTH-1 is inside the local set
+    inside = np.zeros(n, dtype=bool)
+    inside[allpts] = True
+    f = small_naca_conn.full
+    for L in layers[:-1]:
+        for i in L[:: max(1, L.size // 50)]:
+            assert inside[f.neighbors(i)].all()
+
+
+def test_send_lists_match(small_naca_conn):
+    parts = build_parts(small_naca_conn, 3, DEPTH)
+    for p in parts:
+        assert send_lists_for(small_naca_conn, p.rank, 3, DEPTH).keys() == p.send.keys()
+        for peer, s in p.send.items():
+            assert np.array_equal(send_lists_for(small_naca_conn, p.rank, 3, DEPTH)[peer], s)
+            assert np.array_equal(p.global_ids[s], parts[peer].global_ids[parts[peer].recv[p.rank]])
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_partitioned_solve_is_bitwise_global(nranks, small_naca, small_naca_conn):
+    fs = fs_vec(0.63, 2.0)
+    init = perturbed_state(small_naca).as_array()
+    iters = 3
+    ref_hist, ref_prims = global_reference(small_naca_conn, init, fs, iters)
+    parts = build_parts(small_naca_conn, nranks, DEPTH)
+    ranks = [RankState(p, init, fs) for p in parts]
+    n = small_naca.n_points
+    hist = []
+    for it in range(iters):
+        dts = [O.local_timestep(r.pk, r.prims, 0.2) for r in ranks]
+        U_outer = [r.U.copy() for r in ranks]
+        for stage in (1, 2, 3, 4):
+            for r, dt, Uo in zip(ranks, dts, U_outer):
+                r.stage(stage, Uo, dt)
+            for r in ranks:  # halo exchange of q
+                for peer, slots in r.p.recv.items():
+                    r.q[:, slots] = ranks[peer].q[:, parts[peer].send[r.p.rank]]
+        drho2 = np.concatenate([(r.U[0, : r.p.n_owned] - Uo[0, : r.p.n_owned]) ** 2 for r, Uo in zip(ranks, U_outer)])
+        hist.append(math.sqrt(math.fsum(drho2.tolist()) / n))
+    assert np.array_equal(np.array(hist), ref_hist)
+    got = np.empty_like(ref_prims)
+    for r in ranks:
+        got[:, r.p.global_ids[: r.p.n_owned]] = r.owned(r.prims)
+    assert np.array_equal(got, ref_prims)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _gloo_worker(rank, world, port, out):
+    import torch
+    import torch.distributed as dist
+
+    from conftest import fs_vec as fsv, perturbed_state as ps
+    from paper_2108_07031_b200 import build_stencils, generate_naca_cloud
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cloud = generate_naca_cloud(80, 30, 1.15, 20.0)
+    conn = build_stencils(cloud)
+    part = build_part(conn, rank, world, DEPTH)
+    part.send = send_lists_for(conn, rank, world, DEPTH)
+    r = RankState(part, ps(cloud).as_array(), fsv(0.63, 2.0))
+    hist = []
+    for it in range(2):
+        dt = O.local_timestep(r.pk, r.prims, 0.2)
+        Uo = r.U.copy()
+        for stage in (1, 2, 3, 4):
+            r.stage(stage, Uo, dt)
+            reqs, bufs = [], {}
+            for peer, slots in part.send.items():
+                reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(r.q[:, slots])), peer))
+            for peer, slots in part.recv.items():
+                bufs[peer] = torch.empty((4, slots.size), dtype=torch.float64)
+                reqs.append(dist.irecv(bufs[peer], peer))
+            for q_ in reqs:
+                q_.wait()
+            for peer, slots in part.recv.items():
+                r.q[:, slots] = bufs[peer].numpy()
+        # exact residue: gather the owned drho^2 values (order-free fsum)
+        mine = torch.from_numpy((r.U[0, : part.n_owned] - Uo[0, : part.n_owned]) ** 2)
+        sizes = [None] * world
+        dist.all_gather_object(sizes, mine.numel())
+        chunks = [torch.empty(s, dtype=torch.float64) for s in sizes]
+        dist.all_gather(chunks, mine)
+        hist.append(math.sqrt(math.fsum(torch.cat(chunks).tolist()) / cloud.n_points))
+    out[rank] = (hist, r.owned(r.prims).copy(), part.global_ids[: part.n_owned].copy())
+    dist.destroy_process_group()
+
+
+def test_gloo_two_ranks_bitwise_global(small_naca, small_naca_conn):
+    import torch.multiprocessing as mp
+
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_gloo_worker, args=(2, port, out), nprocs=2, join=True)
+    fs = fs_vec(0.63, 2.0)
+    ref_hist, ref_prims = global_reference(small_naca_conn, perturbed_state(small_naca).as_array(), fs, 2)
+    for rank in (0, 1):
+        hist, prims, gid = out[rank]
+        assert np.array_equal(np.array(hist), ref_hist)
+        assert np.array_equal(prims, ref_prims[:, gid])

@@ -158,14 +158,21 @@ class DeviceConnectivity:
         if context in (_lib.CTX_WALL_TANGENT, _lib.CTX_WALL_NORMAL, _lib.CTX_OUTER_TANGENT, _lib.CTX_OUTER_NORMAL):
             self._raise_frame(which, prefix)
         if context in (_lib.CTX_C2P_DENSITY, _lib.CTX_C2P_PRESSURE):
-            U = np.empty((4, self.n))
-            _lib.check(L.kmf_diag_stage_state(self._h, stage, _lib.dptr(U)), "kmf_diag_stage_state")
-            fl = np.empty(self.n, dtype=np.uint8)
-            out = np.empty((4, self.n))
-            _lib.check(L.kmf_op_conserved_to_primitives(self.n, _lib.dptr(U), gamma, _lib.dptr(out), _lib.u8ptr(fl)),
-                       "conserved_to_primitives")
-            raise_decode_flags(fl, prefix)
+            raise_decode_flags(self.stage_decode_flags(stage, gamma), prefix)
         raise PositivityError(f"{prefix}positivity failure (context {context})")
+
+    def stage_decode_flags(self, stage: int, gamma: float, n_valid: int | None = None) -> np.ndarray:
+        """state.py:110-128 flags (bit0 rho, bit1 p) of the state the failing
+        update wrote, over the first ``n_valid`` slots (the owned points of a
+        partition: halo slots are not updated and carry stale values)."""
+        L = _lib.lib()
+        U = np.empty((4, self.n))
+        _lib.check(L.kmf_diag_stage_state(self._h, stage, _lib.dptr(U)), "kmf_diag_stage_state")
+        fl = np.empty(self.n, dtype=np.uint8)
+        out = np.empty((4, self.n))
+        _lib.check(L.kmf_op_conserved_to_primitives(self.n, _lib.dptr(U), gamma, _lib.dptr(out), _lib.u8ptr(fl)),
+                   "conserved_to_primitives")
+        return fl if n_valid is None else fl[:n_valid]
 
     def _raise_flux(self, flags: np.ndarray, mode: int, prefix: str):
         """Reproduce the reference raise order: fused walks 4096-point

@@ -27,7 +27,7 @@ from ._device import DeviceConnectivity
 from .geometry import Connectivity
 from .partition import LocalPart, build_part, send_lists_for
 from .solver import SolverConfig, _params, initial_primitives
-from .state import PositivityError, Primitives
+from .state import PositivityError, Primitives, raise_decode_flags
 
 
 def attach_partition(dev: DeviceConnectivity, part: LocalPart) -> None:
@@ -68,9 +68,36 @@ class RankPart:
         return self.part.global_ids[:no], prims[:, :no], U[:, :no]
 
 
-def _raise_rank_error(rp: RankPart, params) -> None:
+def _rank_error(rp: RankPart) -> _lib.ErrorInfo:
     info = _lib.ErrorInfo()
     _lib.lib().kmf_last_error(rp.dev.handle, C.byref(info))
+    return info
+
+
+def _decode_failures(rp: RankPart, info, params) -> tuple:
+    """(iteration, stage, global flags of this rank's owned points) of a
+    conserved_to_primitives failure, for the cross-rank merge."""
+    fl = rp.dev.stage_decode_flags(info.stage, params.gamma, rp.part.n_owned)
+    return info.iteration, info.stage, rp.part.global_ids[: rp.part.n_owned], fl
+
+
+def _raise_merged_decode(fails, n_global: int) -> None:
+    """state.py:110-128 raised over the WHOLE state: the reference checks
+    every point at once, so the failing (owned) points of all ranks that
+    failed at the earliest (iteration, stage) are merged in global order."""
+    first = min((it, st) for it, st, _, _ in fails)
+    fl = np.zeros(n_global, dtype=np.uint8)
+    for it, st, gid, f in fails:
+        if (it, st) == first:
+            fl[gid] |= f
+    raise_decode_flags(fl, f"iteration {first[0]}: ")
+
+
+_C2P = (_lib.CTX_C2P_DENSITY, _lib.CTX_C2P_PRESSURE)
+
+
+def _raise_rank_error(rp: RankPart, params) -> None:
+    info = _rank_error(rp)
     try:
         rp.dev.raise_positivity(info.context, info.stage, which=params.n_inner & 1, mode=params.mode,
                                 prefix=f"iteration {info.iteration}: ", gamma=params.gamma)
@@ -98,11 +125,12 @@ def solve_group(config: SolverConfig, cloud, conn: Connectivity, nranks: int, in
     rc = _lib.lib().kmf_run_group(handles, nranks, C.byref(p), config.n_outer, _lib.dptr(hist), C.byref(done),
                                   C.byref(conv))
     if rc == _lib.KMF_EPOSITIVITY:
-        for rp in ranks:
-            info = _lib.ErrorInfo()
-            _lib.lib().kmf_last_error(rp.dev.handle, C.byref(info))
-            if info.code == _lib.KMF_EPOSITIVITY:
-                _raise_rank_error(rp, p)
+        failed = [(rp, info) for rp in ranks for info in [_rank_error(rp)] if info.code == _lib.KMF_EPOSITIVITY]
+        dec = [_decode_failures(rp, info, p) for rp, info in failed if info.context in _C2P]
+        if dec and len(dec) == len(failed):
+            _raise_merged_decode(dec, cloud.n_points)
+        for rp, info in failed:
+            _raise_rank_error(rp, p)
     _lib.check(rc, "kmf_run_group")
     n = cloud.n_points
     prims, U = np.empty((4, n)), np.empty((4, n))
@@ -142,8 +170,15 @@ class RankSolver:
         rc = _lib.lib().kmf_run(self.rp.dev.handle, C.byref(p), n_iter, _lib.dptr(hist), C.byref(done),
                                 C.byref(conv))
         flags = [None] * self.nranks
-        self.dist.all_gather_object(flags, rc)
-        if any(f == _lib.KMF_EPOSITIVITY for f in flags):
+        mine = None
+        if rc == _lib.KMF_EPOSITIVITY:
+            info = _rank_error(self.rp)
+            mine = (int(info.context), _decode_failures(self.rp, info, p) if info.context in _C2P else None)
+        self.dist.all_gather_object(flags, (rc, mine))
+        if any(f[0] == _lib.KMF_EPOSITIVITY for f in flags):
+            fails = [f[1] for f in flags if f[0] == _lib.KMF_EPOSITIVITY]
+            if all(ctx in _C2P for ctx, _ in fails):
+                _raise_merged_decode([d for _, d in fails], self.rp.part.n_global)
             if rc == _lib.KMF_EPOSITIVITY:
                 _raise_rank_error(self.rp, p)
             raise PositivityError("positivity failure on another rank")

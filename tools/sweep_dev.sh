@@ -1,9 +1,7 @@
-# development sweep of launch shapes / orders (not part of the bench)
-run() { echo "== $*" >> gpurun_out/sweep5.log; env "$@" timeout 120 python tools/quick_perf.py 800 200 1.03 50 2>&1 | grep -E "instrument=False|stage" >> gpurun_out/sweep5.log; }
-run KMF_ORDER=natural
-run KMF_ORDER=ringtile2
-run KMF_ORDER=ringtile4
-run KMF_ORDER=ringtile8
-run KMF_ORDER=ringtile4 KMF_QG_NC=4
-run KMF_ORDER=ringtile8 KMF_QG_NC=4
-run KMF_ORDER=ringtile4 KMF_QG_NC=1
+# development sweep of kernel shapes (not part of the bench); output in gpurun_out/sweep.log
+OUT=gpurun_out/sweep.log
+run() { echo "== $*" >> $OUT; env "$@" timeout 180 python tools/quick_perf.py 800 200 1.03 50 2>&1 | grep -E "instrument=|stage" >> $OUT; }
+run KMF_FLUX_IMPL=1
+run KMF_FLUX_IMPL=3
+run KMF_FLUX_IMPL=3 KMF_FLUX_MINB=4
+for nc in 1 2 4; do for mb in 4 6 8; do run KMF_QG_IMPL=2 KMF_QG_NC=$nc KMF_QG_MINB=$mb; done; done

@@ -5,7 +5,6 @@
 #include "../../include/kmf_b200.h"
 #include "kmf_kernels.cuh"
 #include "kmf_flux3.cuh"
-#include "kmf_qgrad2.cuh"
 
 #include <cuda_runtime.h>
 #include <dlfcn.h>
@@ -88,8 +87,6 @@ struct kmf_ctx {
     bool xy = true;  // offsets recomputed from coordinates
     int qg_nc = 2;   // q-gradient components per thread (KMF_QG_NC)
     int qg_unroll = 1;  // q-gradient edge unroll (KMF_QG_UNROLL)
-    int qg_impl = 1;    // q-gradient kernel shape (KMF_QG_IMPL): 1 slot loop, 2 straight-line slots
-    int qg_minb = 4;    // resident blocks/SM bound of the straight-line kernels (KMF_QG_MINB)
     int flux_impl = 3;  // interior flux kernel shape (KMF_FLUX_IMPL): 1 per-flux, 2 pair, 3 lock-step
     int flux_minb = 3;  // interior flux blocks per SM (KMF_FLUX_MINB)
     bool has_perm = false;
@@ -524,44 +521,14 @@ void launch_sw_t(kmf_ctx *c, cudaStream_t s, const double *Gin, double *Gout, Ct
         }                                                                   \
     } while (0)
 
-template <bool SWEEP, int NC, int MINB>
-void launch_qg2_t(kmf_ctx *c, cudaStream_t s, const double *Gin, double *Gout, Ctrl *ctl, int stage, int slot,
-                  int want_res)
-{
-    const int nb = nblk(c->n, qg_points_per_block<NC>());
-    k_qgrad2<true, SWEEP, NC, 15, MINB><<<nb, kTB, 0, s>>>(c->dg(), c->q.p, Gin, Gout, ctl, stage, slot, want_res);
-}
-
-template <bool SWEEP, int NC>
-void launch_qg2_nc(kmf_ctx *c, cudaStream_t s, const double *Gin, double *Gout, Ctrl *ctl, int stage, int slot,
-                   int want_res)
-{
-    if (c->qg_minb >= 8) launch_qg2_t<SWEEP, NC, 8>(c, s, Gin, Gout, ctl, stage, slot, want_res);
-    else if (c->qg_minb >= 6) launch_qg2_t<SWEEP, NC, 6>(c, s, Gin, Gout, ctl, stage, slot, want_res);
-    else launch_qg2_t<SWEEP, NC, 4>(c, s, Gin, Gout, ctl, stage, slot, want_res);
-}
-
-template <bool SWEEP>
-bool launch_qg2(kmf_ctx *c, cudaStream_t s, const double *Gin, double *Gout, Ctrl *ctl, int stage, int slot,
-                int want_res)
-{
-    if (c->qg_impl != 2 || !c->xy) return false;
-    if (c->qg_nc == 1) launch_qg2_nc<SWEEP, 1>(c, s, Gin, Gout, ctl, stage, slot, want_res);
-    else if (c->qg_nc == 4) launch_qg2_nc<SWEEP, 4>(c, s, Gin, Gout, ctl, stage, slot, want_res);
-    else launch_qg2_nc<SWEEP, 2>(c, s, Gin, Gout, ctl, stage, slot, want_res);
-    return true;
-}
-
 void launch_first_order(kmf_ctx *c, cudaStream_t s, double *G, Ctrl *ctl, int stage)
 {
-    if (launch_qg2<false>(c, s, nullptr, G, ctl, stage, 0, 0)) return;
     KMF_QG_DISPATCH(launch_fo_t, c, s, G, ctl, stage);
 }
 
 void launch_sweep(kmf_ctx *c, cudaStream_t s, const double *Gin, double *Gout, Ctrl *ctl, int stage, int slot,
                   int want_res)
 {
-    if (launch_qg2<true>(c, s, Gin, Gout, ctl, stage, slot, want_res)) return;
     KMF_QG_DISPATCH(launch_sw_t, c, s, Gin, Gout, ctl, stage, slot, want_res);
 }
 
@@ -919,11 +886,6 @@ int kmf_create(kmf_ctx **out, const kmf_geometry *g, int device)
         int v = std::atoi(e);
         if (v == 1 || v == 2 || v == 4) c->qg_unroll = v;
     }
-    if (const char *e = std::getenv("KMF_QG_IMPL")) {
-        int v = std::atoi(e);
-        if (v == 1 || v == 2) c->qg_impl = v;
-    }
-    if (const char *e = std::getenv("KMF_QG_MINB")) c->qg_minb = std::atoi(e);
     if (const char *e = std::getenv("KMF_FLUX_MINB")) {
         int v = std::atoi(e);
         if (v == 3 || v == 4) c->flux_minb = v;

@@ -502,12 +502,21 @@ def _assemble(cloud: PointCloud, lists) -> _Parts:
     return _Parts(full, split, d_min, d_mean, wall_frame, outer_frame, failures)
 
 
-def build_stencils(cloud: PointCloud, epsilon: float | None = None, k: int | None = None) -> Connectivity:
+def build_stencils(cloud: PointCloud, epsilon: float | None = None, k: int | None = None,
+                   native: bool | None = None) -> Connectivity:
     """Full, split and boundary-frame stencils with cached sums (geometry.py:453-518).
 
     Raises StencilDeficiencyError (after widening failing points to k=25)
-    exactly where the reference does.
+    exactly where the reference does.  In k-nearest mode the heavy loops run
+    in the native builder (builder.py, libkmf_build.so) unless native=False;
+    native=None uses it when the library is built.  Both paths give
+    bit-identical connectivities (tests/test_builder.py).
     """
+    if epsilon is None and native is not False:
+        from . import builder
+
+        if native or builder.available():
+            return builder.build_stencils_native(cloud, k)
     cloud.validate()
     if epsilon is not None and k is not None:
         raise ValueError("give either epsilon or k, not both")

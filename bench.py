@@ -47,6 +47,8 @@ CONFIGS = {
     "c1": (400, 100, 1.06, 0.63, 2.0, "NACA0012 40K (400x100, g=1.06) M0.63 AoA2 second order"),
     "c2": (800, 200, 1.03, 0.63, 2.0, "NACA0012 160K (800x200, g=1.03) M0.63 AoA2 second order n_inner=3"),
     "c3": (3160, 790, 1.00734, 0.85, 1.0, "NACA0012 2.5M (3160x790, g=1.00734) M0.85 AoA1 second order"),
+    "c4": (6324, 1581, 1.003647, 0.63, 2.0, "NACA0012 10M (6324x1581, g=1.003647) M0.63 AoA2 second order"),
+    "c5": (12648, 3162, 1.001821, 0.63, 2.0, "NACA0012 40M (12648x3162, g=1.001821) M0.63 AoA2 second order"),
 }
 METRIC = "point-iterations/sec (RDP = 1/value s/point/iter), NACA0012 q-LSKUM"
 UNIT = "point-iterations/s"
@@ -92,10 +94,15 @@ def setup(name):
     from paper_2108_07031_b200 import SolverConfig, build_stencils, generate_naca_cloud, initial_primitives
 
     m, L, g, mach, aoa, _ = CONFIGS[name]
+    t = time.perf_counter()
     cloud = generate_naca_cloud(m, L, g, 20.0)
-    conn = build_stencils(cloud)
+    conn = build_stencils(cloud)  # native builder (libkmf_build.so), bit-exact with the reference's
+    t1 = time.perf_counter()
     cfg = SolverConfig(mach=mach, aoa_deg=aoa, cfl=0.2, n_inner=3, mode="fused")
-    return cloud, conn, cfg, initial_primitives(cfg, cloud)
+    init = initial_primitives(cfg, cloud)
+    print(f"[bench] setup {name}: {cloud.n_points} points, {conn.full.idx.size} edges; generator+builder "
+          f"{t1 - t:.1f} s, initial state {time.perf_counter() - t1:.1f} s", file=sys.stderr, flush=True)
+    return cloud, conn, cfg, init
 
 
 class Clocks:
@@ -167,10 +174,13 @@ def cpu_baseline(conn, cfg, init, target_s=12.0):
     t = time.perf_counter()
     O.solve(pk, init.as_array(), fsv, 1, gamma=cfg.gamma, cfl=cfg.cfl, n_inner=cfg.n_inner)
     one = time.perf_counter() - t
-    iters = int(min(200, max(2, target_s / max(one, 1e-3))))
-    t = time.perf_counter()
-    O.solve(pk, init.as_array(), fsv, iters, gamma=cfg.gamma, cfl=cfg.cfl, n_inner=cfg.n_inner)
-    sec = time.perf_counter() - t
+    if one > 0.5 * target_s:  # large clouds: the first whole iteration is the sample
+        iters, sec = 1, one
+    else:
+        iters = int(min(200, max(2, target_s / max(one, 1e-3))))
+        t = time.perf_counter()
+        O.solve(pk, init.as_array(), fsv, iters, gamma=cfg.gamma, cfl=cfg.cfl, n_inner=cfg.n_inner)
+        sec = time.perf_counter() - t
     n = conn.cloud.n_points
     return {"value": n * iters / sec, "unit": UNIT, "cores": threads, "kind": "port",
             "sample": f"{iters} full outer iterations of the same {n}-point workload ({sec:.1f} s), "
@@ -303,8 +313,10 @@ def run_ours(args):
                           "peak_source": f"DFMA probe in this run: {peak_fp64.value:.2f} TFLOP/s"},
         "clocks": clk.summary(),
     }
-    if not args.no_cpu_baseline and ws == 1:
+    if not args.no_cpu_baseline and ws == 1 and args.config in ("c1", "c2", "c3"):
         line["cpu_baseline"] = cpu_baseline(conn, cfg, init)
+    elif ws == 1:
+        line["cpu_baseline"] = None  # 10M/40M: the oracle's host copy of the split stencils does not fit a bounded run
     print(json.dumps(line), flush=True)
 
 

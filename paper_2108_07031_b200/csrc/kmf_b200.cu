@@ -87,6 +87,8 @@ struct kmf_ctx {
     bool xy = true;  // offsets recomputed from coordinates
     int qg_nc = 2;   // q-gradient components per thread (KMF_QG_NC)
     int qg_unroll = 1;  // q-gradient edge unroll (KMF_QG_UNROLL)
+    int qg_tb = 128;    // q-gradient block size (KMF_QG_TB)
+    int qg_stage = 0;   // stage ELL index slices in shared memory (KMF_QG_STAGE)
     int flux_impl = 3;  // interior flux kernel shape (KMF_FLUX_IMPL): 1 per-flux, 2 pair, 3 lock-step
     int flux_minb = 3;  // interior flux blocks per SM (KMF_FLUX_MINB)
     bool has_perm = false;
@@ -484,19 +486,34 @@ int build_context(kmf_ctx *c, const kmf_geometry *g)
 
 // ------------------------------------------------------------ stage launch
 
+// block size variants (KMF_QG_TB = 128, 256, 512)
+#define KMF_TB_SWITCH(KCALL)                            \
+    switch (c->qg_tb + c->qg_stage) {                   \
+    case 256: KCALL(256, 0); break;                     \
+    case 512: KCALL(512, 0); break;                     \
+    case 129: KCALL(128, 1); break;                     \
+    case 257: KCALL(256, 1); break;                     \
+    default: KCALL(128, 0); break;                      \
+    }
+
 template <bool XY, int NC, int U>
 void launch_fo_t(kmf_ctx *c, cudaStream_t s, double *G, Ctrl *ctl, int stage)
 {
-    const int nb = nblk(c->n, qg_points_per_block<NC>());
-    k_first_order<XY, NC, U><<<nb, kTB, 0, s>>>(c->dg(), c->q.p, G, ctl, stage);
+#define KMF_FO(TB, ST) \
+    k_first_order<XY, NC, U, TB, ST><<<nblk(c->n, qg_points_per_block<NC, TB>()), TB, 0, s>>>(c->dg(), c->q.p, G, ctl, stage)
+    KMF_TB_SWITCH(KMF_FO)
+#undef KMF_FO
 }
 
 template <bool XY, int NC, int U>
 void launch_sw_t(kmf_ctx *c, cudaStream_t s, const double *Gin, double *Gout, Ctrl *ctl, int stage, int slot,
                  int want_res)
 {
-    const int nb = nblk(c->n, qg_points_per_block<NC>());
-    k_sweep<XY, NC, U><<<nb, kTB, 0, s>>>(c->dg(), c->q.p, Gin, Gout, ctl, stage, slot, want_res);
+#define KMF_SW(TB, ST)                                                                              \
+    k_sweep<XY, NC, U, TB, ST><<<nblk(c->n, qg_points_per_block<NC, TB>()), TB, 0, s>>>(c->dg(), c->q.p, Gin, Gout, \
+                                                                                  ctl, stage, slot, want_res)
+    KMF_TB_SWITCH(KMF_SW)
+#undef KMF_SW
 }
 
 // q-gradient launch shape: KMF_QG_NC components per thread (1, 2, 4) and
@@ -886,6 +903,7 @@ int kmf_create(kmf_ctx **out, const kmf_geometry *g, int device)
         int v = std::atoi(e);
         if (v == 1 || v == 2 || v == 4) c->qg_unroll = v;
     }
+    if (const char *e = std::getenv("KMF_QG_TB")) c->qg_tb = std::atoi(e);
     if (const char *e = std::getenv("KMF_FLUX_MINB")) {
         int v = std::atoi(e);
         if (v == 3 || v == 4) c->flux_minb = v;
@@ -899,6 +917,11 @@ int kmf_create(kmf_ctx **out, const kmf_geometry *g, int device)
         delete c;
         return rc;
     }
+    // index staging pays once the stencil streams from HBM (measured: -6.5 %
+    // q-gradient time at 2.5M / 10M points) and costs L1 capacity when the
+    // working set is L2-resident (+7 % at 160K); KMF_QG_STAGE overrides
+    c->qg_stage = c->n > 1000000 ? 1 : 0;
+    if (const char *e = std::getenv("KMF_QG_STAGE")) c->qg_stage = std::atoi(e) ? 1 : 0;
     *out = c;
     return KMF_OK;
 }

@@ -122,18 +122,35 @@ KMF_HD int ell_base(const DG &g, int i) { return g.eoff[i >> 5] + (i & 31); }
 // while multiplying the threads in flight.  A 128-thread block covers
 // 128*NC/4 points; warp w handles component group w % (4/NC) of the
 // 32-point SELL slice w / (4/NC), so slice-local ELL offsets stay coalesced.
-template <int NC>
+template <int NC, int TB = kTB>
 KMF_HD void qg_thread(int &i, int &k0)
 {
     constexpr int CG = 4 / NC;            // component groups per point
-    constexpr int P = kTB / CG;           // points per block
+    constexpr int P = TB / CG;            // points per block
     const int w = threadIdx.x >> 5;
     i = blockIdx.x * P + (w / CG) * 32 + (threadIdx.x & 31);
     k0 = (w % CG) * NC;
 }
 
-template <int NC>
-constexpr int qg_points_per_block() { return kTB * NC / 4; }
+template <int NC, int TB = kTB>
+constexpr int qg_points_per_block() { return TB * NC / 4; }
+
+// Shared-memory staging of a q-gradient block's ELL index slices (ST = 1):
+// one cooperative coalesced pass at block start instead of one dependent
+// index round trip per slot.  SPB = slices per block.
+template <int SPB>
+KMF_HD bool qg_stage_indices(const DG &g, int *sidx, int cap, int &e0)
+{
+    const int ns = (g.n + 31) >> 5;
+    const int s0 = blockIdx.x * SPB;
+    e0 = g.eoff[s0];
+    const int esz = g.eoff[min(s0 + SPB, ns)] - e0;
+    const bool staged = esz <= cap;
+    if (staged)
+        for (int e = threadIdx.x; e < esz; e += blockDim.x) sidx[e] = g.eidx[e0 + e];
+    __syncthreads();
+    return staged;
+}
 
 // The edge loop is unrolled by U: the U neighbour indices, then all their
 // gathers, are issued before any arithmetic (U-fold memory-level
@@ -141,13 +158,20 @@ constexpr int qg_points_per_block() { return kTB * NC / 4; }
 // tail slots are predicated off, so the result is unchanged bit for bit.
 
 // lsq.py:164-175 first_order_q_gradients -- bitwise (CSR-order sums, no FMA)
-template <bool XY, int NC, int U>
-__global__ void __launch_bounds__(kTB) k_first_order(DG g, const double *__restrict__ q,
+// TB: block size.  Larger blocks with a ring-tiled point order
+// (reorder.ring_tiles) put several radially stacked slices on one SM, so
+// the neighbour rings they share are fetched into L1 once.
+template <bool XY, int NC, int U, int TB = kTB, int ST = 0>
+__global__ void __launch_bounds__(TB) k_first_order(DG g, const double *__restrict__ q,
                                                      double *__restrict__ G, Ctrl *c, int stage)
 {
     if (c && should_skip(c, stage, 0)) return;
+    constexpr int SPB = TB * NC / 4 / 32, CAP = ST ? SPB * 32 * 24 : 1;
+    __shared__ int sidx[CAP];
+    int e0 = 0;
+    const bool staged = ST ? qg_stage_indices<SPB>(g, sidx, CAP, e0) : false;
     int i, k0;
-    qg_thread<NC>(i, k0);
+    qg_thread<NC, TB>(i, k0);
     if (i >= g.n) return;
     const int ld = g.ld;
     double qi[NC], sx[NC], sy[NC];
@@ -164,7 +188,7 @@ __global__ void __launch_bounds__(kTB) k_first_order(DG g, const double *__restr
 #pragma unroll
         for (int u = 0; u < U; u++) {
             ent[u] = base + min(s0 + u, d - 1) * 32;
-            jj[u] = g.eidx[ent[u]];
+            jj[u] = (ST && staged) ? sidx[ent[u] - e0] : g.eidx[ent[u]];
         }
         double dx[U], dy[U], qj[U][NC];
 #pragma unroll
@@ -195,14 +219,18 @@ __global__ void __launch_bounds__(kTB) k_first_order(DG g, const double *__restr
 
 // lsq.py:214-227 one Jacobi sweep of the defect-corrected gradients --
 // bitwise.  With want_res the max |new - old| (lsq.py:238-243) is reduced.
-template <bool XY, int NC, int U>
-__global__ void __launch_bounds__(kTB) k_sweep(DG g, const double *__restrict__ q,
+template <bool XY, int NC, int U, int TB = kTB, int ST = 0>
+__global__ void __launch_bounds__(TB) k_sweep(DG g, const double *__restrict__ q,
                                                const double *__restrict__ Gin, double *__restrict__ Gout,
                                                Ctrl *c, int stage, int slot, int want_res)
 {
     if (c && should_skip(c, stage, slot)) return;
+    constexpr int SPB = TB * NC / 4 / 32, CAP = ST ? SPB * 32 * 24 : 1;
+    __shared__ int sidx[CAP];
+    int e0 = 0;
+    const bool staged = ST ? qg_stage_indices<SPB>(g, sidx, CAP, e0) : false;
     int i, k0;
-    qg_thread<NC>(i, k0);
+    qg_thread<NC, TB>(i, k0);
     double rmax = 0.0;
     if (i < g.n) {
         const int ld = g.ld;
@@ -222,7 +250,7 @@ __global__ void __launch_bounds__(kTB) k_sweep(DG g, const double *__restrict__ 
 #pragma unroll
             for (int u = 0; u < U; u++) {
                 ent[u] = base + min(s0 + u, d - 1) * 32;
-                jj[u] = g.eidx[ent[u]];
+                jj[u] = (ST && staged) ? sidx[ent[u] - e0] : g.eidx[ent[u]];
             }
             double dx[U], dy[U], qj[U][NC], gxj[U][NC], gyj[U][NC];
 #pragma unroll

@@ -212,7 +212,7 @@ def initial_primitives(config: SolverConfig, cloud: PointCloud) -> Primitives:
         return prims
     wall_pts = np.column_stack([cloud.x[w], cloud.y[w]])
     tree = cKDTree(wall_pts)
-    dist, near = tree.query(np.column_stack([cloud.x, cloud.y]))
+    dist, near = tree.query(np.column_stack([cloud.x, cloud.y]), workers=-1)  # workers: same result, parallel
     if w.size > 1:
         sigma = 8.0 * float(np.mean(tree.query(wall_pts, k=2)[0][:, 1]))
     else:

@@ -12,7 +12,10 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import numpy as np  # noqa: E402
 
 from paper_2108_07031_b200 import SolverConfig, build_stencils, generate_naca_cloud, initial_primitives  # noqa: E402
-from paper_2108_07031_b200._device import device_for  # noqa: E402
+import os  # noqa: E402
+
+from paper_2108_07031_b200 import reorder  # noqa: E402
+from paper_2108_07031_b200._device import DeviceConnectivity  # noqa: E402
 from paper_2108_07031_b200.solver import _params  # noqa: E402
 
 
@@ -27,7 +30,7 @@ def main():
     cfg = SolverConfig(mach=0.63, aoa_deg=2.0, n_outer=iters)
     init = initial_primitives(cfg, cloud)
     t = time.perf_counter()
-    dev = device_for(conn)
+    dev = DeviceConnectivity(conn, perm=reorder.permutation(cloud, os.environ.get("KMF_ORDER", "natural")))
     print(f"context {time.perf_counter() - t:.2f}s", flush=True)
     for instrument in (False, True):
         dev.set_state(init.as_array())

@@ -1,6 +1,9 @@
 # development sweep of kernel shapes (not part of the bench); output in gpurun_out/sweep.log
 OUT=gpurun_out/sweep.log
-run() { echo "== $*" >> $OUT; env "$@" timeout 180 python tools/quick_perf.py 800 200 1.03 50 2>&1 | grep -E "instrument=True|stage" >> $OUT; }
+run() { echo "== $SZ $*" >> $OUT; env "$@" timeout 300 python tools/quick_perf.py $SZ 2>&1 | grep -E "instrument=True|stage" >> $OUT; }
+for SZ in "3160 790 1.00734 10" "6324 1581 1.003647 5"; do
 run KMF_QG_STAGE=0
-for nc in 1 2 4; do run KMF_QG_STAGE=2 KMF_QG_NC=$nc; done
-run KMF_QG_STAGE=2 KMF_QG_NC=2 KMF_QG_UNROLL=2
+run KMF_QG_STAGE=1
+run KMF_QG_STAGE=1 KMF_QG_TB=256
+run KMF_QG_STAGE=1 KMF_QG_NC=4
+done

@@ -594,7 +594,13 @@ void launch_flux_t(kmf_ctx *c, cudaStream_t s, const double *G, int mode, double
         return;
     }
     const int nb = nblk(c->n);
-    if (c->flux_impl == 3) {
+    if (c->flux_impl == 4) {  // lock-step body + next-edge L1 prefetch (fused only)
+        if (mode == 0) {
+            k_flux3<XY, -1, MINB, GK, 1><<<nb, kTB, 0, s>>>(g, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage);
+            return;
+        }
+    }
+    if (c->flux_impl >= 3) {
         if (mode == 0) {
             k_flux3<XY, -1, MINB, GK><<<nb, kTB, 0, s>>>(g, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage);
         } else {
@@ -904,14 +910,6 @@ int kmf_create(kmf_ctx **out, const kmf_geometry *g, int device)
         if (v == 1 || v == 2 || v == 4) c->qg_unroll = v;
     }
     if (const char *e = std::getenv("KMF_QG_TB")) c->qg_tb = std::atoi(e);
-    if (const char *e = std::getenv("KMF_FLUX_MINB")) {
-        int v = std::atoi(e);
-        if (v == 3 || v == 4) c->flux_minb = v;
-    }
-    if (const char *e = std::getenv("KMF_FLUX_IMPL")) {
-        int v = std::atoi(e);
-        if (v >= 1 && v <= 3) c->flux_impl = v;
-    }
     int rc = build_context(c, g);
     if (rc != KMF_OK) {
         delete c;
@@ -922,6 +920,19 @@ int kmf_create(kmf_ctx **out, const kmf_geometry *g, int device)
     // working set is L2-resident (+7 % at 160K); KMF_QG_STAGE overrides
     c->qg_stage = c->n > 1000000 ? 1 : 0;
     if (const char *e = std::getenv("KMF_QG_STAGE")) c->qg_stage = std::atoi(e) ? 1 : 0;
+    // likewise the flux kernel's next-edge L1 prefetch and 4 blocks/SM
+    // (-5.9 % flux time at 2.5M, +4 % at 160K)
+    const bool big = c->n > 1000000;
+    c->flux_impl = big ? 4 : 3;
+    c->flux_minb = big ? 4 : 3;
+    if (const char *e = std::getenv("KMF_FLUX_MINB")) {
+        int v = std::atoi(e);
+        if (v == 3 || v == 4) c->flux_minb = v;
+    }
+    if (const char *e = std::getenv("KMF_FLUX_IMPL")) {
+        int v = std::atoi(e);
+        if (v >= 1 && v <= 4) c->flux_impl = v;
+    }
     *out = c;
     return KMF_OK;
 }

@@ -342,17 +342,19 @@ static inline double qtilde(const double *q, const double *qx, const double *qy,
 
 /* positivity pre-scan reproducing the reference's raise order
  * (solver.py:164-170 via _interior_kind_term over _Blocks, :218-229) */
+static int64_t n_active(const orc_conn *c) { return c->n_act > 0 && c->n_act < c->n ? c->n_act : c->n; }
+
 static int flux_scan(const orc_conn *c, const double *q, const double *qx, const double *qy, int mode,
                      orc_error *err)
 {
-    int64_t n = c->n;
-    int64_t nb = (n + BLOCK - 1) / BLOCK;
+    int64_t n = c->n, na = n_active(c);
+    int64_t nb = (na + BLOCK - 1) / BLOCK;
     for (int outer = 0; outer < (mode == 0 ? nb : 4); outer++) {
         for (int inner = 0; inner < (mode == 0 ? 4 : nb); inner++) {
             int kind = mode == 0 ? inner : outer;
             int64_t blk = mode == 0 ? outer : inner;
             const orc_stencil *s = &c->split[kind];
-            int64_t lo = blk * BLOCK, hi = lo + BLOCK < n ? lo + BLOCK : n;
+            int64_t lo = blk * BLOCK, hi = lo + BLOCK < na ? lo + BLOCK : na;
             int64_t e0 = s->ptr[lo], e1 = s->ptr[hi];
             int64_t bad = 0, first = -1, nan_i = -1, nan_0 = -1, cnt_i = 0, cnt_0 = 0;
             for (int64_t i = lo; i < hi; i++)
@@ -396,12 +398,12 @@ static int flux_scan(const orc_conn *c, const double *q, const double *qx, const
 int orc_flux_residual(const orc_conn *c, const double *q, const double *qx, const double *qy,
                       int mode, double gamma, double *R, orc_error *err)
 {
-    int64_t n = c->n;
+    int64_t n = c->n, na = n_active(c);
     if (flux_scan(c, q, qx, qy, mode, err)) return 1;
 #pragma omp parallel for schedule(dynamic, 256)
     for (int64_t i = 0; i < n; i++) {
         double acc[4] = {0, 0, 0, 0};
-        if (c->flag[i] != 0) { /* rows zeroed anyway (solver.py:233-234) */
+        if (c->flag[i] != 0 || i >= na) { /* rows zeroed anyway (solver.py:233-234) */
             for (int k = 0; k < 4; k++) R[k * n + i] = 0.0;
             continue;
         }
@@ -705,7 +707,7 @@ int orc_solve(const orc_conn *c, const orc_params *p, double *prims, double *U, 
             if ((rc = orc_conserved_to_primitives(n, U, gamma, prims, err))) goto done;
         }
         err->stage = 0;
-        double res = orc_residue_norm(n, U, Uo);
+        double res = orc_residue_norm(n_active(c), U, Uo);
         history[it - 1] = res;
         *iterations = it;
         if (p->convergence_tol > 0.0 && res <= p->convergence_tol) {

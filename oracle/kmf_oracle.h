@@ -55,6 +55,10 @@ typedef struct {
     const double *det_safe[4];
     int has_wall, has_outer;
     orc_frame wall, outer;
+    /* rows whose flux residual (and residue) are computed: a partition's
+     * owned points (0 = all n).  Test/bench infrastructure for partitioned
+     * checks and bounded CPU samples; the reference has no such field. */
+    int64_t n_act;
 } orc_conn;
 
 /* error contexts (which reference raise site fired) */

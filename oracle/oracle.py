@@ -36,7 +36,7 @@ class OFrame(C.Structure):
 class OConn(C.Structure):
     _fields_ = [("n", C.c_int64), ("flag", _i64p), ("d_min", _dp), ("full", OStencil), ("split", OStencil * 4),
                 ("det_safe", _dp * 4), ("has_wall", C.c_int), ("has_outer", C.c_int),
-                ("wall", OFrame), ("outer", OFrame)]
+                ("wall", OFrame), ("outer", OFrame), ("n_act", C.c_int64)]
 
 
 class OError(C.Structure):

@@ -25,7 +25,7 @@ import numpy as np
 from . import _lib
 from ._device import DeviceConnectivity
 from .geometry import Connectivity
-from .partition import LocalPart, build_part, send_lists_for
+from .partition import LocalPart, build_part, owner_ranges, send_lists_for
 from .solver import SolverConfig, _params, initial_primitives
 from .state import PositivityError, Primitives, raise_decode_flags
 
@@ -141,6 +141,20 @@ def solve_group(config: SolverConfig, cloud, conn: Connectivity, nranks: int, in
     return hist[: done.value], prims, U, bool(conv.value)
 
 
+def exchange_send_lists(part: LocalPart, dist) -> None:
+    """Fill part.send from the peers' receive lists: one object all-gather
+    of halo global ids, instead of every rank recomputing every peer's halo
+    (partition.send_lists_for, O(nranks) halo searches over the global
+    stencil).  send[peer] lists this rank's local (owned) slots in the
+    peer's receive order."""
+    mine = {peer: part.global_ids[slots] for peer, slots in part.recv.items()}
+    allrecv = [None] * part.nranks
+    dist.all_gather_object(allrecv, mine)
+    b = owner_ranges(part.n_global, part.nranks)
+    part.send = {peer: np.asarray(r[part.rank]) - b[part.rank] for peer, r in enumerate(allrecv)
+                 if peer != part.rank and part.rank in r}
+
+
 class RankSolver:
     """This process's rank of an NCCL-partitioned solve (torchrun, one GPU
     per process).  `dist` is an initialised torch.distributed module."""
@@ -148,7 +162,9 @@ class RankSolver:
     def __init__(self, conn: Connectivity, dist, n_inner: int = 3, device: int | None = None):
         self.rank, self.nranks = dist.get_rank(), dist.get_world_size()
         self.dist = dist
-        self.rp = RankPart(conn, self.rank, self.nranks, n_inner, device)
+        part = build_part(conn, self.rank, self.nranks, n_inner + 2)
+        exchange_send_lists(part, dist)
+        self.rp = RankPart(conn, self.rank, self.nranks, n_inner, device, part=part)
         uid = (C.c_char * 128)()
         if self.rank == 0:
             _lib.check(_lib.lib().kmf_nccl_get_unique_id(uid), "kmf_nccl_get_unique_id")

@@ -109,3 +109,17 @@ def test_split_view_materialises_the_sign_subsets():
         assert s.ptr[-1] == m.sum()
         i = 100
         assert np.array_equal(s.neighbors(i), s.idx[s.ptr[i]:s.ptr[i + 1]])
+
+
+def test_store_round_trip_memory_mapped(tmp_path):
+    from paper_2108_07031_b200 import store
+
+    cloud = generate_naca_cloud(80, 30, 1.15, 20.0)
+    conn = build_stencils(cloud, native=True)
+    store.save(conn, tmp_path / "c", extra={"init": np.arange(6.0)})
+    back, extra = store.load(tmp_path / "c")
+    assert isinstance(back.full.idx, np.memmap)
+    assert np.array_equal(extra["init"], np.arange(6.0))
+    for k in ("x", "y", "flag", "nx", "ny"):
+        assert np.array_equal(getattr(back.cloud, k), getattr(cloud, k))
+    assert_same(back, conn)

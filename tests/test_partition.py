@@ -185,3 +185,75 @@ def test_gloo_two_ranks_bitwise_global(small_naca, small_naca_conn):
         hist, prims, gid = out[rank]
         assert np.array_equal(np.array(hist), ref_hist)
         assert np.array_equal(prims, ref_prims[:, gid])
+
+
+def _sendlist_worker(rank, world, port, out):
+    import torch.distributed as dist
+
+    from paper_2108_07031_b200 import build_stencils, generate_naca_cloud
+    from paper_2108_07031_b200.dist import exchange_send_lists
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    conn = build_stencils(generate_naca_cloud(80, 30, 1.15, 20.0))
+    part = build_part(conn, rank, world, DEPTH)
+    exchange_send_lists(part, dist)
+    out[rank] = {k: v.copy() for k, v in part.send.items()}
+    dist.destroy_process_group()
+
+
+def test_gloo_send_lists_from_peer_receive_lists(small_naca_conn):
+    """dist.exchange_send_lists (all-gather of receive lists) == the
+    per-peer halo recomputation of send_lists_for, on 3 gloo ranks."""
+    import torch.multiprocessing as mp
+
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_sendlist_worker, args=(3, port, out), nprocs=3, join=True)
+    for rank in range(3):
+        ref = send_lists_for(small_naca_conn, rank, 3, DEPTH)
+        assert out[rank].keys() == ref.keys()
+        for peer in ref:
+            assert np.array_equal(out[rank][peer], ref[peer])
+
+
+def _setup_worker(rank, world, port, out):
+    import sys
+
+    import torch.distributed as dist
+
+    sys.path.insert(0, str(__import__("pathlib").Path(__file__).resolve().parent.parent))
+    import bench
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cloud, conn, cfg, init = bench.setup("c1", dist, rank)
+    out[rank] = (np.asarray(conn.full.idx[::97]).copy(), np.asarray(conn.split["y-"].sxx[::13]).copy(),
+                 init.as_array()[:, ::29].copy(), cfg.mach)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_shared_setup_store():
+    """bench.setup under 2 ranks: rank 0 builds, both map the /dev/shm store;
+    every rank sees the same connectivity and initial state as a direct build."""
+    import sys
+
+    import torch.multiprocessing as mp
+
+    sys.path.insert(0, str(__import__("pathlib").Path(__file__).resolve().parent.parent))
+    import bench
+
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_setup_worker, args=(2, port, out), nprocs=2, join=True)
+    cloud, conn, cfg, init = bench.build_config("c1")
+    for rank in (0, 1):
+        idx, sxx, ini, mach = out[rank]
+        assert np.array_equal(idx, conn.full.idx[::97])
+        assert np.array_equal(sxx, conn.split["y-"].sxx[::13])
+        assert np.array_equal(ini, init.as_array()[:, ::29]) and mach == cfg.mach

@@ -2,7 +2,6 @@
 OUT=gpurun_out/sweep.log
 run() { echo "== $SZ $*" >> $OUT; env "$@" timeout 300 python tools/quick_perf.py $SZ 2>&1 | grep -E "instrument=True|stage" >> $OUT; }
 for SZ in "3160 790 1.00734 10" "800 200 1.03 50"; do
-run KMF_FLUX_IMPL=3
-run KMF_FLUX_IMPL=4
-run KMF_FLUX_IMPL=4 KMF_FLUX_MINB=4
+run KMF_X=0
+run KMF_QG_STAGE=0
 done

@@ -68,3 +68,19 @@ def test_oracle_library_builds_and_is_separate():
         src = (ROOT / "paper_2108_07031_b200" / f"{mod}.py").read_text()
         assert not re.search(r"^\s*(from|import)\s+oracle", src, flags=re.M), mod
     assert pkg.__version__
+
+
+def test_builder_library_exports_every_symbol():
+    from paper_2108_07031_b200 import builder
+
+    text = re.sub(r"/\*.*?\*/", "", (ROOT / "include" / "kmf_build.h").read_text(), flags=re.S)
+    names = sorted(set(re.findall(r"\b(kmfb_[a-z0-9_]+)\s*\(", text)))
+    assert names == ["kmfb_assemble", "kmfb_knn", "kmfb_threads", "kmfb_visibility"]
+    so = ctypes.CDLL(str(builder.LIB_PATH))
+    for name in names:
+        assert hasattr(so, name), name
+    assert builder.lib().kmfb_threads() >= 1
+    # set-up code, not product compute: it must not depend on the oracle either
+    for mod in ("builder", "store", "partition", "dist", "reorder"):
+        src = (ROOT / "paper_2108_07031_b200" / f"{mod}.py").read_text()
+        assert not re.search(r"^\s*(from|import)\s+oracle", src, flags=re.M), mod

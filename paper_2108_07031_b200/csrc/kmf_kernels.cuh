@@ -1262,6 +1262,7 @@ __global__ void k_fastmath_probe(int n, const double *x, int which, double *out)
     case 0: r = fexp(v); break;
     case 1: r = ferf(v, fexp(-(v * v))); break;
     case 2: r = frcp(v); break;
+    case 4: r = fexp_tab(v, kExpT); break;
     default: r = frsqrt(v); break;
     }
     out[i] = r;

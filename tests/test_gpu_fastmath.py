@@ -48,6 +48,17 @@ def test_exp(gpu):
     assert ulps(probe(x, 0), ref).max() <= 1.0
 
 
+def test_exp_table(gpu):
+    """fexp_tab (lean flux path): 64-entry hi/lo table + degree-5 expm1."""
+    rng = np.random.default_rng(4)
+    x = np.concatenate([rng.uniform(-40, 40, 3000), rng.uniform(-1, 1, 1000), rng.uniform(-700, 700, 500),
+                        [0.0, 1.0, -1.0, 0.5, -0.3465, 0.3466, 0.0054, -0.0054]])
+    ref = np.array([float(D(v).exp()) for v in x])
+    assert ulps(probe(x, 4), ref).max() <= 1.0
+    out = probe(np.array([-800.0, -746.0, 709.0]), 4)
+    assert out[0] == 0.0 and out[1] == 0.0 and np.isfinite(out[2])
+
+
 def test_exp_underflow_and_nan(gpu):
     out = probe(np.array([-800.0, -746.0, 709.0, np.nan]), 0)
     assert out[0] == 0.0 and out[1] == 0.0 and np.isfinite(out[2]) and np.isnan(out[3])

@@ -1685,32 +1685,6 @@ extern "C" int kmf_set_partition(kmf_ctx *c, int64_t n_owned, int64_t n_global, 
     if (c->exec1) cudaGraphExecDestroy(c->exec1), c->exec1 = nullptr;
     if (c->execU) cudaGraphExecDestroy(c->execU), c->execU = nullptr;
     if (c->execB) cudaGraphExecDestroy(c->execB), c->execB = nullptr;
-    // One eager round of the exact send/recv pattern and of the limb
-    // all-reduce before any graph capture: NCCL sets its P2P connections up
-    // lazily at first use, which must not happen inside stream capture.
-    // Nothing is unpacked and the all-reduce runs on scratch memory, so the
-    // solver state is untouched.
-    if (c->dist_on) {
-        api.GroupStart();
-        for (size_t k = 0; k < c->peer_rank.size(); k++) {
-            if (c->send_cnt[k])
-                api.Send(c->sendbuf.p + 4 * c->send_off[k], 4 * c->send_cnt[k], ncclDouble, c->peer_rank[k], comm,
-                         c->s0);
-            if (c->recv_cnt[k])
-                api.Recv(c->recvbuf.p + 4 * c->recv_off[k], 4 * c->recv_cnt[k], ncclDouble, c->peer_rank[k], comm,
-                         c->s0);
-        }
-        r = api.GroupEnd();
-        DBuf<unsigned long long> scratch;
-        CK(scratch.alloc(kLimbs));
-        CK(cudaMemsetAsync(scratch.p, 0, sizeof(unsigned long long) * kLimbs, c->s0));
-        if (r == ncclSuccess) r = api.AllReduce(scratch.p, scratch.p, kLimbs, ncclUint64, ncclSum, comm, c->s0);
-        if (r != ncclSuccess) {
-            set_msg("NCCL warm-up exchange: %s", api.GetErrorString ? api.GetErrorString(r) : "error");
-            return KMF_ENCCL;
-        }
-        CK(cudaStreamSynchronize(c->s0));
-    }
     return KMF_OK;
 }
 

@@ -594,35 +594,31 @@ void launch_flux_t(kmf_ctx *c, cudaStream_t s, const double *G, int mode, double
         return;
     }
     const int nb = nblk(c->n);
-    if (c->flux_impl == 4 || c->flux_impl == 6) {  // lock-step body + next-edge L1 prefetch (fused only)
-        if (mode == 0) {
-            if (c->flux_impl == 6)
-                k_flux3<XY, -1, MINB, GK, 1, true><<<nb, kTB, 0, s>>>(g, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage);
-            else
-                k_flux3<XY, -1, MINB, GK, 1><<<nb, kTB, 0, s>>>(g, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage);
-            return;
-        }
-    }
-    if (c->flux_impl == 5) {  // lean lock-step (table exp, FMA perturbations)
-        if (mode == 0) {
-            k_flux3<XY, -1, MINB, GK, 0, true><<<nb, kTB, 0, s>>>(g, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage);
-        } else {
-            k_flux3<XY, 0, MINB, GK, 0, true><<<nb, kTB, 0, s>>>(g, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage);
-            k_flux3<XY, 1, MINB, GK, 0, true><<<nb, kTB, 0, s>>>(g, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage);
-            k_flux3<XY, 2, MINB, GK, 0, true><<<nb, kTB, 0, s>>>(g, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage);
-            k_flux3<XY, 3, MINB, GK, 0, true><<<nb, kTB, 0, s>>>(g, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage);
-        }
-        return;
-    }
     if (c->flux_impl >= 3) {
+        // 3 lock-step; 4 + next-edge L1 prefetch; 5 lean arithmetic (table
+        // exp, FMA perturbations); 6 = 4 + 5.  The prefetch only changes
+        // the schedule, so split4 uses the same arithmetic variant as fused
+        // and the two modes stay bitwise equal.
+        const bool lean = c->flux_impl >= 5, pf = c->flux_impl == 4 || c->flux_impl == 6;
+#define KMF_F3(FAM, PF, LEAN) \
+    k_flux3<XY, FAM, MINB, GK, PF, LEAN><<<nb, kTB, 0, s>>>(g, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage)
         if (mode == 0) {
-            k_flux3<XY, -1, MINB, GK><<<nb, kTB, 0, s>>>(g, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage);
+            if (lean && pf) KMF_F3(-1, 1, true);
+            else if (lean) KMF_F3(-1, 0, true);
+            else if (pf) KMF_F3(-1, 1, false);
+            else KMF_F3(-1, 0, false);
+        } else if (lean) {
+            KMF_F3(0, 0, true);
+            KMF_F3(1, 0, true);
+            KMF_F3(2, 0, true);
+            KMF_F3(3, 0, true);
         } else {
-            k_flux3<XY, 0, MINB, GK><<<nb, kTB, 0, s>>>(g, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage);
-            k_flux3<XY, 1, MINB, GK><<<nb, kTB, 0, s>>>(g, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage);
-            k_flux3<XY, 2, MINB, GK><<<nb, kTB, 0, s>>>(g, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage);
-            k_flux3<XY, 3, MINB, GK><<<nb, kTB, 0, s>>>(g, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage);
+            KMF_F3(0, 0, false);
+            KMF_F3(1, 0, false);
+            KMF_F3(2, 0, false);
+            KMF_F3(3, 0, false);
         }
+#undef KMF_F3
         return;
     }
     if (mode == 0) {

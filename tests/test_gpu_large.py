@@ -54,3 +54,67 @@ def test_c3_three_iterations_match_oracle(gpu, c3):
     rel = np.abs(res.residue_history - hist) / hist
     assert rel.max() <= 1e-10, rel
     assert np.allclose(res.primitives.as_array(), prims, rtol=1e-10, atol=1e-12)
+
+
+def test_c3_fused_equals_split4_bitwise(gpu, c3):
+    """At 2.5M points the HBM-streaming kernel variants are active (index
+    staging, flux prefetch + lean arithmetic); split4 must still equal fused."""
+    cloud, conn, cfg, init, _ = c3
+    a = solve(SolverConfig(mach=0.85, aoa_deg=1.0, n_outer=2, mode="fused"), cloud, conn, initial_state=init,
+              instrument=False)
+    b = solve(SolverConfig(mach=0.85, aoa_deg=1.0, n_outer=2, mode="split4"), cloud, conn, initial_state=init,
+              instrument=False)
+    assert np.array_equal(a.residue_history, b.residue_history)
+    assert np.array_equal(a.primitives.as_array(), b.primitives.as_array())
+
+
+# --------------------------------------------------------------- 40M (opt-in)
+# The bench's default configuration (BASELINE configs[4]): one whole outer
+# iteration of the device path against the oracle on all 39,992,976 points,
+# plus fused == split4 bitwise.  ~4 min and ~70 GB of host memory, so it runs
+# only with KMF_FULL_SIZE_TESTS=1 (results: profiles/r1_full_size_parity.txt).
+
+full_size = pytest.mark.skipif(not __import__("os").environ.get("KMF_FULL_SIZE_TESTS"),
+                               reason="set KMF_FULL_SIZE_TESTS=1 (40M points, ~4 min, ~70 GB host memory)")
+
+
+@pytest.fixture(scope="module")
+def c5():
+    cloud = generate_naca_cloud(12648, 3162, 1.001821, 20.0)
+    conn = build_stencils(cloud)
+    cfg = SolverConfig(mach=0.63, aoa_deg=2.0, n_outer=1)
+    return cloud, conn, cfg, initial_primitives(cfg, cloud)
+
+
+@full_size
+def test_c5_one_iteration_matches_oracle(gpu, c5):
+    import os
+    import time
+
+    cloud, conn, cfg, init = c5
+    t = time.perf_counter()
+    res = solve(cfg, cloud, conn, initial_state=init, instrument=False)
+    t_gpu = time.perf_counter() - t
+    O.set_threads(os.cpu_count() or 1)
+    pk = O.Packed(conn)
+    fs = free_stream(cfg.mach, cfg.aoa_deg)
+    t = time.perf_counter()
+    hist, prims, _, _, _ = O.solve(pk, init.as_array(), [fs.rho[0], fs.u1[0], fs.u2[0], fs.p[0]], 1)
+    t_cpu = time.perf_counter() - t
+    rel = abs(res.residue_history[0] - hist[0]) / hist[0]
+    err = np.abs(res.primitives.as_array() - prims) / (1e-12 + 1e-10 * np.abs(prims))
+    print(f"c5 one iteration: residue rel diff {rel:.3e}, max scaled state error {err.max():.3e}; "
+          f"device solve {t_gpu:.1f} s (incl. context), oracle {t_cpu:.1f} s")
+    assert rel <= 1e-10
+    assert np.allclose(res.primitives.as_array(), prims, rtol=1e-10, atol=1e-12)
+
+
+@full_size
+def test_c5_fused_equals_split4_bitwise(gpu, c5):
+    cloud, conn, cfg, init = c5
+    a = solve(SolverConfig(mach=0.63, aoa_deg=2.0, n_outer=2, mode="fused"), cloud, conn, initial_state=init,
+              instrument=False)
+    b = solve(SolverConfig(mach=0.63, aoa_deg=2.0, n_outer=2, mode="split4"), cloud, conn, initial_state=init,
+              instrument=False)
+    assert np.array_equal(a.residue_history, b.residue_history)
+    assert np.array_equal(a.primitives.as_array(), b.primitives.as_array())

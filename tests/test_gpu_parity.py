@@ -102,6 +102,23 @@ def test_fused_equals_split4_bitwise(gpu, pre, small_golden, small_naca_conn):
     assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("impl", ["3", "4", "5", "6"])
+def test_flux_kernel_variants_fused_split4_and_tolerance(gpu, impl, small_golden, small_naca, monkeypatch):
+    """Every flux kernel variant (lock-step, + L1 prefetch, lean arithmetic,
+    both; the last two are the defaults above 1M points): fused == split4
+    bitwise and the reference tolerance per call.  The variant is fixed when
+    a context is created, so each case builds a fresh connectivity."""
+    monkeypatch.setenv("KMF_FLUX_IMPL", impl)
+    conn = build_stencils(small_naca)
+    for pre in PREFIXES:
+        G, _ = small_golden
+        a = flux_residual(flow(G, pre), conn, "fused")
+        b = flux_residual(flow(G, pre), conn, "split4")
+        assert np.array_equal(a, b)
+        ref = G[f"{pre}.R_int"]
+        assert np.all(np.abs(a - ref) <= flux_tol(ref))
+
+
 @pytest.mark.parametrize("pre", PREFIXES)
 def test_boundary_closure_tolerance(gpu, pre, small_golden, small_naca_conn):
     G, _ = small_golden

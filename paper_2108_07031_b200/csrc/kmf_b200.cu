@@ -493,6 +493,7 @@ int build_context(kmf_ctx *c, const kmf_geometry *g)
     case 512: KCALL(512, 0); break;                     \
     case 129: KCALL(128, 1); break;                     \
     case 257: KCALL(256, 1); break;                     \
+    case 513: KCALL(512, 1); break;                     \
     default: KCALL(128, 0); break;                      \
     }
 
@@ -931,8 +932,12 @@ int kmf_create(kmf_ctx **out, const kmf_geometry *g, int device)
     c->qg_stage = c->n > 1000000 ? 1 : 0;
     if (const char *e = std::getenv("KMF_QG_STAGE")) c->qg_stage = std::atoi(e) ? 1 : 0;
     // likewise the flux kernel's next-edge L1 prefetch and 4 blocks/SM
-    // (-5.9 % flux time at 2.5M, +4 % at 160K)
+    // (-5.9 % flux time at 2.5M, +4 % at 160K), and one thread per point
+    // (NC = 4) in 256-thread blocks for the staged q-gradient kernels
+    // (-5 % / -6.8 % q-gradient time at 2.5M / 10M)
     const bool big = c->n > 1000000;
+    if (big && !std::getenv("KMF_QG_NC")) c->qg_nc = 4;
+    if (big && !std::getenv("KMF_QG_TB")) c->qg_tb = 256;
     c->flux_impl = big ? 6 : 3;  // 6: + lean arithmetic (table exp, FMA perturbations): -3.4 % at 2.5M
     c->flux_minb = big ? 4 : 3;
     if (const char *e = std::getenv("KMF_FLUX_MINB")) {

@@ -88,6 +88,7 @@ struct kmf_ctx {
     int qg_nc = 2;   // q-gradient components per thread (KMF_QG_NC)
     int qg_unroll = 1;  // q-gradient edge unroll (KMF_QG_UNROLL)
     int qg_tb = 128;    // q-gradient block size (KMF_QG_TB)
+    int qg_minb = 1;    // min resident blocks of the staged 256-thread q-gradient kernels (KMF_QG_MINB)
     int qg_stage = 0;   // stage ELL index slices in shared memory (KMF_QG_STAGE)
     int flux_impl = 3;  // interior flux kernel shape (KMF_FLUX_IMPL): 1 per-flux, 2 pair, 3 lock-step
     int flux_minb = 3;  // interior flux blocks per SM (KMF_FLUX_MINB)
@@ -489,19 +490,23 @@ int build_context(kmf_ctx *c, const kmf_geometry *g)
 // block size variants (KMF_QG_TB = 128, 256, 512)
 #define KMF_TB_SWITCH(KCALL)                            \
     switch (c->qg_tb + c->qg_stage) {                   \
-    case 256: KCALL(256, 0); break;                     \
-    case 512: KCALL(512, 0); break;                     \
-    case 129: KCALL(128, 1); break;                     \
-    case 257: KCALL(256, 1); break;                     \
-    case 513: KCALL(512, 1); break;                     \
-    default: KCALL(128, 0); break;                      \
+    case 256: KCALL(256, 0, 0); break;                  \
+    case 512: KCALL(512, 0, 0); break;                  \
+    case 129: KCALL(128, 1, 0); break;                  \
+    case 257:                                           \
+        if (c->qg_minb == 4) KCALL(256, 1, 4);          \
+        else if (c->qg_minb == 3) KCALL(256, 1, 3);     \
+        else KCALL(256, 1, 0);                          \
+        break;                                          \
+    case 513: KCALL(512, 1, 0); break;                  \
+    default: KCALL(128, 0, 0); break;                   \
     }
 
 template <bool XY, int NC, int U>
 void launch_fo_t(kmf_ctx *c, cudaStream_t s, double *G, Ctrl *ctl, int stage)
 {
-#define KMF_FO(TB, ST) \
-    k_first_order<XY, NC, U, TB, ST><<<nblk(c->n, qg_points_per_block<NC, TB>()), TB, 0, s>>>(c->dg(), c->q.p, G, ctl, stage)
+#define KMF_FO(TB, ST, MB) \
+    k_first_order<XY, NC, U, TB, ST, MB><<<nblk(c->n, qg_points_per_block<NC, TB>()), TB, 0, s>>>(c->dg(), c->q.p, G, ctl, stage)
     KMF_TB_SWITCH(KMF_FO)
 #undef KMF_FO
 }
@@ -510,8 +515,8 @@ template <bool XY, int NC, int U>
 void launch_sw_t(kmf_ctx *c, cudaStream_t s, const double *Gin, double *Gout, Ctrl *ctl, int stage, int slot,
                  int want_res)
 {
-#define KMF_SW(TB, ST)                                                                              \
-    k_sweep<XY, NC, U, TB, ST><<<nblk(c->n, qg_points_per_block<NC, TB>()), TB, 0, s>>>(c->dg(), c->q.p, Gin, Gout, \
+#define KMF_SW(TB, ST, MB)                                                                          \
+    k_sweep<XY, NC, U, TB, ST, MB><<<nblk(c->n, qg_points_per_block<NC, TB>()), TB, 0, s>>>(c->dg(), c->q.p, Gin, Gout, \
                                                                                   ctl, stage, slot, want_res)
     KMF_TB_SWITCH(KMF_SW)
 #undef KMF_SW
@@ -921,6 +926,7 @@ int kmf_create(kmf_ctx **out, const kmf_geometry *g, int device)
         if (v == 1 || v == 2 || v == 4) c->qg_unroll = v;
     }
     if (const char *e = std::getenv("KMF_QG_TB")) c->qg_tb = std::atoi(e);
+    if (const char *e = std::getenv("KMF_QG_MINB")) c->qg_minb = std::atoi(e);
     int rc = build_context(c, g);
     if (rc != KMF_OK) {
         delete c;

@@ -161,8 +161,8 @@ KMF_HD bool qg_stage_indices(const DG &g, int *sidx, int cap, int &e0)
 // TB: block size.  Larger blocks with a ring-tiled point order
 // (reorder.ring_tiles) put several radially stacked slices on one SM, so
 // the neighbour rings they share are fetched into L1 once.
-template <bool XY, int NC, int U, int TB = kTB, int ST = 0>
-__global__ void __launch_bounds__(TB) k_first_order(DG g, const double *__restrict__ q,
+template <bool XY, int NC, int U, int TB = kTB, int ST = 0, int MB = 0>
+__global__ void __launch_bounds__(TB, MB) k_first_order(DG g, const double *__restrict__ q,
                                                      double *__restrict__ G, Ctrl *c, int stage)
 {
     if (c && should_skip(c, stage, 0)) return;
@@ -219,8 +219,8 @@ __global__ void __launch_bounds__(TB) k_first_order(DG g, const double *__restri
 
 // lsq.py:214-227 one Jacobi sweep of the defect-corrected gradients --
 // bitwise.  With want_res the max |new - old| (lsq.py:238-243) is reduced.
-template <bool XY, int NC, int U, int TB = kTB, int ST = 0>
-__global__ void __launch_bounds__(TB) k_sweep(DG g, const double *__restrict__ q,
+template <bool XY, int NC, int U, int TB = kTB, int ST = 0, int MB = 0>
+__global__ void __launch_bounds__(TB, MB) k_sweep(DG g, const double *__restrict__ q,
                                                const double *__restrict__ Gin, double *__restrict__ Gout,
                                                Ctrl *c, int stage, int slot, int want_res)
 {

@@ -3,9 +3,5 @@ OUT=gpurun_out/sweep.log
 run() { echo "== $SZ $*" >> $OUT; env "$@" timeout 300 python tools/quick_perf.py $SZ 2>&1 | grep -E "instrument=True|stage" >> $OUT; }
 for SZ in "3160 790 1.00734 10" "6324 1581 1.003647 4"; do
 run KMF_X=0
-run KMF_QG_TB=256 KMF_QG_NC=4
-run KMF_QG_TB=512 KMF_QG_NC=4
-run KMF_QG_TB=256 KMF_QG_NC=2
-run KMF_QG_TB=512 KMF_QG_NC=2
-run KMF_QG_TB=256 KMF_QG_NC=4 KMF_QG_UNROLL=2
+run KMF_QG_MINB=4
 done

@@ -56,6 +56,10 @@ def _frame_struct(fr, keep) -> _lib.Frame:
 def _check_split_layout(conn: Connectivity):
     """The device derives split membership from the signs of full.dx/dy
     (geometry.py:544-549); refuse connectivities built differently."""
+    from .builder import SplitView
+
+    if all(isinstance(conn.split[k], SplitView) for k in SPLIT_KINDS):
+        return  # derived from the full stencil's signs by construction (builder.py)
     f = conn.full
     masks = {"x+": f.dx <= 0.0, "x-": f.dx >= 0.0, "y+": f.dy <= 0.0, "y-": f.dy >= 0.0}
     for kind, m in masks.items():

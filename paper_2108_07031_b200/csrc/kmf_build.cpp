@@ -292,12 +292,17 @@ int kmfb_visibility(int64_t n, const double *x, const double *y, int64_t nw, con
         return 0;
     }
     std::vector<double> wx(nw), wy(nw);
-    double maxsp = 0.0;
+    double maxsp = 0.0, bx0 = INFINITY, bx1 = -INFINITY, by0 = INFINITY, by1 = -INFINITY;
     for (int64_t a = 0; a < nw; a++) {
         wx[a] = x[wall[a]];
         wy[a] = y[wall[a]];
         maxsp = std::max(maxsp, spacing[a]);
+        bx0 = std::min(bx0, wx[a]);
+        bx1 = std::max(bx1, wx[a]);
+        by0 = std::min(by0, wy[a]);
+        by1 = std::max(by1, wy[a]);
     }
+    const double margin = 2.0 * maxsp * (1.0 + 1e-12);
     std::vector<int32_t> ids = iota32(nw);
     Tree t;
     t.build(wx.data(), wy.data(), ids.data(), nw);
@@ -310,6 +315,20 @@ int kmfb_visibility(int64_t n, const double *x, const double *y, int64_t nw, con
         for (int64_t r = 0; r < nrows; r++) {
             const int64_t o = owners ? owners[r] : r;
             const double x0 = x[o], y0 = y[o];
+            // cheap lower bound first: distance to the wall points' bounding
+            // box; owners far from the body keep every edge without a query
+            double lmax = 0.0;
+            for (int64_t e = ptr[r]; e < ptr[r + 1]; e++) {
+                const double ex = x[idx[e]] - x0, ey = y[idx[e]] - y0;
+                lmax = std::max(lmax, std::sqrt(ex * ex + ey * ey));
+            }
+            const double gx = std::max(0.0, std::max(bx0 - x0, x0 - bx1));
+            const double gy = std::max(0.0, std::max(by0 - y0, y0 - by1));
+            const double dbox = std::sqrt(gx * gx + gy * gy);
+            if (dbox * (1.0 - 1e-12) - lmax * (1.0 + 1e-12) > margin) {
+                for (int64_t e = ptr[r]; e < ptr[r + 1]; e++) keep[e] = 1;
+                continue;
+            }
             const double D0 = std::sqrt(t.nearest(x0, y0, ties));
             for (int64_t e = ptr[r]; e < ptr[r + 1]; e++) {
                 const int64_t j = idx[e];
@@ -317,7 +336,7 @@ int kmfb_visibility(int64_t n, const double *x, const double *y, int64_t nw, con
                 const double len = std::sqrt(ddx * ddx + ddy * ddy);
                 // every sample lies within len of the owner: its distance to
                 // any wall point exceeds 2*spacing[near] for sure
-                if (D0 * (1.0 - 1e-12) - len * (1.0 + 1e-12) > 2.0 * maxsp * (1.0 + 1e-12)) {
+                if (D0 * (1.0 - 1e-12) - len * (1.0 + 1e-12) > margin) {
                     keep[e] = 1;
                     continue;
                 }

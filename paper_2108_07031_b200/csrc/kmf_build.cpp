@@ -111,12 +111,12 @@ struct Tree {
         return dx * dx + dy * dy;
     }
 
-    // k smallest squared distances (max-heap `h` of size k); returns the k-th
     struct Frame {
         int64_t v, lo, hi;
     };
 
-    double kth_d2(double qx, double qy, int k, double *h) const
+    // the k smallest (d2, index) pairs, unordered, in h (max-heap on d2)
+    int knn_pairs(double qx, double qy, int k, std::pair<double, int32_t> *h) const
     {
         int hn = 0;
         Frame st[128];
@@ -129,11 +129,11 @@ struct Tree {
                     const int32_t p = perm[t];
                     const double v = d2(qx, qy, x[p], y[p]);
                     if (hn < k) {
-                        h[hn++] = v;
+                        h[hn++] = {v, p};
                         std::push_heap(h, h + hn);
-                    } else if (v < h[0]) {
+                    } else if (v < h[0].first) {
                         std::pop_heap(h, h + hn);
-                        h[hn - 1] = v;
+                        h[hn - 1] = {v, p};
                         std::push_heap(h, h + hn);
                     }
                 }
@@ -144,11 +144,10 @@ struct Tree {
             const double diff = q - split[f.v];
             const Frame nearf = diff <= 0.0 ? Frame{2 * f.v, f.lo, mid} : Frame{2 * f.v + 1, mid, f.hi};
             const Frame farf = diff <= 0.0 ? Frame{2 * f.v + 1, mid, f.hi} : Frame{2 * f.v, f.lo, mid};
-            // every point of the far side has d^2 >= diff^2 (monotone rounding)
-            if (hn < k || diff * diff <= h[0]) st[sp++] = farf;
+            if (hn < k || diff * diff <= h[0].first) st[sp++] = farf;
             st[sp++] = nearf;
         }
-        return hn ? h[0] : INFINITY;
+        return hn;
     }
 
     // all points with squared distance <= r2, appended to out
@@ -234,18 +233,53 @@ int kmfb_threads(void) { return omp_get_max_threads(); }
 // geometry.py:315-346 tie-inclusive kNN rows (self excluded, ascending).
 // Pass 1 (rows == NULL): counts[r] for each query row.  Pass 2: rows
 // filled at offsets ptr[r] (caller's prefix sum of counts).
+// Rows of the last counting pass, kept for the filling pass of the same
+// query (the two-call protocol would otherwise search everything twice).
+struct KnnCache {
+    const double *x = nullptr, *y = nullptr;
+    const int64_t *query = nullptr;
+    int64_t n = 0, nq = 0;
+    int k = 0;
+    std::vector<int64_t> off;
+    std::vector<int32_t> rows;
+};
+static KnnCache g_knn;
+
 int kmfb_knn(int64_t n, const double *x, const double *y, int k, int64_t nq, const int64_t *query,
              int64_t *counts, const int64_t *ptr, int64_t *rows)
 {
     if (n <= 0 || k < 1 || nq < 0) return 2;
+    if (rows && g_knn.x == x && g_knn.y == y && g_knn.query == query && g_knn.n == n && g_knn.nq == nq &&
+        g_knn.k == k) {
+#pragma omp parallel for schedule(static, 4096)
+        for (int64_t r = 0; r < nq; r++) {
+            int64_t o = ptr[r];
+            for (int64_t e = g_knn.off[r]; e < g_knn.off[r + 1]; e++) rows[o++] = g_knn.rows[e];
+        }
+        g_knn = KnnCache();
+        return 0;
+    }
+    g_knn = KnnCache();
     std::vector<int32_t> all = iota32(n);
     Tree t;
     t.build(x, y, all.data(), n);
     const int k_eff = (int)std::min<int64_t>(k + 1, n);
     int bad = 0;
+    // one traversal with a padded heap (k_eff + 8 nearest, like the
+    // reference's pad, geometry.py:329): D_k is the k_eff-th smallest; if
+    // the pad's farthest entry is provably beyond D_k the heap holds every
+    // point with d <= D_k, else (a distance plateau) a range query collects
+    // them.  sqrt(v) <= D can hold for v slightly above D^2, hence the
+    // (1 + 1e-15) widening before the exact filter.
+    const int kpad = (int)std::min<int64_t>(k_eff + 8, n);
+    const int nt = omp_get_max_threads();
+    std::vector<std::vector<int32_t>> tbuf(nt);                   // per-thread row storage
+    std::vector<std::vector<std::pair<int64_t, int64_t>>> tloc(nt);  // (query row, start in tbuf)
+    std::vector<int64_t> cnt(nq, 0);
 #pragma omp parallel
     {
-        std::vector<double> heap(k_eff + 1);
+        const int tid = omp_get_thread_num();
+        std::vector<std::pair<double, int32_t>> heap(kpad + 1);
         std::vector<int32_t> got;
         got.reserve(64);
 #pragma omp for schedule(dynamic, 1024)
@@ -257,23 +291,51 @@ int kmfb_knn(int64_t n, const double *x, const double *y, int k, int64_t nq, con
                 continue;
             }
             const double qx = x[i], qy = y[i];
-            const double D2 = t.kth_d2(qx, qy, k_eff, heap.data());
+            const int hn = t.knn_pairs(qx, qy, kpad, heap.data());
+            std::sort(heap.begin(), heap.begin() + hn);
+            const double D2 = heap[k_eff - 1].first;
             const double D = std::sqrt(D2);
             got.clear();
-            // sqrt(v) <= D can hold for v slightly above D2: widen, then filter exactly
-            t.range(qx, qy, D2 * (1.0 + 1e-15), [&](int32_t p, double v) {
-                if (p != i && std::sqrt(v) <= D) got.push_back(p);
-            });
-            std::sort(got.begin(), got.end());
-            if (!rows) {
-                counts[r] = (int64_t)got.size();
+            if (hn < n && heap[hn - 1].first > D2 * (1.0 + 1e-15)) {
+                for (int h = 0; h < hn; h++)
+                    if (heap[h].second != i && std::sqrt(heap[h].first) <= D) got.push_back(heap[h].second);
             } else {
-                int64_t o = ptr[r];
-                for (int32_t p : got) rows[o++] = p;
+                t.range(qx, qy, D2 * (1.0 + 1e-15), [&](int32_t p, double v) {
+                    if (p != i && std::sqrt(v) <= D) got.push_back(p);
+                });
             }
+            std::sort(got.begin(), got.end());
+            cnt[r] = (int64_t)got.size();
+            tloc[tid].push_back({r, (int64_t)tbuf[tid].size()});
+            tbuf[tid].insert(tbuf[tid].end(), got.begin(), got.end());
         }
     }
-    return bad ? 2 : 0;
+    if (bad) return 2;
+    std::vector<int64_t> off(nq + 1, 0);
+    for (int64_t r = 0; r < nq; r++) off[r + 1] = off[r] + cnt[r];
+    if (!rows) {
+        // counting pass: report the counts, keep the rows for the fill pass
+        std::memcpy(counts, cnt.data(), sizeof(int64_t) * nq);
+        g_knn.rows.resize(off[nq]);
+        for (int th = 0; th < nt; th++)
+            for (const auto &pl : tloc[th])
+                std::memcpy(g_knn.rows.data() + off[pl.first], tbuf[th].data() + pl.second,
+                            sizeof(int32_t) * cnt[pl.first]);
+        g_knn.off = std::move(off);
+        g_knn.x = x;
+        g_knn.y = y;
+        g_knn.query = query;
+        g_knn.n = n;
+        g_knn.nq = nq;
+        g_knn.k = k;
+        return 0;
+    }
+    for (int th = 0; th < nt; th++)
+        for (const auto &pl : tloc[th]) {
+            int64_t o = ptr[pl.first];
+            for (int64_t e = 0; e < cnt[pl.first]; e++) rows[o++] = tbuf[th][pl.second + e];
+        }
+    return 0;
 }
 
 // geometry.py:396-450 visibility filter.  Wall statistics (spacing, tol)

@@ -68,6 +68,20 @@ def test_c3_fused_equals_split4_bitwise(gpu, c3):
     assert np.array_equal(a.primitives.as_array(), b.primitives.as_array())
 
 
+def test_c3_partitioned_solve_bitwise(gpu, c3):
+    """Two partitions of the 2.5M cloud (1.25M owned points each: the
+    HBM-streaming kernel variants, on partitioned contexts) reproduce the
+    single-domain history and state bit for bit."""
+    from paper_2108_07031_b200.dist import solve_group
+
+    cloud, conn, cfg, init, _ = c3
+    two = SolverConfig(mach=0.85, aoa_deg=1.0, n_outer=2)
+    ref = solve(two, cloud, conn, initial_state=init, instrument=False)
+    hist, prims, U, _ = solve_group(two, cloud, conn, 2, initial_state=init)
+    assert np.array_equal(hist, ref.residue_history)
+    assert np.array_equal(prims, ref.primitives.as_array())
+
+
 # --------------------------------------------------------------- 40M (opt-in)
 # The bench's default configuration (BASELINE configs[4]): one whole outer
 # iteration of the device path against the oracle on all 39,992,976 points,

@@ -493,11 +493,13 @@ int build_context(kmf_ctx *c, const kmf_geometry *g)
     case 256: KCALL(256, 0, 0); break;                  \
     case 512: KCALL(512, 0, 0); break;                  \
     case 129: KCALL(128, 1, 0); break;                  \
+    case 130: KCALL(128, 2, 0); break;                  \
     case 257:                                           \
         if (c->qg_minb == 4) KCALL(256, 1, 4);          \
         else if (c->qg_minb == 3) KCALL(256, 1, 3);     \
         else KCALL(256, 1, 0);                          \
         break;                                          \
+    case 258: KCALL(256, 2, 0); break;                  \
     case 513: KCALL(512, 1, 0); break;                  \
     default: KCALL(128, 0, 0); break;                   \
     }
@@ -932,11 +934,13 @@ int kmf_create(kmf_ctx **out, const kmf_geometry *g, int device)
         delete c;
         return rc;
     }
-    // index staging pays once the stencil streams from HBM (measured: -6.5 %
-    // q-gradient time at 2.5M / 10M points) and costs L1 capacity when the
-    // working set is L2-resident (+7 % at 160K); KMF_QG_STAGE overrides
-    c->qg_stage = c->n > 1000000 ? 1 : 0;
-    if (const char *e = std::getenv("KMF_QG_STAGE")) c->qg_stage = std::atoi(e) ? 1 : 0;
+    // index staging pays once the stencil streams from HBM and costs L1
+    // capacity when the working set is L2-resident: 1 = cooperative loads
+    // (-6.5 % q-gradient time at 2.5M / 10M, +7 % at 160K), 2 = one TMA
+    // bulk copy per block (a further -8.5 %, neutral at 160K); KMF_QG_STAGE
+    // overrides
+    c->qg_stage = c->n > 1000000 ? 2 : 0;
+    if (const char *e = std::getenv("KMF_QG_STAGE")) c->qg_stage = std::atoi(e);
     // likewise the flux kernel's next-edge L1 prefetch and 4 blocks/SM
     // (-5.9 % flux time at 2.5M, +4 % at 160K), and one thread per point
     // (NC = 4) in 256-thread blocks for the staged q-gradient kernels

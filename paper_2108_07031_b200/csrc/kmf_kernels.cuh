@@ -152,6 +152,47 @@ KMF_HD bool qg_stage_indices(const DG &g, int *sidx, int cap, int &e0)
     return staged;
 }
 
+// ST = 2: the same staging as ONE TMA bulk copy.  The block's slices are
+// contiguous in the ELL table (offsets are multiples of 32 entries, so
+// the source is 128 B aligned and the size a multiple of 128 B); one
+// thread arms an mbarrier with the byte count and issues
+// cp.async.bulk global -> shared, every thread waits on the barrier's
+// phase.  No register staging, no per-thread load/store round trips.
+KMF_HD uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+template <int SPB>
+KMF_HD bool qg_stage_indices_tma(const DG &g, int *sidx, int cap, int &e0, unsigned long long *mbar)
+{
+    const int ns = (g.n + 31) >> 5;
+    const int s0 = blockIdx.x * SPB;
+    e0 = g.eoff[s0];
+    const int esz = g.eoff[min(s0 + SPB, ns)] - e0;
+    const bool staged = esz <= cap && esz > 0;
+    const uint32_t bar = smem_u32(mbar);
+    if (staged && threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        const uint32_t bytes = (uint32_t)esz * 4u;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(sidx)),
+            "l"(g.eidx + e0), "r"(bytes), "r"(bar)
+            : "memory");
+    }
+    __syncthreads();  // the barrier is initialised before anyone polls it
+    if (staged) {
+        uint32_t done = 0;
+        while (!done)
+            asm volatile(
+                "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                : "=r"(done)
+                : "r"(bar)
+                : "memory");
+    }
+    return staged;
+}
+
 // The edge loop is unrolled by U: the U neighbour indices, then all their
 // gathers, are issued before any arithmetic (U-fold memory-level
 // parallelism); the accumulation itself stays strictly in slot order and
@@ -167,9 +208,12 @@ __global__ void __launch_bounds__(TB, MB) k_first_order(DG g, const double *__re
 {
     if (c && should_skip(c, stage, 0)) return;
     constexpr int SPB = TB * NC / 4 / 32, CAP = ST ? SPB * 32 * 24 : 1;
-    __shared__ int sidx[CAP];
+    __shared__ __align__(128) int sidx[CAP];
+    __shared__ unsigned long long mbar;
     int e0 = 0;
-    const bool staged = ST ? qg_stage_indices<SPB>(g, sidx, CAP, e0) : false;
+    const bool staged = ST == 2   ? qg_stage_indices_tma<SPB>(g, sidx, CAP, e0, &mbar)
+                        : ST == 1 ? qg_stage_indices<SPB>(g, sidx, CAP, e0)
+                                  : false;
     int i, k0;
     qg_thread<NC, TB>(i, k0);
     if (i >= g.n) return;
@@ -226,9 +270,12 @@ __global__ void __launch_bounds__(TB, MB) k_sweep(DG g, const double *__restrict
 {
     if (c && should_skip(c, stage, slot)) return;
     constexpr int SPB = TB * NC / 4 / 32, CAP = ST ? SPB * 32 * 24 : 1;
-    __shared__ int sidx[CAP];
+    __shared__ __align__(128) int sidx[CAP];
+    __shared__ unsigned long long mbar;
     int e0 = 0;
-    const bool staged = ST ? qg_stage_indices<SPB>(g, sidx, CAP, e0) : false;
+    const bool staged = ST == 2   ? qg_stage_indices_tma<SPB>(g, sidx, CAP, e0, &mbar)
+                        : ST == 1 ? qg_stage_indices<SPB>(g, sidx, CAP, e0)
+                                  : false;
     int i, k0;
     qg_thread<NC, TB>(i, k0);
     double rmax = 0.0;

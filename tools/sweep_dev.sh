@@ -1,11 +1,8 @@
 # development sweep of kernel shapes (not part of the bench); output in gpurun_out/sweep.log
 OUT=gpurun_out/sweep.log
 run() { echo "== $SZ $*" >> $OUT; env "$@" timeout 300 python tools/quick_perf.py $SZ 2>&1 | grep -E "instrument=True|stage" >> $OUT; }
-SZ="3160 790 1.00734 10"
-run KMF_X=0
-run KMF_FLUX_MINB=5
-SZ="800 200 1.03 50"
-run KMF_X=0
-run KMF_FLUX_IMPL=5
-run KMF_FLUX_IMPL=6
-run KMF_FLUX_IMPL=6 KMF_FLUX_MINB=4
+for SZ in "3160 790 1.00734 10" "6324 1581 1.003647 4"; do
+run KMF_QG_STAGE=2
+run KMF_QG_STAGE=3 KMF_QG_TILE_NC=1
+run KMF_QG_STAGE=3 KMF_QG_TILE_NC=2
+done

@@ -2,7 +2,7 @@
 OUT=gpurun_out/sweep.log
 run() { echo "== $SZ $*" >> $OUT; env "$@" timeout 300 python tools/quick_perf.py $SZ 2>&1 | grep -E "instrument=True|stage" >> $OUT; }
 for SZ in "3160 790 1.00734 10" "6324 1581 1.003647 4"; do
-run KMF_QG_STAGE=2
-run KMF_QG_STAGE=3 KMF_QG_TILE_NC=1
-run KMF_QG_STAGE=3 KMF_QG_TILE_NC=2
+run KMF_FLUX_IMPL=6
+run KMF_FLUX_IMPL=7
 done
+SZ="800 200 1.03 50"; run KMF_FLUX_IMPL=3; run KMF_FLUX_IMPL=7 KMF_FLUX_MINB=3

@@ -257,3 +257,22 @@ def test_gloo_shared_setup_store():
         assert np.array_equal(idx, conn.full.idx[::97])
         assert np.array_equal(sxx, conn.split["y-"].sxx[::13])
         assert np.array_equal(ini, init.as_array()[:, ::29]) and mach == cfg.mach
+
+
+def test_oracle_n_act_equals_owned_flux_view(small_naca_conn, small_naca):
+    """oracle n_act (flux and residue on a partition's owned rows, used for
+    the bounded CPU samples of bench.py) == the owned-row flux view."""
+    part = build_part(small_naca_conn, 1, 3, DEPTH)
+    init = perturbed_state(small_naca).as_array()[:, part.global_ids]
+    pk = O.Packed(part.conn)
+    pk.c.n_act = part.n_owned
+    ref = O.Packed(flux_view(part.conn, part.n_owned))
+    q = O.primitives_to_q(init)
+    qx, qy, _ = O.q_derivatives(pk, q, 3)
+    a = O.flux_residual(pk, q, qx, qy)
+    b = O.flux_residual(ref, q, qx, qy)
+    no = part.n_owned
+    assert np.array_equal(a[:, :no], b[:, :no]) and not a[:, no:].any()
+    # a sampled solve runs without touching the (garbage) halo fluxes
+    hist, _, _, its, _ = O.solve(pk, init, fs_vec(0.63, 2.0), 2)
+    assert its == 2 and np.all(np.isfinite(hist))

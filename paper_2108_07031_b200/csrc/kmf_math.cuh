@@ -95,6 +95,17 @@ KMF_HD double qtilde(double q, double gx, double gy, double dx, double dy)
     return SUB(q, MUL(0.5, ADD(MUL(dx, gx), MUL(dy, gy))));
 }
 
+// The same value from pre-halved offsets hdx = 0.5*dx, hdy = 0.5*dy (shared
+// by all components of an edge): scaling by 0.5 commutes with round-to-
+// nearest as long as no intermediate drops below 2^-1021 (|dx*gx| far from
+// subnormal here), so RN(hdx*gx) + RN(hdy*gy) rounds to exactly
+// 0.5*RN(RN(dx*gx) + RN(dy*gy)): bit-identical with one multiply fewer on
+// the dependency chain.
+KMF_HD double qtilde_h(double q, double gx, double gy, double hdx, double hdy)
+{
+    return SUB(q, ADD(MUL(hdx, gx), MUL(hdy, gy)));
+}
+
 // ------------------------------------------------------------- tolerance
 
 // Decoded perturbed edge state (state.py:141-163 restated for the FP64

@@ -88,6 +88,7 @@ struct kmf_ctx {
     int qg_nc = 2;   // q-gradient components per thread (KMF_QG_NC)
     int qg_unroll = 1;  // q-gradient edge unroll (KMF_QG_UNROLL)
     int qg_tb = 128;    // q-gradient block size (KMF_QG_TB)
+    bool pdl = false;   // programmatic dependent launch in the iteration graph (KMF_PDL)
     int qg_minb = 1;    // min resident blocks of the staged 256-thread q-gradient kernels (KMF_QG_MINB)
     int qg_stage = 0;   // stage ELL index slices in shared memory (KMF_QG_STAGE)
     int flux_impl = 3;  // interior flux kernel shape (KMF_FLUX_IMPL): 1 per-flux, 2 pair, 3 lock-step
@@ -486,6 +487,26 @@ int build_context(kmf_ctx *c, const kmf_geometry *g)
 }
 
 // ------------------------------------------------------------ stage launch
+// Kernel launch with programmatic stream serialization (PDL) when enabled:
+// the kernel may start its geometry prologue while the previous kernel of
+// the stream drains (the kernels synchronise with pdl_wait before touching
+// solver state).  Captured into the iteration graph as programmatic edges.
+template <typename... KArgs, typename... Args>
+void launch_ex(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+               Args &&...args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // block size variants (KMF_QG_TB = 128, 256, 512)
 #define KMF_TB_SWITCH(KCALL)                            \
@@ -507,8 +528,9 @@ int build_context(kmf_ctx *c, const kmf_geometry *g)
 template <bool XY, int NC, int U>
 void launch_fo_t(kmf_ctx *c, cudaStream_t s, double *G, Ctrl *ctl, int stage)
 {
-#define KMF_FO(TB, ST, MB) \
-    k_first_order<XY, NC, U, TB, ST, MB><<<nblk(c->n, qg_points_per_block<NC, TB>()), TB, 0, s>>>(c->dg(), c->q.p, G, ctl, stage)
+#define KMF_FO(TB, ST, MB)                                                                                        \
+    launch_ex(c->pdl, k_first_order<XY, NC, U, TB, ST, MB>, dim3(nblk(c->n, qg_points_per_block<NC, TB>())), dim3(TB), \
+              0, s, c->dg(), (const double *)c->q.p, G, ctl, stage)
     KMF_TB_SWITCH(KMF_FO)
 #undef KMF_FO
 }
@@ -517,9 +539,9 @@ template <bool XY, int NC, int U>
 void launch_sw_t(kmf_ctx *c, cudaStream_t s, const double *Gin, double *Gout, Ctrl *ctl, int stage, int slot,
                  int want_res)
 {
-#define KMF_SW(TB, ST, MB)                                                                          \
-    k_sweep<XY, NC, U, TB, ST, MB><<<nblk(c->n, qg_points_per_block<NC, TB>()), TB, 0, s>>>(c->dg(), c->q.p, Gin, Gout, \
-                                                                                  ctl, stage, slot, want_res)
+#define KMF_SW(TB, ST, MB)                                                                                  \
+    launch_ex(c->pdl, k_sweep<XY, NC, U, TB, ST, MB>, dim3(nblk(c->n, qg_points_per_block<NC, TB>())), dim3(TB), 0, \
+              s, c->dg(), (const double *)c->q.p, Gin, Gout, ctl, stage, slot, want_res)
     KMF_TB_SWITCH(KMF_SW)
 #undef KMF_SW
 }
@@ -608,8 +630,9 @@ void launch_flux_t(kmf_ctx *c, cudaStream_t s, const double *G, int mode, double
         // the schedule, so split4 uses the same arithmetic variant as fused
         // and the two modes stay bitwise equal.
         const bool lean = c->flux_impl >= 5, pf = c->flux_impl == 4 || c->flux_impl == 6;
-#define KMF_F3(FAM, PF, LEAN) \
-    k_flux3<XY, FAM, MINB, GK, PF, LEAN><<<nb, kTB, 0, s>>>(g, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage)
+#define KMF_F3(FAM, PF, LEAN)                                                                                 \
+    launch_ex(c->pdl, k_flux3<XY, FAM, MINB, GK, PF, LEAN>, dim3(nb), dim3(kTB), 0, s, g, q, G, R, inv_gm1, c_i0, \
+              zero_bnd, ctl, stage)
         if (mode == 0) {
             if (lean && pf) KMF_F3(-1, 1, true);
             else if (lean) KMF_F3(-1, 0, true);
@@ -928,6 +951,7 @@ int kmf_create(kmf_ctx **out, const kmf_geometry *g, int device)
         if (v == 1 || v == 2 || v == 4) c->qg_unroll = v;
     }
     if (const char *e = std::getenv("KMF_QG_TB")) c->qg_tb = std::atoi(e);
+    if (const char *e = std::getenv("KMF_PDL")) c->pdl = std::atoi(e) != 0;
     if (const char *e = std::getenv("KMF_QG_MINB")) c->qg_minb = std::atoi(e);
     int rc = build_context(c, g);
     if (rc != KMF_OK) {

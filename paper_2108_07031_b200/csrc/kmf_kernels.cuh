@@ -115,6 +115,16 @@ KMF_HD void edge_offsets(const DG &g, int ent, int j, double xi, double yi, doub
 
 KMF_HD int ell_base(const DG &g, int i) { return g.eoff[i >> 5] + (i & 31); }
 
+// Programmatic dependent launch (kernels launched with the PDL attribute,
+// launch_ex in kmf_b200.cu): pdl_trigger lets the next kernel of the
+// stream be scheduled while this grid's last wave drains; pdl_wait blocks
+// until the previous grid has completed and its writes are visible.  Each
+// kernel does its geometry-only prologue (indices, coordinates, TMA index
+// staging) before pdl_wait and touches solver state only after it.  Both
+// are no-ops for kernels launched without the attribute.
+KMF_HD void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+KMF_HD void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ---------------------------------------------------------------------------
 // q-gradient kernels: NC components of one point per thread (NC = 1, 2, 4).
 // The four components of q are independent in every LS sum, so splitting
@@ -206,7 +216,7 @@ template <bool XY, int NC, int U, int TB = kTB, int ST = 0, int MB = 0>
 __global__ void __launch_bounds__(TB, MB) k_first_order(DG g, const double *__restrict__ q,
                                                      double *__restrict__ G, Ctrl *c, int stage)
 {
-    if (c && should_skip(c, stage, 0)) return;
+    pdl_trigger();
     constexpr int SPB = TB * NC / 4 / 32, CAP = ST ? SPB * 32 * 24 : 1;
     __shared__ __align__(128) int sidx[CAP];
     __shared__ unsigned long long mbar;
@@ -214,6 +224,8 @@ __global__ void __launch_bounds__(TB, MB) k_first_order(DG g, const double *__re
     const bool staged = ST == 2   ? qg_stage_indices_tma<SPB>(g, sidx, CAP, e0, &mbar)
                         : ST == 1 ? qg_stage_indices<SPB>(g, sidx, CAP, e0)
                                   : false;
+    pdl_wait();
+    if (c && should_skip(c, stage, 0)) return;
     int i, k0;
     qg_thread<NC, TB>(i, k0);
     if (i >= g.n) return;
@@ -268,7 +280,7 @@ __global__ void __launch_bounds__(TB, MB) k_sweep(DG g, const double *__restrict
                                                const double *__restrict__ Gin, double *__restrict__ Gout,
                                                Ctrl *c, int stage, int slot, int want_res)
 {
-    if (c && should_skip(c, stage, slot)) return;
+    pdl_trigger();
     constexpr int SPB = TB * NC / 4 / 32, CAP = ST ? SPB * 32 * 24 : 1;
     __shared__ __align__(128) int sidx[CAP];
     __shared__ unsigned long long mbar;
@@ -276,6 +288,8 @@ __global__ void __launch_bounds__(TB, MB) k_sweep(DG g, const double *__restrict
     const bool staged = ST == 2   ? qg_stage_indices_tma<SPB>(g, sidx, CAP, e0, &mbar)
                         : ST == 1 ? qg_stage_indices<SPB>(g, sidx, CAP, e0)
                                   : false;
+    pdl_wait();
+    if (c && should_skip(c, stage, slot)) return;
     int i, k0;
     qg_thread<NC, TB>(i, k0);
     double rmax = 0.0;

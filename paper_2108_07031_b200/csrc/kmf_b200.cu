@@ -972,7 +972,9 @@ int kmf_create(kmf_ctx **out, const kmf_geometry *g, int device)
     const bool big = c->n > 1000000;
     if (big && !std::getenv("KMF_QG_NC")) c->qg_nc = 4;
     if (big && !std::getenv("KMF_QG_TB")) c->qg_tb = 256;
-    c->flux_impl = big ? 6 : 3;  // 6: + lean arithmetic (table exp, FMA perturbations): -3.4 % at 2.5M
+    // 5: lean arithmetic (table exp, FMA perturbations, select-free family
+    // accumulation): -4.3 % flux time at 160K; 6: + next-edge prefetch
+    c->flux_impl = big ? 6 : 5;
     c->flux_minb = big ? 4 : 3;
     if (const char *e = std::getenv("KMF_FLUX_MINB")) {
         int v = std::atoi(e);

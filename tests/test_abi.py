@@ -5,7 +5,6 @@ fallback).  CPU only (no compute calls)."""
 import ctypes
 import re
 
-import numpy as np
 import pytest
 
 from conftest import ROOT

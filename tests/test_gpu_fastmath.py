@@ -2,7 +2,6 @@
 100-digit decimal references: exp <= 1 ulp, erf <= 1 ulp of max(|erf|, 0.1),
 reciprocal / rsqrt <= 1 ulp."""
 
-import ctypes as C
 from decimal import Decimal as D, getcontext
 
 import numpy as np

@@ -5,7 +5,7 @@ import pytest
 
 from conftest import perturbed_state
 from paper_2108_07031_b200 import SolverConfig, compute_q_derivatives, solve
-from paper_2108_07031_b200 import _device, reorder
+from paper_2108_07031_b200 import _device
 
 pytestmark = pytest.mark.gpu
 

@@ -9,7 +9,6 @@ from __future__ import annotations
 
 import ctypes as C
 import os
-import threading
 import weakref
 
 import numpy as np
@@ -112,7 +111,6 @@ class DeviceConnectivity:
         _lib.check(_lib.lib().kmf_create(C.byref(h), C.byref(g), _lib.device_index() if device is None else device),
                    "kmf_create")
         self._h = h
-        self._lock = threading.Lock()
         self._fin = weakref.finalize(self, _lib.lib().kmf_destroy, h)
 
     @property

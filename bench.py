@@ -68,6 +68,9 @@ UNIT = "point-iterations/s"
 # algorithmic work of flux_residual interior per point-stage
 FLUX_BYTES_PER_POINT = 337
 FLUX_DP_OPS_PER_POINT = 13214
+# algorithmic bytes / DP ops of one whole point-iteration
+# (timestep, 4 x [q, first order, 3 sweeps, flux, update], residue)
+ITER_BYTES_PER_POINT = 6440
 L2_FLUSH_BYTES = 256 << 20
 
 
@@ -394,6 +397,12 @@ def run_ours(args):
                      "bytes_per_point": FLUX_BYTES_PER_POINT, "launch_us": flux_launch_s * 1e6,
                      "share_of_step": stage_share,
                      "note": "the flux kernel is FP64-pipe bound (SURVEY.md 8(d)); see roofline_fp64"},
+        "roofline_iteration": {
+            "bound": "hbm", "bytes_per_point_iter": ITER_BYTES_PER_POINT,
+            "achieved": ITER_BYTES_PER_POINT * value / 1e9, "peak": hbm_peak, "unit": "GB/s",
+            "frac": ITER_BYTES_PER_POINT * value / 1e9 / hbm_peak,
+            "note": "whole outer iteration against the HBM roofline implied by SURVEY 8(d)'s 6.44 KB per "
+                    "point-iteration (north star); value is the whole-job point-iterations/s"},
         "roofline_fp64": roofline_fp64(counts, n, n_flux, flux_launch_s, dfma_rate, achieved_ops, peak_fp64.value),
         "clocks": clk.summary(),
     }

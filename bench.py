@@ -399,10 +399,10 @@ def run_ours(args):
                      "note": "the flux kernel is FP64-pipe bound (SURVEY.md 8(d)); see roofline_fp64"},
         "roofline_iteration": {
             "bound": "hbm", "bytes_per_point_iter": ITER_BYTES_PER_POINT,
-            "achieved": ITER_BYTES_PER_POINT * value / 1e9, "peak": hbm_peak, "unit": "GB/s",
-            "frac": ITER_BYTES_PER_POINT * value / 1e9 / hbm_peak,
+            "achieved": ITER_BYTES_PER_POINT * value / ws / 1e9, "peak": hbm_peak, "unit": "GB/s",
+            "frac": ITER_BYTES_PER_POINT * value / ws / 1e9 / hbm_peak,
             "note": "whole outer iteration against the HBM roofline implied by SURVEY 8(d)'s 6.44 KB per "
-                    "point-iteration (north star); value is the whole-job point-iterations/s"},
+                    "point-iteration (north star), per GPU"},
         "roofline_fp64": roofline_fp64(counts, n, n_flux, flux_launch_s, dfma_rate, achieved_ops, peak_fp64.value),
         "clocks": clk.summary(),
     }

@@ -132,3 +132,27 @@ def test_c5_fused_equals_split4_bitwise(gpu, c5):
               instrument=False)
     assert np.array_equal(a.residue_history, b.residue_history)
     assert np.array_equal(a.primitives.as_array(), b.primitives.as_array())
+
+
+@full_size
+def test_c2_thousand_iterations_match_oracle(gpu):
+    """BASELINE configs[1] (160K points, M 0.63, AoA 2) for the paper's 1000
+    iterations: residue history within 1e-10 relative per iteration and
+    final primitives within rtol 1e-10 / atol 1e-12 of the oracle."""
+    import os
+
+    cloud = generate_naca_cloud(800, 200, 1.03, 20.0)
+    conn = build_stencils(cloud)
+    cfg = SolverConfig(mach=0.63, aoa_deg=2.0, n_outer=1000)
+    init = initial_primitives(cfg, cloud)
+    res = solve(cfg, cloud, conn, initial_state=init, instrument=False)
+    O.set_threads(os.cpu_count() or 1)
+    fs = free_stream(cfg.mach, cfg.aoa_deg)
+    hist, prims, _, its, _ = O.solve(O.Packed(conn), init.as_array(), [fs.rho[0], fs.u1[0], fs.u2[0], fs.p[0]], 1000)
+    assert res.iterations == its == 1000
+    rel = np.abs(res.residue_history - hist) / hist
+    err = np.abs(res.primitives.as_array() - prims) / (1e-12 + 1e-10 * np.abs(prims))
+    print(f"c2 1000 iterations: max residue rel diff {rel.max():.3e} (at iteration {int(rel.argmax()) + 1}), "
+          f"max scaled state error {err.max():.3e}; residue {hist[0]:.6e} -> {hist[-1]:.6e}")
+    assert rel.max() <= 1e-10
+    assert np.allclose(res.primitives.as_array(), prims, rtol=1e-10, atol=1e-12)

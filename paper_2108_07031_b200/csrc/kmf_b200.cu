@@ -958,20 +958,19 @@ int kmf_create(kmf_ctx **out, const kmf_geometry *g, int device)
         delete c;
         return rc;
     }
-    // index staging pays once the stencil streams from HBM and costs L1
-    // capacity when the working set is L2-resident: 1 = cooperative loads
-    // (-6.5 % q-gradient time at 2.5M / 10M, +7 % at 160K), 2 = one TMA
-    // bulk copy per block (a further -8.5 %, neutral at 160K); KMF_QG_STAGE
-    // overrides
-    c->qg_stage = c->n > 1000000 ? 2 : 0;
+    // q-gradient ELL index staging: 1 = cooperative loads (-6.5 % at 2.5M,
+    // +7 % at 160K: costs L1 capacity), 2 = one TMA bulk copy per block
+    // (default at every size: -8.5 % at 2.5M / 10M, and with the pre-halved
+    // offsets it enables -11 % at 40K); KMF_QG_STAGE overrides
+    c->qg_stage = 2;
     if (const char *e = std::getenv("KMF_QG_STAGE")) c->qg_stage = std::atoi(e);
-    // likewise the flux kernel's next-edge L1 prefetch and 4 blocks/SM
-    // (-5.9 % flux time at 2.5M, +4 % at 160K), and one thread per point
-    // (NC = 4) in 256-thread blocks for the staged q-gradient kernels
-    // (-5 % / -6.8 % q-gradient time at 2.5M / 10M)
+    // the flux kernel's next-edge L1 prefetch and 4 blocks/SM pay once the
+    // cloud streams from HBM (-5.9 % flux time at 2.5M, +4 % at 160K)
     const bool big = c->n > 1000000;
-    if (big && !std::getenv("KMF_QG_NC")) c->qg_nc = 4;
-    if (big && !std::getenv("KMF_QG_TB")) c->qg_tb = 256;
+    // with the TMA index staging and pre-halved offsets: one thread per point
+    // (NC = 4) in 128-thread blocks from 160K points up (-6 % q-gradient
+    // time at 160K / 2.5M / 10M); small clouds keep 2 threads per point
+    if (c->n > 100000 && !std::getenv("KMF_QG_NC")) c->qg_nc = 4;
     // 5: lean arithmetic (table exp, FMA perturbations, select-free family
     // accumulation): -4.3 % flux time at 160K; 6: + next-edge prefetch
     c->flux_impl = big ? 6 : 5;

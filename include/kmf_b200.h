@@ -247,7 +247,8 @@ int kmf_bench_steps(kmf_ctx *ctx, const kmf_params *p, int n_steps, int64_t flus
 /* measured FP64 (DFMA) pipe peak of the current device, TFLOP/s */
 int kmf_fp64_peak(double *tflops);
 /* device transcendentals of the flux path on host inputs (accuracy tests):
- * which 0 exp, 1 erf, 2 reciprocal, 3 reciprocal square root, 4 table exp */
+ * which 0 exp, 1 erf, 2 reciprocal, 3 reciprocal square root, 4 table exp,
+ * 5 table exp without clamps (arguments <= 0) */
 int kmf_fastmath_probe(int64_t n, const double *x, int which, double *out);
 /* pinned host memory for host-buffer (end-to-end) transfers */
 void *kmf_host_alloc(int64_t bytes);

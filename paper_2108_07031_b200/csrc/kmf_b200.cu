@@ -1646,7 +1646,7 @@ void kmf_host_free(void *p)
 
 extern "C" int kmf_fastmath_probe(int64_t n, const double *x, int which, double *out)
 {
-    if (n <= 0 || !x || !out || which < 0 || which > 4) return KMF_EINVAL;
+    if (n <= 0 || !x || !out || which < 0 || which > 5) return KMF_EINVAL;
     if (int rc = ensure_device()) return rc;
     Tmp tmp;
     TMP_OR_FAIL(dx, double, n);

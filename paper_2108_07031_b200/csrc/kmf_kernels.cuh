@@ -1329,6 +1329,7 @@ __global__ void k_fastmath_probe(int n, const double *x, int which, double *out)
     case 1: r = ferf(v, fexp(-(v * v))); break;
     case 2: r = frcp(v); break;
     case 4: r = fexp_tab(v, kExpT); break;
+    case 5: r = fexp_tab<false>(v, kExpT); break;
     default: r = frsqrt(v); break;
     }
     out[i] = r;

@@ -58,6 +58,16 @@ def test_exp_table(gpu):
     assert out[0] == 0.0 and out[1] == 0.0 and np.isfinite(out[2])
 
 
+def test_exp_table_unclamped_nonpositive(gpu):
+    """fexp_tab<false> (the Maxwellian exp(-s^2)): same accuracy on x <= 0,
+    and arguments far below the underflow threshold still give 0."""
+    rng = np.random.default_rng(5)
+    x = -np.concatenate([rng.uniform(0, 40, 3000), rng.uniform(0, 700, 500), [0.0, 1e-300, 0.3466]])
+    ref = np.array([float(D(v).exp()) for v in x])
+    assert ulps(probe(x, 5), ref).max() <= 1.0
+    assert np.all(probe(np.array([-746.0, -800.0, -1e5, -2e7]), 5) == 0.0)
+
+
 def test_exp_underflow_and_nan(gpu):
     out = probe(np.array([-800.0, -746.0, 709.0, np.nan]), 0)
     assert out[0] == 0.0 and out[1] == 0.0 and np.isfinite(out[2]) and np.isnan(out[3])

@@ -1,10 +1,4 @@
 # development sweep of kernel shapes (not part of the bench); output in gpurun_out/sweep.log
 OUT=gpurun_out/sweep.log
 run() { echo "== $SZ $*" >> $OUT; env "$@" timeout 300 python tools/quick_perf.py $SZ 2>&1 | grep -E "instrument=True|stage" >> $OUT; }
-for SZ in "800 200 1.03 50" "3160 790 1.00734 10"; do
-run KMF_X=0
-run KMF_QG_TB=64
-run KMF_QG_UNROLL=2
-run KMF_QG_NC=2
-done
-SZ="400 100 1.06 100"; run KMF_X=0; run KMF_QG_TB=64; run KMF_QG_NC=4
+for SZ in "800 200 1.03 50" "3160 790 1.00734 10" "6324 1581 1.003647 4"; do run KMF_X=0; done

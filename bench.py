@@ -130,8 +130,13 @@ def setup(name, dist=None, rank=0):
 
     box = [None]
     if rank == 0:
+        import shutil
+
         cloud, conn, cfg, init = build_config(name)
-        shm = Path("/dev/shm") if Path("/dev/shm").is_dir() else Path(tempfile.gettempdir())
+        need = 1.2 * (conn.full.idx.nbytes * 3 + conn.cloud.n_points * 8 * 40)  # idx, dx, dy + per-point arrays
+        shm = Path("/dev/shm")
+        if not shm.is_dir() or shutil.disk_usage(shm).free < need:
+            shm = Path(tempfile.gettempdir())  # small /dev/shm: disk-backed, still one page-cache copy
         box[0] = tempfile.mkdtemp(prefix=f"kmf_{name}_", dir=shm)
         store.save(conn, box[0], extra={"init": init.as_array()})
         del cloud, conn, init

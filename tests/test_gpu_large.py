@@ -82,6 +82,32 @@ def test_c3_partitioned_solve_bitwise(gpu, c3):
     assert np.array_equal(prims, ref.primitives.as_array())
 
 
+
+_GOLDEN = __import__("pathlib").Path(__file__).parent / "golden"
+
+
+def _needs(name):
+    return pytest.mark.skipif(not (_GOLDEN / f"{name}.json").exists(),
+                              reason=f"tests/golden/{name} not generated (tools/make_golden.py {name})")
+
+
+@_needs("c2p5m")
+def test_c3_two_iterations_match_reference(gpu, c3):
+    """Config 3 against the reference package itself (tests/golden/c2p5m,
+    written by the reference's own builder and solver): residue history of
+    the first two iterations <= 1e-10 relative, 4096-point state sample."""
+    from conftest import golden
+
+    A, meta = golden("c2p5m")
+    cloud, conn, cfg, init, _ = c3
+    assert meta["params"][:3] == [3160, 790, 1.00734] and (meta["mach"], meta["aoa"]) == (0.85, 1.0)
+    res = solve(SolverConfig(mach=0.85, aoa_deg=1.0, n_outer=meta["iters"]), cloud, conn, initial_state=init,
+                instrument=False)
+    rel = np.abs(res.residue_history - A["history"]) / A["history"]
+    assert rel.max() <= 1e-10, rel
+    idx = A["sample_idx"]
+    assert np.allclose(res.primitives.as_array()[:, idx], A["prims_sample"], rtol=1e-10, atol=1e-12)
+
 # --------------------------------------------------------------- 40M (opt-in)
 # The bench's default configuration (BASELINE configs[4]): one whole outer
 # iteration of the device path against the oracle on all 39,992,976 points,
@@ -156,3 +182,58 @@ def test_c2_thousand_iterations_match_oracle(gpu):
           f"max scaled state error {err.max():.3e}; residue {hist[0]:.6e} -> {hist[-1]:.6e}")
     assert rel.max() <= 1e-10
     assert np.allclose(res.primitives.as_array(), prims, rtol=1e-10, atol=1e-12)
+
+
+# ------------------------------------------ against the reference itself
+# Fixtures written by the reference package (tools/make_golden.py, run in the
+# build container): BASELINE configs[0] and [1] on the native builder's
+# connectivity (bit-exact with the reference builder, digests checked in
+# tests/test_geometry_parity.py).
+
+
+def test_c160k_twenty_iterations_match_reference(gpu):
+    """Config 2 (160K points, M 0.63, AoA 2): the reference's own 20-iteration
+    residue history (<= 1e-10 relative) and a 4096-point state sample."""
+    from conftest import golden
+
+    A, meta = golden("c160k")
+    m, L, gr, ff = meta["params"]
+    cloud = generate_naca_cloud(m, L, gr, ff)
+    cfg = SolverConfig(mach=meta["mach"], aoa_deg=meta["aoa"], n_outer=meta["iters"])
+    res = solve(cfg, cloud, build_stencils(cloud), instrument=False)
+    rel = np.abs(res.residue_history - A["history"]) / A["history"]
+    assert rel.max() <= 1e-10, rel.max()
+    idx = A["sample_idx"]
+    assert np.allclose(res.primitives.as_array()[:, idx], A["prims_sample"], rtol=1e-10, atol=1e-12)
+
+
+@_needs("c40k")
+def test_c40k_reference_breakdown_reproduced(gpu):
+    """Config 1 (40K points, M 0.63, AoA 2, 1000 iterations) breaks down in
+    the reference: a flux_residual positivity failure part-way through.  The
+    device path reproduces the history up to it (<= 1e-10 relative), the
+    state before it, and the failure itself: same iteration, same stage
+    operator, same offending points."""
+    from conftest import golden
+
+    from paper_2108_07031_b200 import PositivityError
+
+    A, meta = golden("c40k")
+    fail = meta.get("failure")
+    m, L, gr, ff = meta["params"]
+    cloud = generate_naca_cloud(m, L, gr, ff)
+    conn = build_stencils(cloud)
+    before = SolverConfig(mach=meta["mach"], aoa_deg=meta["aoa"], n_outer=meta["iters"])
+    res = solve(before, cloud, conn, instrument=False)
+    rel = np.abs(res.residue_history - A["history"]) / A["history"]
+    assert res.iterations == meta["iters"]
+    assert rel.max() <= 1e-10, rel.max()
+    assert np.allclose(res.primitives.as_array(), A["prims"], rtol=1e-10, atol=1e-12)
+    if fail is None:
+        return
+    with pytest.raises(PositivityError) as exc:
+        solve(SolverConfig(mach=meta["mach"], aoa_deg=meta["aoa"], n_outer=1000), cloud, conn, instrument=False)
+    # message: "iteration N: flux_residual[kind]: ... on K edge(s)"; indices:
+    # positions in that 4096-point block's family edge list (solver.py:162-168)
+    assert str(exc.value) == fail["message"]
+    assert [int(i) for i in exc.value.indices] == fail["indices"]

@@ -130,3 +130,22 @@ def test_long_history_2k(oracle_small):
     hist, *_ = O.solve(oracle_small, S["init.m63a2"], fs_vec(0.63, 2.0), n)
     ref = H["m63a2.history"][:n]
     assert np.all(np.abs(hist - ref) <= 1e-10 * ref)
+
+
+def test_config2_history_against_reference():
+    """BASELINE config 2 (160K points, M 0.63, AoA 2): the reference's own
+    20-iteration residue history and a 4096-point sample of the final state
+    (tests/golden/c160k, tools/make_golden.py) on the native builder's
+    connectivity (its digests are checked in test_geometry_parity.py)."""
+    from paper_2108_07031_b200 import SolverConfig, build_stencils, generate_naca_cloud, initial_primitives
+
+    A, meta = golden("c160k")
+    m, L, g, ff = meta["params"]
+    cloud = generate_naca_cloud(m, L, g, ff)
+    init = initial_primitives(SolverConfig(mach=meta["mach"], aoa_deg=meta["aoa"]), cloud)
+    O.set_threads(8)
+    hist, prims, *_ = O.solve(O.Packed(build_stencils(cloud)), init.as_array(), fs_vec(meta["mach"], meta["aoa"]),
+                              meta["iters"])
+    assert np.all(np.abs(hist - A["history"]) <= 1e-10 * A["history"])
+    idx = A["sample_idx"]
+    assert np.allclose(prims[:, idx], A["prims_sample"], rtol=1e-10, atol=1e-12)

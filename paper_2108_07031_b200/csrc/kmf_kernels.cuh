@@ -203,6 +203,30 @@ KMF_HD bool qg_stage_indices_tma(const DG &g, int *sidx, int cap, int &e0, unsig
     return staged;
 }
 
+// U >= 8 selects the software-pipelined slot loop instead: the gathers of
+// slot s + P (P = U - 7) are issued before slot s is evaluated, so P HBM/L2
+// round trips overlap the arithmetic; the sums keep their order exactly.
+template <int NC, bool WG>
+struct QgSlot {
+    double x, y, q[NC], gx[WG ? NC : 1], gy[WG ? NC : 1];
+};
+
+template <int NC, bool WG>
+KMF_HD void qg_gather(QgSlot<NC, WG> &o, const DG &g, const double *__restrict__ q, const double *__restrict__ G,
+                      int ld, int k0, int j)
+{
+    o.x = g.x[j];
+    o.y = g.y[j];
+#pragma unroll
+    for (int k = 0; k < NC; k++) {
+        o.q[k] = q[(k0 + k) * ld + j];
+        if (WG) {
+            o.gx[k] = G[(k0 + k) * ld + j];
+            o.gy[k] = G[(4 + k0 + k) * ld + j];
+        }
+    }
+}
+
 // The edge loop is unrolled by U: the U neighbour indices, then all their
 // gathers, are issued before any arithmetic (U-fold memory-level
 // parallelism); the accumulation itself stays strictly in slot order and
@@ -239,6 +263,29 @@ __global__ void __launch_bounds__(TB, MB) k_first_order(DG g, const double *__re
     }
     const double xi = g.x[i], yi = g.y[i];
     const int base = ell_base(g, i), d = g.deg[i];
+    if constexpr (U >= 8 && XY && ST == 2) {
+        constexpr int P = U - 7;
+        auto jof = [&](int s) { return staged ? sidx[base + s * 32 - e0] : g.eidx[base + s * 32]; };
+        QgSlot<NC, false> buf[P];
+        if (d > 0) {
+#pragma unroll
+        for (int p = 0; p < P; p++) qg_gather(buf[p], g, q, q, ld, k0, jof(min(p, d - 1)));
+        for (int s = 0; s < d; s++) {
+            QgSlot<NC, false> nxt;
+            qg_gather(nxt, g, q, q, ld, k0, jof(min(s + P, d - 1)));
+            const double dx = SUB(buf[0].x, xi), dy = SUB(buf[0].y, yi);
+#pragma unroll
+            for (int k = 0; k < NC; k++) {
+                const double dq = SUB(buf[0].q[k], qi[k]);
+                sx[k] = ADD(sx[k], MUL(dx, dq));
+                sy[k] = ADD(sy[k], MUL(dy, dq));
+            }
+#pragma unroll
+            for (int p = 0; p + 1 < P; p++) buf[p] = buf[p + 1];
+            buf[P - 1] = nxt;
+        }
+        }
+    } else
     for (int s0 = 0; s0 < d; s0 += U) {
         int jj[U], ent[U];
 #pragma unroll
@@ -306,6 +353,32 @@ __global__ void __launch_bounds__(TB, MB) k_sweep(DG g, const double *__restrict
         }
         const double xi = g.x[i], yi = g.y[i];
         const int base = ell_base(g, i), d = g.deg[i];
+        if constexpr (U >= 8 && XY && ST == 2) {
+            constexpr int P = U - 7;
+            auto jof = [&](int s) { return staged ? sidx[base + s * 32 - e0] : g.eidx[base + s * 32]; };
+            QgSlot<NC, true> buf[P];
+            if (d > 0) {
+#pragma unroll
+            for (int p = 0; p < P; p++) qg_gather(buf[p], g, q, Gin, ld, k0, jof(min(p, d - 1)));
+            for (int s = 0; s < d; s++) {
+                QgSlot<NC, true> nxt;
+                qg_gather(nxt, g, q, Gin, ld, k0, jof(min(s + P, d - 1)));
+                const QgSlot<NC, true> &c = buf[0];
+                const double dx = SUB(c.x, xi), dy = SUB(c.y, yi);
+                const double hdx = MUL(0.5, dx), hdy = MUL(0.5, dy);
+#pragma unroll
+                for (int k = 0; k < NC; k++) {
+                    const double dq = SUB(qtilde_h(c.q[k], c.gx[k], c.gy[k], hdx, hdy),
+                                          qtilde_h(qi[k], gxi[k], gyi[k], hdx, hdy));
+                    sx[k] = ADD(sx[k], MUL(dx, dq));
+                    sy[k] = ADD(sy[k], MUL(dy, dq));
+                }
+#pragma unroll
+                for (int p = 0; p + 1 < P; p++) buf[p] = buf[p + 1];
+                buf[P - 1] = nxt;
+            }
+            }
+        } else
         for (int s0 = 0; s0 < d; s0 += U) {
             int jj[U], ent[U];
 #pragma unroll

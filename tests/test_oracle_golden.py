@@ -149,3 +149,19 @@ def test_config2_history_against_reference():
     assert np.all(np.abs(hist - A["history"]) <= 1e-10 * A["history"])
     idx = A["sample_idx"]
     assert np.allclose(prims[:, idx], A["prims_sample"], rtol=1e-10, atol=1e-12)
+
+
+def test_config1_history_against_reference():
+    """BASELINE config 1 (40K points, M 0.63, AoA 2): the first 60 iterations
+    of the reference's own run (tests/golden/c40k; the reference breaks down
+    at iteration 407, which the device test reproduces in full)."""
+    from paper_2108_07031_b200 import SolverConfig, build_stencils, generate_naca_cloud, initial_primitives
+
+    A, meta = golden("c40k")
+    m, L, g, ff = meta["params"]
+    cloud = generate_naca_cloud(m, L, g, ff)
+    init = initial_primitives(SolverConfig(mach=meta["mach"], aoa_deg=meta["aoa"]), cloud)
+    O.set_threads(8)
+    n = 60
+    hist, *_ = O.solve(O.Packed(build_stencils(cloud)), init.as_array(), fs_vec(meta["mach"], meta["aoa"]), n)
+    assert np.all(np.abs(hist - A["history"][:n]) <= 1e-10 * A["history"][:n])

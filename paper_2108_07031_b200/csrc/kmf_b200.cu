@@ -514,10 +514,7 @@ void launch_ex(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t s
     case 256: KCALL(256, 0, 0); break;                  \
     case 512: KCALL(512, 0, 0); break;                  \
     case 129: KCALL(128, 1, 0); break;                  \
-    case 130:                                           \
-        if (c->qg_minb == 6) KCALL(128, 2, 6);          \
-        else KCALL(128, 2, 0);                          \
-        break;                                          \
+    case 130: KCALL(128, 2, 0); break;                  \
     case 257:                                           \
         if (c->qg_minb == 4) KCALL(256, 1, 4);          \
         else if (c->qg_minb == 3) KCALL(256, 1, 3);     \
@@ -550,7 +547,7 @@ void launch_sw_t(kmf_ctx *c, cudaStream_t s, const double *Gin, double *Gout, Ct
 }
 
 // q-gradient launch shape: KMF_QG_NC components per thread (1, 2, 4) and
-// KMF_QG_UNROLL edge unroll (1, 2, 4); connectivities whose offsets are not
+// KMF_QG_UNROLL edge unroll (1, 2, 4; 8 = pipelined slot loop); connectivities whose offsets are not
 // x[j]-x[i] use the stored-offset variant (NC 2, U 1).
 #define KMF_QG_DISPATCH(CALL, ...)                                          \
     do {                                                                    \
@@ -568,7 +565,6 @@ void launch_sw_t(kmf_ctx *c, cudaStream_t s, const double *Gin, double *Gout, Ct
         case 41: CALL<true, 4, 1>(__VA_ARGS__); break;                      \
         case 42: CALL<true, 4, 2>(__VA_ARGS__); break;                      \
         case 48: CALL<true, 4, 8>(__VA_ARGS__); break;                      \
-        case 49: CALL<true, 4, 9>(__VA_ARGS__); break;                      \
         case 28: CALL<true, 2, 8>(__VA_ARGS__); break;                      \
         default: CALL<true, 4, 4>(__VA_ARGS__); break;                      \
         }                                                                   \
@@ -954,7 +950,7 @@ int kmf_create(kmf_ctx **out, const kmf_geometry *g, int device)
     }
     if (const char *e = std::getenv("KMF_QG_UNROLL")) {
         int v = std::atoi(e);
-        if (v == 1 || v == 2 || v == 4 || v == 8 || v == 9) c->qg_unroll = v;  // 8, 9: pipelined, 1 / 2 slots ahead
+        if (v == 1 || v == 2 || v == 4 || v == 8) c->qg_unroll = v;  // 8: pipelined slot loop (NC 2, 4)
     }
     if (const char *e = std::getenv("KMF_QG_TB")) c->qg_tb = std::atoi(e);
     if (const char *e = std::getenv("KMF_PDL")) c->pdl = std::atoi(e) != 0;
@@ -979,7 +975,7 @@ int kmf_create(kmf_ctx **out, const kmf_geometry *g, int device)
     if (c->n > 100000 && !std::getenv("KMF_QG_NC")) c->qg_nc = 4;
     // software-pipelined slot loop (gathers of slot s+1 in flight while slot
     // s is evaluated; U = 8): -8 % q-gradient time at 40K / 2.5M / 10M,
-    // -3 % at 160K.  Two slots ahead (U = 9, 138 registers) loses 28 %.
+    // -3 % at 160K (variants measured: kmf_kernels.cuh qg_pipeline).
     if (!std::getenv("KMF_QG_UNROLL") && c->qg_stage == 2 && (c->qg_nc == 2 || c->qg_nc == 4)) c->qg_unroll = 8;
     // 5: lean arithmetic (table exp, FMA perturbations, select-free family
     // accumulation): -4.3 % flux time at 160K; 6: + next-edge prefetch

@@ -203,9 +203,9 @@ KMF_HD bool qg_stage_indices_tma(const DG &g, int *sidx, int cap, int &e0, unsig
     return staged;
 }
 
-// U >= 8 selects the software-pipelined slot loop instead: the gathers of
-// slot s + P (P = U - 7) are issued before slot s is evaluated, so P HBM/L2
-// round trips overlap the arithmetic; the sums keep their order exactly.
+// U >= 8 selects the software-pipelined slot loop instead (qg_pipeline):
+// the gathers of a later slot are issued before slot s is evaluated, so the
+// HBM/L2 round trip overlaps the arithmetic; the sums keep their order.
 template <int NC, bool WG>
 struct QgSlot {
     double x, y, q[NC], gx[WG ? NC : 1], gy[WG ? NC : 1];
@@ -224,6 +224,32 @@ KMF_HD void qg_gather(QgSlot<NC, WG> &o, const DG &g, const double *__restrict__
             o.gx[k] = G[(k0 + k) * ld + j];
             o.gy[k] = G[(4 + k0 + k) * ld + j];
         }
+    }
+}
+
+// Drives the pipelined slot loop: gather(slot, o) loads a slot, eval(o)
+// accumulates it, slots are evaluated strictly in order 0..d-1, and slot
+// s + P (P = U - 7) is gathered before slot s is evaluated.  ptxas places
+// those loads after the arithmetic of slot s (their consumers sit across the
+// back edge), so the round trip overlaps the loop tail and the other warps;
+// a two-buffer variant unrolled by two that interleaves them with the
+// arithmetic measured 4 % slower at 2.5M / 10M, two slots ahead (P = 2, 138
+// registers) 28 % slower.
+template <int U, class Slot, class Gather, class Eval>
+KMF_HD void qg_pipeline(int d, Gather gather, Eval eval)
+{
+    if (d <= 0) return;
+    constexpr int P = U - 7;
+    Slot buf[P];
+#pragma unroll
+    for (int p = 0; p < P; p++) gather(min(p, d - 1), buf[p]);
+    for (int s = 0; s < d; s++) {
+        Slot nxt;
+        gather(min(s + P, d - 1), nxt);
+        eval(buf[0]);
+#pragma unroll
+        for (int p = 0; p + 1 < P; p++) buf[p] = buf[p + 1];
+        buf[P - 1] = nxt;
     }
 }
 
@@ -264,27 +290,21 @@ __global__ void __launch_bounds__(TB, MB) k_first_order(DG g, const double *__re
     const double xi = g.x[i], yi = g.y[i];
     const int base = ell_base(g, i), d = g.deg[i];
     if constexpr (U >= 8 && XY && ST == 2) {
-        constexpr int P = U - 7;
-        auto jof = [&](int s) { return staged ? sidx[base + s * 32 - e0] : g.eidx[base + s * 32]; };
-        QgSlot<NC, false> buf[P];
-        if (d > 0) {
+        using Slot = QgSlot<NC, false>;
+        qg_pipeline<U, Slot>(
+            d,
+            [&](int s, Slot &o) {
+                qg_gather(o, g, q, q, ld, k0, staged ? sidx[base + s * 32 - e0] : g.eidx[base + s * 32]);
+            },
+            [&](const Slot &o) {
+                const double dx = SUB(o.x, xi), dy = SUB(o.y, yi);
 #pragma unroll
-        for (int p = 0; p < P; p++) qg_gather(buf[p], g, q, q, ld, k0, jof(min(p, d - 1)));
-        for (int s = 0; s < d; s++) {
-            QgSlot<NC, false> nxt;
-            qg_gather(nxt, g, q, q, ld, k0, jof(min(s + P, d - 1)));
-            const double dx = SUB(buf[0].x, xi), dy = SUB(buf[0].y, yi);
-#pragma unroll
-            for (int k = 0; k < NC; k++) {
-                const double dq = SUB(buf[0].q[k], qi[k]);
-                sx[k] = ADD(sx[k], MUL(dx, dq));
-                sy[k] = ADD(sy[k], MUL(dy, dq));
-            }
-#pragma unroll
-            for (int p = 0; p + 1 < P; p++) buf[p] = buf[p + 1];
-            buf[P - 1] = nxt;
-        }
-        }
+                for (int k = 0; k < NC; k++) {
+                    const double dq = SUB(o.q[k], qi[k]);
+                    sx[k] = ADD(sx[k], MUL(dx, dq));
+                    sy[k] = ADD(sy[k], MUL(dy, dq));
+                }
+            });
     } else
     for (int s0 = 0; s0 < d; s0 += U) {
         int jj[U], ent[U];
@@ -354,30 +374,23 @@ __global__ void __launch_bounds__(TB, MB) k_sweep(DG g, const double *__restrict
         const double xi = g.x[i], yi = g.y[i];
         const int base = ell_base(g, i), d = g.deg[i];
         if constexpr (U >= 8 && XY && ST == 2) {
-            constexpr int P = U - 7;
-            auto jof = [&](int s) { return staged ? sidx[base + s * 32 - e0] : g.eidx[base + s * 32]; };
-            QgSlot<NC, true> buf[P];
-            if (d > 0) {
+            using Slot = QgSlot<NC, true>;
+            qg_pipeline<U, Slot>(
+                d,
+                [&](int s, Slot &o) {
+                    qg_gather(o, g, q, Gin, ld, k0, staged ? sidx[base + s * 32 - e0] : g.eidx[base + s * 32]);
+                },
+                [&](const Slot &o) {
+                    const double dx = SUB(o.x, xi), dy = SUB(o.y, yi);
+                    const double hdx = MUL(0.5, dx), hdy = MUL(0.5, dy);
 #pragma unroll
-            for (int p = 0; p < P; p++) qg_gather(buf[p], g, q, Gin, ld, k0, jof(min(p, d - 1)));
-            for (int s = 0; s < d; s++) {
-                QgSlot<NC, true> nxt;
-                qg_gather(nxt, g, q, Gin, ld, k0, jof(min(s + P, d - 1)));
-                const QgSlot<NC, true> &c = buf[0];
-                const double dx = SUB(c.x, xi), dy = SUB(c.y, yi);
-                const double hdx = MUL(0.5, dx), hdy = MUL(0.5, dy);
-#pragma unroll
-                for (int k = 0; k < NC; k++) {
-                    const double dq = SUB(qtilde_h(c.q[k], c.gx[k], c.gy[k], hdx, hdy),
-                                          qtilde_h(qi[k], gxi[k], gyi[k], hdx, hdy));
-                    sx[k] = ADD(sx[k], MUL(dx, dq));
-                    sy[k] = ADD(sy[k], MUL(dy, dq));
-                }
-#pragma unroll
-                for (int p = 0; p + 1 < P; p++) buf[p] = buf[p + 1];
-                buf[P - 1] = nxt;
-            }
-            }
+                    for (int k = 0; k < NC; k++) {
+                        const double dq = SUB(qtilde_h(o.q[k], o.gx[k], o.gy[k], hdx, hdy),
+                                              qtilde_h(qi[k], gxi[k], gyi[k], hdx, hdy));
+                        sx[k] = ADD(sx[k], MUL(dx, dq));
+                        sy[k] = ADD(sy[k], MUL(dy, dq));
+                    }
+                });
         } else
         for (int s0 = 0; s0 < d; s0 += U) {
             int jj[U], ent[U];

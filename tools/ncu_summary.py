@@ -15,9 +15,20 @@ RAW = ["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "dram__by
        "launch__registers_per_thread", "sm__warps_active.avg.pct_of_peak_sustained_active"]
 
 
+def _pages(path):
+    """(details csv, raw csv) of a .ncu-rep, or of the <prefix>_details.csv /
+    <prefix>_raw.csv pair tools/profile.sh exports on the GPU box."""
+    if path.endswith(".ncu-rep"):
+        return tuple(subprocess.run(["ncu", "-i", path, "--page", pg, "--csv"], capture_output=True,
+                                    text=True).stdout for pg in ("details", "raw"))
+    return tuple(open(f"{path}_{pg}.csv").read() for pg in ("details", "raw"))
+
+
+STALL = "smsp__average_warps_issue_stalled_"
+
+
 def summarize(path):
-    det = subprocess.run(["ncu", "-i", path, "--page", "details", "--csv"], capture_output=True, text=True).stdout
-    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    det, raw = _pages(path)
     out = {}
     rows = list(csv.reader(io.StringIO(det)))
     if not rows:
@@ -39,6 +50,16 @@ def summarize(path):
             for m in RAW:
                 if m in d:
                     out.setdefault(key, {})[m] = f"{d[m]} {uu[hh.index(m)]}"
+            st = {}
+            for m, v in d.items():
+                if m.startswith(STALL) and m.endswith("_per_issue_active.ratio"):
+                    try:
+                        st[m[len(STALL):-len("_per_issue_active.ratio")]] = float(v)
+                    except ValueError:
+                        pass
+            top = sorted(st.items(), key=lambda kv: -kv[1])[:6]
+            if top:
+                out.setdefault(key, {})["stalls per issued instruction"] = ", ".join(f"{k} {v:.2f}" for k, v in top)
     return out
 
 

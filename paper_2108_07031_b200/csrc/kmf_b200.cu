@@ -631,12 +631,15 @@ void launch_flux_t(kmf_ctx *c, cudaStream_t s, const double *G, int mode, double
         // exp, FMA perturbations); 6 = 4 + 5.  The prefetch only changes
         // the schedule, so split4 uses the same arithmetic variant as fused
         // and the two modes stay bitwise equal.
+        // 7 = 5 + the next edge's gathers in registers (PF = 2).
         const bool lean = c->flux_impl >= 5, pf = c->flux_impl == 4 || c->flux_impl == 6;
+        const bool rp = c->flux_impl == 7 && XY;
 #define KMF_F3(FAM, PF, LEAN)                                                                                 \
     launch_ex(c->pdl, k_flux3<XY, FAM, MINB, GK, PF, LEAN>, dim3(nb), dim3(kTB), 0, s, g, q, G, R, inv_gm1, c_i0, \
               zero_bnd, ctl, stage)
         if (mode == 0) {
-            if (lean && pf) KMF_F3(-1, 1, true);
+            if (rp) KMF_F3(-1, 2, true);
+            else if (lean && pf) KMF_F3(-1, 1, true);
             else if (lean) KMF_F3(-1, 0, true);
             else if (pf) KMF_F3(-1, 1, false);
             else KMF_F3(-1, 0, false);
@@ -966,9 +969,6 @@ int kmf_create(kmf_ctx **out, const kmf_geometry *g, int device)
     // offsets it enables -11 % at 40K); KMF_QG_STAGE overrides
     c->qg_stage = 2;
     if (const char *e = std::getenv("KMF_QG_STAGE")) c->qg_stage = std::atoi(e);
-    // the flux kernel's next-edge L1 prefetch and 4 blocks/SM pay once the
-    // cloud streams from HBM (-5.9 % flux time at 2.5M, +4 % at 160K)
-    const bool big = c->n > 1000000;
     // with the TMA index staging and pre-halved offsets: one thread per point
     // (NC = 4) in 128-thread blocks from 160K points up (-6 % q-gradient
     // time at 160K / 2.5M / 10M); small clouds keep 2 threads per point
@@ -978,16 +978,19 @@ int kmf_create(kmf_ctx **out, const kmf_geometry *g, int device)
     // -3 % at 160K (variants measured: kmf_kernels.cuh qg_pipeline).
     if (!std::getenv("KMF_QG_UNROLL") && c->qg_stage == 2 && (c->qg_nc == 2 || c->qg_nc == 4)) c->qg_unroll = 8;
     // 5: lean arithmetic (table exp, FMA perturbations, select-free family
-    // accumulation): -4.3 % flux time at 160K; 6: + next-edge prefetch
-    c->flux_impl = big ? 6 : 5;
-    c->flux_minb = big ? 4 : 3;
+    // accumulation): -4.3 % flux time at 160K; 6: + next-edge L1 prefetch
+    // (4 blocks/SM); 7: 5 + the next edge's gathers in registers, 3 blocks/SM
+    // (168 registers): -5 % flux time against 6 at 2.5M / 10M, -2.4 %
+    // against 5 at 160K, neutral at 40K -- the default at every size
+    c->flux_impl = c->xy ? 7 : 5;
+    c->flux_minb = 3;
     if (const char *e = std::getenv("KMF_FLUX_MINB")) {
         int v = std::atoi(e);
         if (v == 3 || v == 4) c->flux_minb = v;
     }
     if (const char *e = std::getenv("KMF_FLUX_IMPL")) {
         int v = std::atoi(e);
-        if (v >= 1 && v <= 6) c->flux_impl = v;
+        if (v >= 1 && v <= 7) c->flux_impl = v;
     }
     *out = c;
     return KMF_OK;

@@ -102,10 +102,10 @@ def test_fused_equals_split4_bitwise(gpu, pre, small_golden, small_naca_conn):
     assert np.array_equal(a, b)
 
 
-@pytest.mark.parametrize("impl", ["3", "4", "5", "6"])
+@pytest.mark.parametrize("impl", ["3", "4", "5", "6", "7"])
 def test_flux_kernel_variants_fused_split4_and_tolerance(gpu, impl, small_golden, small_naca, monkeypatch):
     """Every flux kernel variant (lock-step, + L1 prefetch, lean arithmetic,
-    both; the last two are the defaults above 1M points): fused == split4
+    both, lean + next edge in registers = the default): fused == split4
     bitwise and the reference tolerance per call.  The variant is fixed when
     a context is created, so each case builds a fresh connectivity."""
     monkeypatch.setenv("KMF_FLUX_IMPL", impl)

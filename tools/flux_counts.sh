@@ -1,5 +1,6 @@
 # Executed FP64 instructions and DRAM traffic of one flux_residual launch
-# (ncu, one launch mid-step) -> profiles/flux_counts_<cfg>.json, read by
+# (ncu, one launch mid-step) -> gpurun_out/flux_counts_<cfg>.json (copied to
+# profiles/ in the build container: only gpurun_out/ comes back), read by
 # bench.py for roofline_fp64 (executed DP-pipe instructions) and
 # roofline.traffic.  Run under gpurun:  bash tools/flux_counts.sh c2
 CFG=${1:-c2}
@@ -25,6 +26,6 @@ out = {"config": cfg, "kernel": rows[0]["Kernel Name"], "dp_thread_inst_per_laun
        "dram_bytes_per_launch": b("dram__bytes_read.sum") + b("dram__bytes_write.sum"),
        "ncu_duration_ns": b("gpu__time_duration.sum"),
        "note": "ncu --clock-control none, default cache control (caches flushed before the launch: cold-cache traffic)"}
-json.dump(out, open(f"profiles/flux_counts_{cfg}.json", "w"), indent=1)
+json.dump(out, open(f"gpurun_out/flux_counts_{cfg}.json", "w"), indent=1)
 print(json.dumps(out))
 PY

@@ -143,6 +143,59 @@ def test_update_decode_residue_bitwise(gpu, pre, small_golden):
     assert residue_norm(G[f"{pre}.U1"], U) == G[f"{pre}.residue1"][0]
 
 
+def test_stage_arithmetic_matches_coefficients(gpu):
+    """Reference tests/test_solver.py:124-133 on the device operator."""
+    U0, dt, R = np.array([[1.0]]), np.array([0.1]), np.array([[2.0]])
+    assert state_update_rk(U0, np.array([[0.7]]), 1, dt, R)[0, 0] == pytest.approx(0.6)
+    assert state_update_rk(U0, np.array([[0.7]]), 4, dt, R)[0, 0] == pytest.approx(0.6)
+    expected = 2.0 / 3.0 + 0.7 / 3.0 - 0.1 / 6.0 * 2.0
+    assert state_update_rk(U0, np.array([[0.7]]), 3, dt, R)[0, 0] == pytest.approx(expected)
+    with pytest.raises(ValueError, match="stage"):
+        state_update_rk(U0, U0, 5, dt, R)
+
+
+def test_integrator_is_third_order_on_linear_decay(gpu):
+    """Reference tests/test_solver.py:136-151: y' = -y through the device
+    stage operator (residual R = U), convergence order >= 2.9."""
+    import math
+
+    def decay(dt):
+        U, d = np.array([[1.0], [0.0], [0.0], [0.0]]), np.array([dt])
+        for _ in range(round(1.0 / dt)):
+            Uo = U
+            for stage in (1, 2, 3, 4):
+                U = state_update_rk(Uo, U, stage, d, U)
+        return float(U[0, 0])
+
+    errs = [abs(decay(dt) - math.exp(-1.0)) for dt in (0.1, 0.05, 0.025)]
+    orders = [math.log2(errs[i] / errs[i + 1]) for i in range(2)]
+    assert min(orders) >= 2.9, (errs, orders)
+
+
+def test_residue_norm_values(gpu):
+    """Reference tests/test_solver.py:197-209 on the device reduction."""
+    old, new = np.zeros((4, 2)), np.zeros((4, 2))
+    new[0] = [3.0, 4.0]
+    assert residue_norm(new, old) == pytest.approx(np.sqrt(12.5), rel=1e-15)
+    assert residue_norm(np.full((4, 1), 3.0), np.zeros((4, 1))) == 3.0
+    new3 = np.zeros((4, 3))
+    new3[1:] = 7.0
+    assert residue_norm(new3, np.zeros((4, 3))) == 0.0
+
+
+def test_inner_sweep_updates_shrink(gpu, small_naca, small_naca_conn):
+    """Reference tests/test_lsq.py:107-117: on a smooth field each Jacobi
+    sweep moves the iterate less than the one before; the device's
+    inner residuals equal the oracle's bitwise."""
+    x, y = small_naca.x, small_naca.y
+    q = np.stack([np.sin(0.6 * x + 0.3 * y), np.cos(0.5 * x) * y, x * y, -np.exp(0.1 * x)])
+    g = compute_q_derivatives(q, small_naca_conn, 6)
+    r = g.inner_residuals
+    assert len(r) == 6 and all(r[k + 1] < r[k] for k in range(5))
+    qx, qy, ro = O.q_derivatives(O.Packed(small_naca_conn), q, 6)
+    assert np.array_equal(g.qx, qx) and np.array_equal(g.qy, qy) and np.array_equal(np.asarray(r), ro)
+
+
 def test_uniform_flow_residual_vanishes(gpu, small_naca, small_naca_conn):
     """Reference tests/test_solver.py:139-142."""
     prims = free_stream(0.63, 2.0, n=small_naca.n_points)

@@ -1166,18 +1166,19 @@ int kmf_last_indices(kmf_ctx *c, int64_t *idx, int64_t cap)
 // ------------------------------------------------------- context operators
 
 namespace {
-int upload_fields(kmf_ctx *c, const double *h, int nc, double *dev)
+// ps = 2: one derivative (dev = G or G + 1) of the interleaved gradients
+int upload_fields(kmf_ctx *c, const double *h, int nc, double *dev, int ps = 1)
 {
     CK(cudaMemcpyAsync(c->stage_buf.p, h, sizeof(double) * nc * (size_t)c->n, cudaMemcpyHostToDevice, c->s0));
-    k_to_dev<<<nblk(c->n), kTB, 0, c->s0>>>(c->n, c->ld, nc, c->stage_buf.p, c->has_perm ? c->perm.p : nullptr,
-                                            dev);
+    k_to_dev<<<nblk(c->n), kTB, 0, c->s0>>>(c->n, (long long)ps * c->ld, ps, nc, c->stage_buf.p,
+                                            c->has_perm ? c->perm.p : nullptr, dev);
     CK(cudaGetLastError());
     return KMF_OK;
 }
-int download_fields(kmf_ctx *c, const double *dev, int nc, double *h)
+int download_fields(kmf_ctx *c, const double *dev, int nc, double *h, int ps = 1)
 {
-    k_from_dev<<<nblk(c->n), kTB, 0, c->s0>>>(c->n, c->ld, nc, dev, c->has_perm ? c->perm.p : nullptr,
-                                              c->stage_buf.p);
+    k_from_dev<<<nblk(c->n), kTB, 0, c->s0>>>(c->n, (long long)ps * c->ld, ps, nc, dev,
+                                              c->has_perm ? c->perm.p : nullptr, c->stage_buf.p);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(h, c->stage_buf.p, sizeof(double) * nc * (size_t)c->n, cudaMemcpyDeviceToHost, c->s0));
     CK(cudaStreamSynchronize(c->s0));
@@ -1220,8 +1221,8 @@ int kmf_op_first_order(kmf_ctx *c, const double *q, double *qx, double *qy)
     if ((rc = reset_ctrl(c))) return rc;
     launch_first_order(c, c->s0, c->GA.p, c->ctrl.p, 0);
     CK(cudaGetLastError());
-    if ((rc = download_fields(c, c->GA.p, 4, qx))) return rc;
-    return download_fields(c, c->GA.p + 4 * (size_t)c->ld, 4, qy);
+    if ((rc = download_fields(c, c->GA.p, 4, qx, 2))) return rc;
+    return download_fields(c, c->GA.p + 1, 4, qy, 2);
 }
 
 int kmf_op_q_derivatives(kmf_ctx *c, const double *q, int n_inner, const double *pqx, const double *pqy,
@@ -1239,8 +1240,8 @@ int kmf_op_q_derivatives(kmf_ctx *c, const double *q, int n_inner, const double 
     const int nb = nblk(c->n);
     DG g = c->dg();
     if (pqx && pqy) {
-        if ((rc = upload_fields(c, pqx, 4, c->GA.p))) return rc;
-        if ((rc = upload_fields(c, pqy, 4, c->GA.p + 4 * (size_t)c->ld))) return rc;
+        if ((rc = upload_fields(c, pqx, 4, c->GA.p, 2))) return rc;
+        if ((rc = upload_fields(c, pqy, 4, c->GA.p + 1, 2))) return rc;
     } else {
         launch_first_order(c, c->s0, c->GA.p, c->ctrl.p, 0);
     }
@@ -1257,8 +1258,8 @@ int kmf_op_q_derivatives(kmf_ctx *c, const double *q, int n_inner, const double 
         }
         std::swap(cur, nxt);
     }
-    if ((rc = download_fields(c, cur, 4, qx))) return rc;
-    return download_fields(c, cur + 4 * (size_t)c->ld, 4, qy);
+    if ((rc = download_fields(c, cur, 4, qx, 2))) return rc;
+    return download_fields(c, cur + 1, 4, qy, 2);
 }
 
 namespace {
@@ -1266,8 +1267,8 @@ int upload_flow(kmf_ctx *c, const double *q, const double *qx, const double *qy)
 {
     int rc = upload_fields(c, q, 4, c->q.p);
     if (rc) return rc;
-    if ((rc = upload_fields(c, qx, 4, c->GA.p))) return rc;
-    return upload_fields(c, qy, 4, c->GA.p + 4 * (size_t)c->ld);
+    if ((rc = upload_fields(c, qx, 4, c->GA.p, 2))) return rc;
+    return upload_fields(c, qy, 4, c->GA.p + 1, 2);
 }
 }  // namespace
 

@@ -2,8 +2,10 @@
 //
 // Device data layout:
 //   * per-point fields are SoA with a padded leading dimension `ld`
-//     (component c of device slot i at [c*ld + i]): q[4], G[8] = (qx[4],
-//     qy[4]), U_outer[4], U_stage[4], R[4], dt, flags;
+//     (component c of device slot i at [c*ld + i]): q[4], U_outer[4],
+//     U_stage[4], R[4], dt, flags; the q gradients G interleave the two
+//     derivatives of a component, (qx_c, qy_c) of slot i as one double2 at
+//     G2[c*ld + i], so a gather of both is one 16-byte load (gload);
 //   * the full stencil is stored as sliced ELLPACK with slice height 32
 //     (one warp): neighbour slot s of point i lives at
 //     eoff[i/32] + s*32 + i%32, so the per-slot gathers of a warp are one
@@ -115,6 +117,16 @@ KMF_HD void edge_offsets(const DG &g, int ent, int j, double xi, double yi, doub
 
 KMF_HD int ell_base(const DG &g, int i) { return g.eoff[i >> 5] + (i & 31); }
 
+// (qx_k, qy_k) of slot i in the interleaved gradient layout
+KMF_HD double2 gload(const double *__restrict__ G, int ld, int k, int i)
+{
+    return reinterpret_cast<const double2 *>(G)[k * ld + i];
+}
+KMF_HD void gstore(double *__restrict__ G, int ld, int k, int i, double gx, double gy)
+{
+    reinterpret_cast<double2 *>(G)[k * ld + i] = make_double2(gx, gy);
+}
+
 // Programmatic dependent launch (kernels launched with the PDL attribute,
 // launch_ex in kmf_b200.cu): pdl_trigger lets the next kernel of the
 // stream be scheduled while this grid's last wave drains; pdl_wait blocks
@@ -221,8 +233,9 @@ KMF_HD void qg_gather(QgSlot<NC, WG> &o, const DG &g, const double *__restrict__
     for (int k = 0; k < NC; k++) {
         o.q[k] = q[(k0 + k) * ld + j];
         if (WG) {
-            o.gx[k] = G[(k0 + k) * ld + j];
-            o.gy[k] = G[(4 + k0 + k) * ld + j];
+            const double2 v = gload(G, ld, k0 + k, j);
+            o.gx[k] = v.x;
+            o.gy[k] = v.y;
         }
     }
 }
@@ -335,8 +348,8 @@ __global__ void __launch_bounds__(TB, MB) k_first_order(DG g, const double *__re
     const double sxx = g.fsum[i], sxy = g.fsum[ld + i], syy = g.fsum[2 * ld + i], det = g.fsum[3 * ld + i];
 #pragma unroll
     for (int k = 0; k < NC; k++) {
-        G[(k0 + k) * ld + i] = DIV(SUB(MUL(syy, sx[k]), MUL(sxy, sy[k])), det);
-        G[(4 + k0 + k) * ld + i] = DIV(SUB(MUL(sxx, sy[k]), MUL(sxy, sx[k])), det);
+        gstore(G, ld, k0 + k, i, DIV(SUB(MUL(syy, sx[k]), MUL(sxy, sy[k])), det),
+               DIV(SUB(MUL(sxx, sy[k]), MUL(sxy, sx[k])), det));
     }
 }
 
@@ -366,8 +379,9 @@ __global__ void __launch_bounds__(TB, MB) k_sweep(DG g, const double *__restrict
 #pragma unroll
         for (int k = 0; k < NC; k++) {
             qi[k] = q[(k0 + k) * ld + i];
-            gxi[k] = Gin[(k0 + k) * ld + i];
-            gyi[k] = Gin[(4 + k0 + k) * ld + i];
+            const double2 v = gload(Gin, ld, k0 + k, i);
+            gxi[k] = v.x;
+            gyi[k] = v.y;
             sx[k] = 0.0;
             sy[k] = 0.0;
         }
@@ -406,8 +420,9 @@ __global__ void __launch_bounds__(TB, MB) k_sweep(DG g, const double *__restrict
 #pragma unroll
                 for (int k = 0; k < NC; k++) {
                     qj[u][k] = q[(k0 + k) * ld + jj[u]];
-                    gxj[u][k] = Gin[(k0 + k) * ld + jj[u]];
-                    gyj[u][k] = Gin[(4 + k0 + k) * ld + jj[u]];
+                    const double2 v = gload(Gin, ld, k0 + k, jj[u]);
+                    gxj[u][k] = v.x;
+                    gyj[u][k] = v.y;
                 }
             }
 #pragma unroll
@@ -435,8 +450,7 @@ __global__ void __launch_bounds__(TB, MB) k_sweep(DG g, const double *__restrict
         for (int k = 0; k < NC; k++) {
             double nx_ = DIV(SUB(MUL(syy, sx[k]), MUL(sxy, sy[k])), det);
             double ny_ = DIV(SUB(MUL(sxx, sy[k]), MUL(sxy, sx[k])), det);
-            Gout[(k0 + k) * ld + i] = nx_;
-            Gout[(4 + k0 + k) * ld + i] = ny_;
+            gstore(Gout, ld, k0 + k, i, nx_, ny_);
             if (want_res) {
                 rmax = fmax(rmax, fabs(nx_ - gxi[k]));
                 rmax = fmax(rmax, fabs(ny_ - gyi[k]));
@@ -503,8 +517,8 @@ __global__ void __launch_bounds__(kTB, MINB) k_flux(DG g, const double *__restri
         double ti[4], t0[4];
 #pragma unroll
         for (int k = 0; k < 4; k++) {
-            ti[k] = qtilde(q[k * ld + j], G[k * ld + j], G[(4 + k) * ld + j], dx, dy);
-            t0[k] = qtilde(q[k * ld + io], G[k * ld + io], G[(4 + k) * ld + io], dx, dy);
+            ti[k] = qtilde(q[k * ld + j], gload(G, ld, k, j).x, gload(G, ld, k, j).y, dx, dy);
+            t0[k] = qtilde(q[k * ld + io], gload(G, ld, k, io).x, gload(G, ld, k, io).y, dx, dy);
         }
         const double *cf = g.fcoef + io;  // cf[k * ld]: (cx, cy) of x+, x-, y+, y-
         // solver.py:164 positivity (q4 >= 0, NaN caught by q_to_primitives)
@@ -618,8 +632,8 @@ __global__ void __launch_bounds__(kTB, MINB) k_flux2(DG g, const double *__restr
 #pragma unroll
     for (int k = 0; k < 4; k++) {
         qi[k] = q[k * ld + ii];
-        gxi[k] = G[k * ld + ii];
-        gyi[k] = G[(4 + k) * ld + ii];
+        gxi[k] = gload(G, ld, k, ii).x;
+        gyi[k] = gload(G, ld, k, ii).y;
     }
     // this lane's two families: A -> (x+, x-), B -> (y+, y-)
     const double cP_x = interior ? g.fcoef[(roleA ? 0 : 4) * ld + ii] : 0.0;
@@ -646,8 +660,8 @@ __global__ void __launch_bounds__(kTB, MINB) k_flux2(DG g, const double *__restr
 #pragma unroll
         for (int k = 0; k < 4; k++) {
             const double qq = roleA ? q[k * ld + p] : qi[k];
-            const double gx = roleA ? G[k * ld + p] : gxi[k];
-            const double gy = roleA ? G[(4 + k) * ld + p] : gyi[k];
+            const double gx = roleA ? gload(G, ld, k, p).x : gxi[k];
+            const double gy = roleA ? gload(G, ld, k, p).y : gyi[k];
             t[k] = qtilde(qq, gx, gy, dx, dy);  // solver.py:184-185, bitwise
         }
         const double t4o = __shfl_xor_sync(FULL, t[3], 1);
@@ -770,8 +784,8 @@ __global__ void __launch_bounds__(kTB) k_boundary(DG g, DB b, const double *__re
 #pragma unroll
     for (int k = 0; k < 4; k++) {
         qi[k] = q[k * ld + pt];
-        gxi[k] = G[k * ld + pt];
-        gyi[k] = G[(4 + k) * ld + pt];
+        gxi[k] = gload(G, ld, k, pt).x;
+        gyi[k] = gload(G, ld, k, pt).y;
     }
     // free-stream Maxwellian in this point's frame (solver.py:365-369)
     double gfs[4] = {0, 0, 0, 0};
@@ -806,7 +820,7 @@ __global__ void __launch_bounds__(kTB) k_boundary(DG g, DB b, const double *__re
             double ti[4], t0[4];
 #pragma unroll
             for (int k = 0; k < 4; k++) {
-                ti[k] = qtilde(q[k * ld + j], G[k * ld + j], G[(4 + k) * ld + j], dxg, dyg);
+                ti[k] = qtilde(q[k * ld + j], gload(G, ld, k, j).x, gload(G, ld, k, j).y, dxg, dyg);
                 t0[k] = qtilde(qi[k], gxi[k], gyi[k], dxg, dyg);
             }
             if (!(ti[3] < 0.0) || !(t0[3] < 0.0)) {
@@ -1171,22 +1185,25 @@ __global__ void k_get_state(DG g, const double *__restrict__ Uo, const long long
 }
 
 // device slots <-> caller order for (nc, n) SoA fields
-__global__ void k_to_dev(int n, int ld, int nc, const double *__restrict__ src, const long long *__restrict__ perm,
-                         double *__restrict__ dst)
+// host (nc, n) caller order <-> device slots; field k of slot i at
+// dst[k * fs + i * ps] (ps = 1, fs = ld: SoA; ps = 2, fs = 2 ld: one half of
+// the interleaved gradient layout)
+__global__ void k_to_dev(int n, long long fs, int ps, int nc, const double *__restrict__ src,
+                         const long long *__restrict__ perm, double *__restrict__ dst)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const long long s = perm ? perm[i] : i;
-    for (int k = 0; k < nc; k++) dst[k * ld + i] = src[(long long)k * n + s];
+    for (int k = 0; k < nc; k++) dst[k * fs + (long long)i * ps] = src[(long long)k * n + s];
 }
 
-__global__ void k_from_dev(int n, int ld, int nc, const double *__restrict__ src, const long long *__restrict__ perm,
-                           double *__restrict__ dst)
+__global__ void k_from_dev(int n, long long fs, int ps, int nc, const double *__restrict__ src,
+                           const long long *__restrict__ perm, double *__restrict__ dst)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const long long s = perm ? perm[i] : i;
-    for (int k = 0; k < nc; k++) dst[(long long)k * n + s] = src[k * ld + i];
+    for (int k = 0; k < nc; k++) dst[(long long)k * n + s] = src[k * fs + (long long)i * ps];
 }
 
 // --------------------------------------------------------------- diagnostics
@@ -1208,8 +1225,8 @@ __global__ void k_diag_flux(DG g, const double *__restrict__ q, const double *__
         const int j = g.eidx[ent];
         double dx, dy;
         edge_offsets<XY>(g, ent, j, xi, yi, dx, dy);
-        double ti = qtilde(q[3 * ld + j], G[3 * ld + j], G[7 * ld + j], dx, dy);
-        double t0 = qtilde(q[3 * ld + i], G[3 * ld + i], G[7 * ld + i], dx, dy);
+        double ti = qtilde(q[3 * ld + j], gload(G, ld, 3, j).x, gload(G, ld, 3, j).y, dx, dy);
+        double t0 = qtilde(q[3 * ld + i], gload(G, ld, 3, i).x, gload(G, ld, 3, i).y, dx, dy);
         unsigned char f = 0;
         if (ti >= 0.0 || t0 >= 0.0) f |= 1;
         if (isnan(ti)) f |= 2;
@@ -1232,8 +1249,8 @@ __global__ void k_diag_frame(DG g, DB b, int fam, const double *__restrict__ q, 
         const double dt = b.dt[fam][e], dn = b.dn[fam][e];
         const double dxg = ADD(MUL(dt, tx), MUL(dn, nx));
         const double dyg = ADD(MUL(dt, ty), MUL(dn, ny));
-        double ti = qtilde(q[3 * ld + j], G[3 * ld + j], G[7 * ld + j], dxg, dyg);
-        double t0 = qtilde(q[3 * ld + pt], G[3 * ld + pt], G[7 * ld + pt], dxg, dyg);
+        double ti = qtilde(q[3 * ld + j], gload(G, ld, 3, j).x, gload(G, ld, 3, j).y, dxg, dyg);
+        double t0 = qtilde(q[3 * ld + pt], gload(G, ld, 3, pt).x, gload(G, ld, 3, pt).y, dxg, dyg);
         out[e] = (ti >= 0.0 || t0 >= 0.0) ? 1 : 0;
     }
 }

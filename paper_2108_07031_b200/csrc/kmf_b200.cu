@@ -98,7 +98,7 @@ struct kmf_ctx {
     cudaEvent_t fork = nullptr, join = nullptr;
 
     // geometry
-    DBuf<double> x, y, dmin, fsum, fcoef, edx, edy;
+    DBuf<double> x, y, pxy, dmin, fsum, fcoef, edx, edy;
     DBuf<unsigned char> flag;
     DBuf<int> eoff, deg, eidx;
     DBuf<long long> perm, cptr;
@@ -158,6 +158,7 @@ struct kmf_ctx {
         g.n_norm = dist_on ? (int)n_global : n;
         g.x = x.p;
         g.y = y.p;
+        g.pxy = reinterpret_cast<const double2 *>(pxy.p);
         g.flag = flag.p;
         g.dmin = dmin.p;
         g.eoff = eoff.p;
@@ -280,6 +281,11 @@ int build_context(kmf_ctx *c, const kmf_geometry *g)
     std::vector<double> hx = pad(g->x, 0.0), hy = pad(g->y, 0.0), hd = pad(g->d_min, 1.0);
     CK(c->x.upload(hx.data(), ld));
     CK(c->y.upload(hy.data(), ld));
+    {
+        std::vector<double> hxy(2 * (size_t)ld);
+        for (long long k = 0; k < ld; k++) hxy[2 * k] = hx[k], hxy[2 * k + 1] = hy[k];
+        CK(c->pxy.upload(hxy.data(), hxy.size()));
+    }
     CK(c->dmin.upload(hd.data(), ld));
     {
         std::vector<unsigned char> fl(ld, 0);

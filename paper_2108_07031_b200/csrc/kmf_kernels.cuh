@@ -78,6 +78,7 @@ struct DG {
     int n_norm;  // residue normalisation (global point count under a partition)
     const double *__restrict__ x;
     const double *__restrict__ y;
+    const double2 *__restrict__ pxy;  // (x, y) interleaved: one 16-byte neighbour gather
     const unsigned char *__restrict__ flag;
     const double *__restrict__ dmin;
     const int *__restrict__ eoff;   // per 32-point slice
@@ -107,8 +108,9 @@ template <bool XY>
 KMF_HD void edge_offsets(const DG &g, int ent, int j, double xi, double yi, double &dx, double &dy)
 {
     if (XY) {
-        dx = SUB(g.x[j], xi);  // geometry.py:382-383, bitwise
-        dy = SUB(g.y[j], yi);
+        const double2 pj = g.pxy[j];
+        dx = SUB(pj.x, xi);  // geometry.py:382-383, bitwise
+        dy = SUB(pj.y, yi);
     } else {
         dx = g.edx[ent];
         dy = g.edy[ent];
@@ -227,8 +229,9 @@ template <int NC, bool WG>
 KMF_HD void qg_gather(QgSlot<NC, WG> &o, const DG &g, const double *__restrict__ q, const double *__restrict__ G,
                       int ld, int k0, int j)
 {
-    o.x = g.x[j];
-    o.y = g.y[j];
+    const double2 pj = g.pxy[j];
+    o.x = pj.x;
+    o.y = pj.y;
 #pragma unroll
     for (int k = 0; k < NC; k++) {
         o.q[k] = q[(k0 + k) * ld + j];

@@ -1172,11 +1172,12 @@ int kmf_last_indices(kmf_ctx *c, int64_t *idx, int64_t cap)
 // ------------------------------------------------------- context operators
 
 namespace {
-// ps = 2: one derivative (dev = G or G + 1) of the interleaved gradients
-int upload_fields(kmf_ctx *c, const double *h, int nc, double *dev, int ps = 1)
+// ps = 2: one derivative (dev = G or G + 1) of the interleaved gradients;
+// ps = 4, fs = 1: the per-point q records
+int upload_fields(kmf_ctx *c, const double *h, int nc, double *dev, int ps = 1, long long fs = -1)
 {
     CK(cudaMemcpyAsync(c->stage_buf.p, h, sizeof(double) * nc * (size_t)c->n, cudaMemcpyHostToDevice, c->s0));
-    k_to_dev<<<nblk(c->n), kTB, 0, c->s0>>>(c->n, (long long)ps * c->ld, ps, nc, c->stage_buf.p,
+    k_to_dev<<<nblk(c->n), kTB, 0, c->s0>>>(c->n, fs < 0 ? (long long)ps * c->ld : fs, ps, nc, c->stage_buf.p,
                                             c->has_perm ? c->perm.p : nullptr, dev);
     CK(cudaGetLastError());
     return KMF_OK;
@@ -1222,7 +1223,7 @@ int kmf_op_first_order(kmf_ctx *c, const double *q, double *qx, double *qy)
 {
     if (!c || !q || !qx || !qy) return KMF_EINVAL;
     CK(cudaSetDevice(c->device));
-    int rc = upload_fields(c, q, 4, c->q.p);
+    int rc = upload_fields(c, q, 4, c->q.p, 4, 1);
     if (rc) return rc;
     if ((rc = reset_ctrl(c))) return rc;
     launch_first_order(c, c->s0, c->GA.p, c->ctrl.p, 0);
@@ -1240,7 +1241,7 @@ int kmf_op_q_derivatives(kmf_ctx *c, const double *q, int n_inner, const double 
         return KMF_EINVAL;
     }
     CK(cudaSetDevice(c->device));
-    int rc = upload_fields(c, q, 4, c->q.p);
+    int rc = upload_fields(c, q, 4, c->q.p, 4, 1);
     if (rc) return rc;
     if ((rc = reset_ctrl(c))) return rc;
     const int nb = nblk(c->n);
@@ -1271,7 +1272,7 @@ int kmf_op_q_derivatives(kmf_ctx *c, const double *q, int n_inner, const double 
 namespace {
 int upload_flow(kmf_ctx *c, const double *q, const double *qx, const double *qy)
 {
-    int rc = upload_fields(c, q, 4, c->q.p);
+    int rc = upload_fields(c, q, 4, c->q.p, 4, 1);
     if (rc) return rc;
     if ((rc = upload_fields(c, qx, 4, c->GA.p, 2))) return rc;
     return upload_fields(c, qy, 4, c->GA.p + 1, 2);

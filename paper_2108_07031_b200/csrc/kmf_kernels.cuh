@@ -2,10 +2,12 @@
 //
 // Device data layout:
 //   * per-point fields are SoA with a padded leading dimension `ld`
-//     (component c of device slot i at [c*ld + i]): q[4], U_outer[4],
-//     U_stage[4], R[4], dt, flags; the q gradients G interleave the two
-//     derivatives of a component, (qx_c, qy_c) of slot i as one double2 at
-//     G2[c*ld + i], so a gather of both is one 16-byte load (gload);
+//     (component c of device slot i at [c*ld + i]): U_outer[4], U_stage[4],
+//     R[4], dt, flags; the fields the stencil gathers are packed per point
+//     instead: q as one 32-byte record q[4*i + c] (one 256-bit load per
+//     neighbour, qload), the q gradients G with the two derivatives of a
+//     component interleaved, (qx_c, qy_c) of slot i as one double2 at
+//     G2[c*ld + i] (gload), and (x, y) as one double2 (pxy);
 //   * the full stencil is stored as sliced ELLPACK with slice height 32
 //     (one warp): neighbour slot s of point i lives at
 //     eoff[i/32] + s*32 + i%32, so the per-slot gathers of a warp are one
@@ -118,6 +120,36 @@ KMF_HD void edge_offsets(const DG &g, int ent, int j, double xi, double yi, doub
 }
 
 KMF_HD int ell_base(const DG &g, int i) { return g.eoff[i >> 5] + (i & 31); }
+
+// the q record of slot i: one 256-bit load (LDG.E.ENL2.256)
+struct __align__(32) Q4 {
+    double v[4];
+};
+KMF_HD Q4 qload(const double *__restrict__ q, int i) { return reinterpret_cast<const Q4 *>(q)[i]; }
+// components k0 .. k0+NC-1 of slot i's record (NC 4: 256-bit, 2: 128-bit)
+template <int NC>
+KMF_HD void qload_nc(const double *__restrict__ q, int i, int k0, double (&out)[NC])
+{
+    if (NC == 4) {
+        const Q4 r = qload(q, i);
+#pragma unroll
+        for (int k = 0; k < NC; k++) out[k] = r.v[k];
+    } else if (NC == 2) {
+        const double2 r = reinterpret_cast<const double2 *>(q + 4 * i + k0)[0];
+        out[0] = r.x;
+        out[NC - 1] = r.y;
+    } else {
+#pragma unroll
+        for (int k = 0; k < NC; k++) out[k] = q[4 * i + k0 + k];
+    }
+}
+KMF_HD void qstore(double *__restrict__ q, int i, const double (&v)[4])
+{
+    Q4 r;
+#pragma unroll
+    for (int k = 0; k < 4; k++) r.v[k] = v[k];
+    reinterpret_cast<Q4 *>(q)[i] = r;
+}
 
 // (qx_k, qy_k) of slot i in the interleaved gradient layout
 KMF_HD double2 gload(const double *__restrict__ G, int ld, int k, int i)
@@ -232,9 +264,9 @@ KMF_HD void qg_gather(QgSlot<NC, WG> &o, const DG &g, const double *__restrict__
     const double2 pj = g.pxy[j];
     o.x = pj.x;
     o.y = pj.y;
+    qload_nc<NC>(q, j, k0, o.q);
 #pragma unroll
     for (int k = 0; k < NC; k++) {
-        o.q[k] = q[(k0 + k) * ld + j];
         if (WG) {
             const double2 v = gload(G, ld, k0 + k, j);
             o.gx[k] = v.x;
@@ -279,7 +311,7 @@ KMF_HD void qg_pipeline(int d, Gather gather, Eval eval)
 // (reorder.ring_tiles) put several radially stacked slices on one SM, so
 // the neighbour rings they share are fetched into L1 once.
 template <bool XY, int NC, int U, int TB = kTB, int ST = 0, int MB = 0>
-__global__ void __launch_bounds__(TB, MB) k_first_order(DG g, const double *__restrict__ q,
+__global__ void __launch_bounds__(TB, (MB ? MB : (NC == 4 && TB == 128 ? 8 : 0))) k_first_order(DG g, const double *__restrict__ q,
                                                      double *__restrict__ G, Ctrl *c, int stage)
 {
     pdl_trigger();
@@ -297,9 +329,9 @@ __global__ void __launch_bounds__(TB, MB) k_first_order(DG g, const double *__re
     if (i >= g.n) return;
     const int ld = g.ld;
     double qi[NC], sx[NC], sy[NC];
+    qload_nc<NC>(q, i, k0, qi);
 #pragma unroll
     for (int k = 0; k < NC; k++) {
-        qi[k] = q[(k0 + k) * ld + i];
         sx[k] = 0.0;
         sy[k] = 0.0;
     }
@@ -334,7 +366,7 @@ __global__ void __launch_bounds__(TB, MB) k_first_order(DG g, const double *__re
         for (int u = 0; u < U; u++) {
             edge_offsets<XY>(g, ent[u], jj[u], xi, yi, dx[u], dy[u]);
 #pragma unroll
-            for (int k = 0; k < NC; k++) qj[u][k] = q[(k0 + k) * ld + jj[u]];
+            for (int k = 0; k < NC; k++) qj[u][k] = q[4 * jj[u] + k0 + k];
         }
 #pragma unroll
         for (int u = 0; u < U; u++) {
@@ -379,9 +411,9 @@ __global__ void __launch_bounds__(TB, MB) k_sweep(DG g, const double *__restrict
     if (i < g.n) {
         const int ld = g.ld;
         double qi[NC], gxi[NC], gyi[NC], sx[NC], sy[NC];
+        qload_nc<NC>(q, i, k0, qi);
 #pragma unroll
         for (int k = 0; k < NC; k++) {
-            qi[k] = q[(k0 + k) * ld + i];
             const double2 v = gload(Gin, ld, k0 + k, i);
             gxi[k] = v.x;
             gyi[k] = v.y;
@@ -422,7 +454,7 @@ __global__ void __launch_bounds__(TB, MB) k_sweep(DG g, const double *__restrict
                 edge_offsets<XY>(g, ent[u], jj[u], xi, yi, dx[u], dy[u]);
 #pragma unroll
                 for (int k = 0; k < NC; k++) {
-                    qj[u][k] = q[(k0 + k) * ld + jj[u]];
+                    qj[u][k] = q[4 * jj[u] + k0 + k];
                     const double2 v = gload(Gin, ld, k0 + k, jj[u]);
                     gxj[u][k] = v.x;
                     gyj[u][k] = v.y;
@@ -520,8 +552,8 @@ __global__ void __launch_bounds__(kTB, MINB) k_flux(DG g, const double *__restri
         double ti[4], t0[4];
 #pragma unroll
         for (int k = 0; k < 4; k++) {
-            ti[k] = qtilde(q[k * ld + j], gload(G, ld, k, j).x, gload(G, ld, k, j).y, dx, dy);
-            t0[k] = qtilde(q[k * ld + io], gload(G, ld, k, io).x, gload(G, ld, k, io).y, dx, dy);
+            ti[k] = qtilde(q[4 * j + k], gload(G, ld, k, j).x, gload(G, ld, k, j).y, dx, dy);
+            t0[k] = qtilde(q[4 * io + k], gload(G, ld, k, io).x, gload(G, ld, k, io).y, dx, dy);
         }
         const double *cf = g.fcoef + io;  // cf[k * ld]: (cx, cy) of x+, x-, y+, y-
         // solver.py:164 positivity (q4 >= 0, NaN caught by q_to_primitives)
@@ -634,7 +666,7 @@ __global__ void __launch_bounds__(kTB, MINB) k_flux2(DG g, const double *__restr
     double qi[4], gxi[4], gyi[4];
 #pragma unroll
     for (int k = 0; k < 4; k++) {
-        qi[k] = q[k * ld + ii];
+        qi[k] = q[4 * ii + k];
         gxi[k] = gload(G, ld, k, ii).x;
         gyi[k] = gload(G, ld, k, ii).y;
     }
@@ -662,7 +694,7 @@ __global__ void __launch_bounds__(kTB, MINB) k_flux2(DG g, const double *__restr
         double t[4];
 #pragma unroll
         for (int k = 0; k < 4; k++) {
-            const double qq = roleA ? q[k * ld + p] : qi[k];
+            const double qq = roleA ? q[4 * p + k] : qi[k];
             const double gx = roleA ? gload(G, ld, k, p).x : gxi[k];
             const double gy = roleA ? gload(G, ld, k, p).y : gyi[k];
             t[k] = qtilde(qq, gx, gy, dx, dy);  // solver.py:184-185, bitwise
@@ -786,7 +818,7 @@ __global__ void __launch_bounds__(kTB) k_boundary(DG g, DB b, const double *__re
     double qi[4], gxi[4], gyi[4];
 #pragma unroll
     for (int k = 0; k < 4; k++) {
-        qi[k] = q[k * ld + pt];
+        qi[k] = q[4 * pt + k];
         gxi[k] = gload(G, ld, k, pt).x;
         gyi[k] = gload(G, ld, k, pt).y;
     }
@@ -823,7 +855,7 @@ __global__ void __launch_bounds__(kTB) k_boundary(DG g, DB b, const double *__re
             double ti[4], t0[4];
 #pragma unroll
             for (int k = 0; k < 4; k++) {
-                ti[k] = qtilde(q[k * ld + j], gload(G, ld, k, j).x, gload(G, ld, k, j).y, dxg, dyg);
+                ti[k] = qtilde(q[4 * j + k], gload(G, ld, k, j).x, gload(G, ld, k, j).y, dxg, dyg);
                 t0[k] = qtilde(qi[k], gxi[k], gyi[k], dxg, dyg);
             }
             if (!(ti[3] < 0.0) || !(t0[3] < 0.0)) {
@@ -999,7 +1031,7 @@ __global__ void __launch_bounds__(kTB) k_update(DG g, double *__restrict__ Uo, d
         double qq[4];
         p2q(rho, u1, u2, p, gamma, qq);
 #pragma unroll
-        for (int k = 0; k < 4; k++) q[k * ld + i] = qq[k];
+        qstore(q, i, qq);
         if (STAGE == 4) {
             dt[i] = timestep(rho, u1, u2, p, gamma, cfl, g.dmin[i]);
             const double dr = SUB(un[0], uo[0]);
@@ -1049,7 +1081,7 @@ __global__ void k_halo_pack(int total, const int *__restrict__ slot, const int *
     if (t >= total) return;
     const int s = slot[t], b = base[t], st = stride[t];
 #pragma unroll
-    for (int k = 0; k < 4; k++) buf[b + k * st] = q[k * ld + s];
+    for (int k = 0; k < 4; k++) buf[b + k * st] = q[4 * s + k];
 }
 
 __global__ void k_halo_unpack(int total, const int *__restrict__ slot, const int *__restrict__ base,
@@ -1060,7 +1092,7 @@ __global__ void k_halo_unpack(int total, const int *__restrict__ slot, const int
     if (t >= total) return;
     const int s = slot[t], b = base[t], st = stride[t];
 #pragma unroll
-    for (int k = 0; k < 4; k++) q[k * ld + s] = buf[b + k * st];
+    for (int k = 0; k < 4; k++) q[4 * s + k] = buf[b + k * st];
 }
 
 // 96-bit window of the normalised digit array starting at bit p
@@ -1139,10 +1171,8 @@ __global__ void k_init(DG g, const double *__restrict__ prims, const long long *
     p2u(rho, u1, u2, p, gamma, U);
     p2q(rho, u1, u2, p, gamma, qq);
 #pragma unroll
-    for (int k = 0; k < 4; k++) {
-        Uo[k * ld + i] = U[k];
-        q[k * ld + i] = qq[k];
-    }
+    for (int k = 0; k < 4; k++) Uo[k * ld + i] = U[k];
+    qstore(q, i, qq);
     dt[i] = timestep(rho, u1, u2, p, gamma, cfl, g.dmin[i]);
 }
 
@@ -1160,7 +1190,7 @@ __global__ void k_refresh(DG g, const double *__restrict__ Uo, double *__restric
     u2p(u, gamma, rho, u1, u2, p);
     p2q(rho, u1, u2, p, gamma, qq);
 #pragma unroll
-    for (int k = 0; k < 4; k++) q[k * ld + i] = qq[k];
+    qstore(q, i, qq);
     dt[i] = timestep(rho, u1, u2, p, gamma, cfl, g.dmin[i]);
 }
 
@@ -1228,8 +1258,8 @@ __global__ void k_diag_flux(DG g, const double *__restrict__ q, const double *__
         const int j = g.eidx[ent];
         double dx, dy;
         edge_offsets<XY>(g, ent, j, xi, yi, dx, dy);
-        double ti = qtilde(q[3 * ld + j], gload(G, ld, 3, j).x, gload(G, ld, 3, j).y, dx, dy);
-        double t0 = qtilde(q[3 * ld + i], gload(G, ld, 3, i).x, gload(G, ld, 3, i).y, dx, dy);
+        double ti = qtilde(q[4 * j + 3], gload(G, ld, 3, j).x, gload(G, ld, 3, j).y, dx, dy);
+        double t0 = qtilde(q[4 * i + 3], gload(G, ld, 3, i).x, gload(G, ld, 3, i).y, dx, dy);
         unsigned char f = 0;
         if (ti >= 0.0 || t0 >= 0.0) f |= 1;
         if (isnan(ti)) f |= 2;
@@ -1252,8 +1282,8 @@ __global__ void k_diag_frame(DG g, DB b, int fam, const double *__restrict__ q, 
         const double dt = b.dt[fam][e], dn = b.dn[fam][e];
         const double dxg = ADD(MUL(dt, tx), MUL(dn, nx));
         const double dyg = ADD(MUL(dt, ty), MUL(dn, ny));
-        double ti = qtilde(q[3 * ld + j], gload(G, ld, 3, j).x, gload(G, ld, 3, j).y, dxg, dyg);
-        double t0 = qtilde(q[3 * ld + pt], gload(G, ld, 3, pt).x, gload(G, ld, 3, pt).y, dxg, dyg);
+        double ti = qtilde(q[4 * j + 3], gload(G, ld, 3, j).x, gload(G, ld, 3, j).y, dxg, dyg);
+        double t0 = qtilde(q[4 * pt + 3], gload(G, ld, 3, pt).x, gload(G, ld, 3, pt).y, dxg, dyg);
         out[e] = (ti >= 0.0 || t0 >= 0.0) ? 1 : 0;
     }
 }

@@ -52,12 +52,14 @@ sys.path.insert(0, str(ROOT))
 
 CONFIGS = {
     # name: (chord_points, layers, growth, mach, aoa, description)
-    "c1": (400, 100, 1.06, 0.63, 2.0, "NACA0012 40K (400x100, g=1.06) M0.63 AoA2 second order"),
+    "c1": (400, 100, 1.06, 0.63, 2.0, "NACA0012 40K (400x100, g=1.06) M0.63 AoA2 first order (qx = qy = 0)"),
     "c2": (800, 200, 1.03, 0.63, 2.0, "NACA0012 160K (800x200, g=1.03) M0.63 AoA2 second order n_inner=3"),
     "c3": (3160, 790, 1.00734, 0.85, 1.0, "NACA0012 2.5M (3160x790, g=1.00734) M0.85 AoA1 second order"),
     "c4": (6324, 1581, 1.003647, 0.63, 2.0, "NACA0012 10M (6324x1581, g=1.003647) M0.63 AoA2 second order"),
     "c5": (12648, 3162, 1.001821, 0.63, 2.0, "NACA0012 40M (12648x3162, g=1.001821) M0.63 AoA2 second order"),
 }
+# BASELINE configs[0] is the first-order scheme (SolverConfig.order = 1)
+ORDER = {"c1": 1}
 # best published RDP for this metric, C++ optimised on V100,
 # NACA 0012 40M points -> point-iterations/s
 PUBLISHED = {"c5": 1.0 / 3.41e-8}
@@ -71,6 +73,8 @@ FLUX_DP_OPS_PER_POINT = 13214
 # algorithmic bytes / DP ops of one whole point-iteration
 # (timestep, 4 x [q, first order, 3 sweeps, flux, update], residue)
 ITER_BYTES_PER_POINT = 6440
+# first-order scheme: no q-gradient kernels (4 x (208 + 3 x 272) B fewer)
+ITER_BYTES_PER_POINT_O1 = ITER_BYTES_PER_POINT - 4 * (208 + 3 * 272)
 L2_FLUSH_BYTES = 256 << 20
 
 
@@ -114,7 +118,7 @@ def build_config(name):
     cloud = generate_naca_cloud(m, L, g, 20.0)
     conn = build_stencils(cloud)  # native builder (libkmf_build.so), bit-exact with the reference's
     t1 = time.perf_counter()
-    cfg = SolverConfig(mach=mach, aoa_deg=aoa, cfl=0.2, n_inner=3, mode="fused")
+    cfg = SolverConfig(mach=mach, aoa_deg=aoa, cfl=0.2, n_inner=3, mode="fused", order=ORDER.get(name, 2))
     init = initial_primitives(cfg, cloud)
     print(f"[bench] setup {name}: {cloud.n_points} points, {conn.full.idx.size} edges; generator+builder "
           f"{t1 - t:.1f} s, initial state {time.perf_counter() - t1:.1f} s", file=sys.stderr, flush=True)
@@ -148,7 +152,7 @@ def setup(name, dist=None, rank=0):
 
         shutil.rmtree(box[0], ignore_errors=True)  # mappings stay valid until the ranks exit
     _, _, _, mach, aoa, _ = CONFIGS[name]
-    cfg = SolverConfig(mach=mach, aoa_deg=aoa, cfl=0.2, n_inner=3, mode="fused")
+    cfg = SolverConfig(mach=mach, aoa_deg=aoa, cfl=0.2, n_inner=3, mode="fused", order=ORDER.get(name, 2))
     return conn.cloud, conn, cfg, Primitives.from_array(np.asarray(extra["init"]))
 
 
@@ -240,14 +244,14 @@ def cpu_baseline(conn, cfg, init, target_s=12.0):
     fs = free_stream(cfg.mach, cfg.aoa_deg, cfg.gamma)
     fsv = [fs.rho[0], fs.u1[0], fs.u2[0], fs.p[0]]
     t = time.perf_counter()
-    O.solve(pk, init4n, fsv, 1, gamma=cfg.gamma, cfl=cfg.cfl, n_inner=cfg.n_inner)
+    O.solve(pk, init4n, fsv, 1, gamma=cfg.gamma, cfl=cfg.cfl, n_inner=cfg.n_inner if cfg.order == 2 else 0)
     one = time.perf_counter() - t
     if one > 0.5 * target_s:  # the first whole iteration is the sample
         iters, sec = 1, one
     else:
         iters = int(min(200, max(2, target_s / max(one, 1e-3))))
         t = time.perf_counter()
-        O.solve(pk, init4n, fsv, iters, gamma=cfg.gamma, cfl=cfg.cfl, n_inner=cfg.n_inner)
+        O.solve(pk, init4n, fsv, iters, gamma=cfg.gamma, cfl=cfg.cfl, n_inner=cfg.n_inner if cfg.order == 2 else 0)
         sec = time.perf_counter() - t
     return {"value": npts * iters / sec, "unit": UNIT, "cores": threads, "kind": "port",
             "sample": f"{iters} outer iterations ({sec:.1f} s) on {desc}; oracle/kmf_oracle.c with OpenMP "
@@ -373,6 +377,7 @@ def run_ours(args):
     if tf.exists():
         counts = json.loads(tf.read_text())
         traffic = counts.get("dram_bytes_per_launch")
+    iter_bytes = ITER_BYTES_PER_POINT_O1 if cfg.order == 1 else ITER_BYTES_PER_POINT
     line = {
         "metric": METRIC,
         "value": value,
@@ -389,7 +394,7 @@ def run_ours(args):
         "dtype": "f64",
         "data": "synthetic (procedurally generated NACA 0012 O-cloud, reference generator restated bit-exactly)",
         "config": {"workload": CONFIGS[args.config][5], "config_key": args.config, "n_points": n,
-                   "n_edges": int(conn.full.idx.size), "n_inner": cfg.n_inner, "mode": cfg.mode,
+                   "n_edges": int(conn.full.idx.size), "n_inner": cfg.n_inner, "order": cfg.order, "mode": cfg.mode,
                    "l2": "flushed between timed steps (256 MiB memset on the solver stream)",
                    "parallelism": f"partition x{ws} (deep halo, NCCL)" if ws > 1 else "single GPU",
                    "point_order": args.order},
@@ -403,9 +408,9 @@ def run_ours(args):
                      "share_of_step": stage_share,
                      "note": "the flux kernel is FP64-pipe bound (SURVEY.md 8(d)); see roofline_fp64"},
         "roofline_iteration": {
-            "bound": "hbm", "bytes_per_point_iter": ITER_BYTES_PER_POINT,
-            "achieved": ITER_BYTES_PER_POINT * value / ws / 1e9, "peak": hbm_peak, "unit": "GB/s",
-            "frac": ITER_BYTES_PER_POINT * value / ws / 1e9 / hbm_peak,
+            "bound": "hbm", "bytes_per_point_iter": iter_bytes,
+            "achieved": iter_bytes * value / ws / 1e9, "peak": hbm_peak, "unit": "GB/s",
+            "frac": iter_bytes * value / ws / 1e9 / hbm_peak,
             "note": "whole outer iteration against the HBM roofline implied by SURVEY 8(d)'s 6.44 KB per "
                     "point-iteration (north star), per GPU"},
         "roofline_fp64": roofline_fp64(counts, n, n_flux, flux_launch_s, dfma_rate, achieved_ops, peak_fp64.value),
@@ -432,9 +437,10 @@ def run_reference(args):
     fsv = [fs.rho[0], fs.u1[0], fs.u2[0], fs.p[0]]
     W, K = max(args.warmup, 0), args.steps
     if W:
-        _, prims, _, _, _ = O.solve(pk, prims, fsv, W, gamma=cfg.gamma, cfl=cfg.cfl, n_inner=cfg.n_inner)
+        _, prims, _, _, _ = O.solve(pk, prims, fsv, W, gamma=cfg.gamma, cfl=cfg.cfl,
+                                    n_inner=cfg.n_inner if cfg.order == 2 else 0)
     t = time.perf_counter()
-    O.solve(pk, prims, fsv, K, gamma=cfg.gamma, cfl=cfg.cfl, n_inner=cfg.n_inner)
+    O.solve(pk, prims, fsv, K, gamma=cfg.gamma, cfl=cfg.cfl, n_inner=cfg.n_inner if cfg.order == 2 else 0)
     sec = time.perf_counter() - t
     value = npts * K / sec
     line = {

@@ -108,7 +108,7 @@ typedef struct {
     double gamma;
     double cfl;
     double fs[4];            /* free_stream(mach, aoa, gamma) primitives, state.py:170-185 */
-    int n_inner;             /* Jacobi sweeps per stage (lsq.py:229) */
+    int n_inner;             /* Jacobi sweeps per stage (lsq.py:229); 0 = first-order scheme (qx = qy = 0) */
     int mode;                /* 0 fused, 1 split4 (solver.py:51, :218-229) */
     double convergence_tol;  /* <= 0: none (solver.py:557-559) */
     int instrument;          /* per-stage device timing (solver.py:461-474) */

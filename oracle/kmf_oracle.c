@@ -699,7 +699,12 @@ int orc_solve(const orc_conn *c, const orc_params *p, double *prims, double *U, 
             err->iteration = it;
             err->stage = stage;
             if ((rc = orc_primitives_to_q(n, prims, gamma, q, err))) goto done;
-            orc_compute_q_derivatives(c, q, p->n_inner, qx, qy, NULL);
+            if (p->n_inner > 0) {
+                orc_compute_q_derivatives(c, q, p->n_inner, qx, qy, NULL);
+            } else {  /* first-order scheme: qx = qy = 0 */
+                memset(qx, 0, sizeof(double) * m);
+                memset(qy, 0, sizeof(double) * m);
+            }
             if ((rc = orc_flux_residual(c, q, qx, qy, p->mode, gamma, R, err))) goto done;
             if ((rc = orc_apply_boundary(c, q, qx, qy, fs, gamma, R, err))) goto done;
             orc_state_update_rk(n, Uo, U, stage, dt, R, Un);

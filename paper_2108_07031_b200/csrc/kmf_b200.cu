@@ -838,7 +838,12 @@ void enqueue_stage(kmf_ctx *c, const kmf_params *p, int stage, IterOut io, int h
     const bool inst = how == ITER_INSTRUMENT, bench = how == ITER_BENCH;
     cudaEvent_t *e = &c->ev[4 * (stage - 1)];
     if (inst) cudaEventRecord(e[0], c->s0);
-    int which = launch_qgrad(c, c->s0, stage, p->n_inner, ctl, 0);
+    // n_inner = 0: the first-order scheme (qx = qy = 0 -> q~ = q bitwise)
+    int which = 0;
+    if (p->n_inner > 0)
+        which = launch_qgrad(c, c->s0, stage, p->n_inner, ctl, 0);
+    else
+        cudaMemsetAsync(c->GA.p, 0, sizeof(double) * 8 * (size_t)c->ld, c->s0);
     const double *G = which ? c->GB.p : c->GA.p;
     c->last_G = which;
     if (inst) cudaEventRecord(e[1], c->s0);
@@ -1048,7 +1053,7 @@ int kmf_run(kmf_ctx *c, const kmf_params *p, int n_iter, double *history, int *i
         set_msg("kmf_run: no state (call kmf_set_state first)");
         return KMF_EINVAL;
     }
-    if (p->n_inner < 1 || !(p->gamma > 1.0 && p->gamma < 2.0) || !(p->cfl > 0.0 && p->cfl <= 1.0) ||
+    if (p->n_inner < 0 || !(p->gamma > 1.0 && p->gamma < 2.0) || !(p->cfl > 0.0 && p->cfl <= 1.0) ||
         (p->mode != 0 && p->mode != 1)) {
         set_msg("kmf_run: invalid parameters");
         return KMF_EINVAL;
@@ -1605,7 +1610,7 @@ int kmf_bench_steps(kmf_ctx *c, const kmf_params *p, int n_steps, int64_t flush_
     Ctrl fin;
     CK(cudaMemcpy(&fin, c->ctrl.p, sizeof fin, cudaMemcpyDeviceToHost));
     if (launches_per_step)
-        *launches_per_step = 4 * (1 + p->n_inner + (p->mode ? 4 : 1) + (c->nb > 0 ? 1 : 0) + 1) +  // the iteration close is fused into update<4>
+        *launches_per_step = 4 * ((p->n_inner ? 1 + p->n_inner : 0) + (p->mode ? 4 : 1) + (c->nb > 0 ? 1 : 0) + 1) +  // the iteration close is fused into update<4>
                              ((c->dist_on && c->nccl) ? 4 * ((c->send_total ? 1 : 0) + (c->recv_total ? 1 : 0)) + 1 : 0);
     if ((fin.state & 3ull) == 1ull) {
         set_msg("kmf_bench_steps: positivity failure at iteration %d", fin.err_iter);

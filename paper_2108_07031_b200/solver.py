@@ -57,6 +57,9 @@ class SolverConfig:
     mode: str = "fused"
     threads: int = 1
     convergence_tol: float | None = None
+    # extension: 1 = first-order scheme (qx = qy = 0, BASELINE config 1
+    # "first-order"); the reference's solve() is second order
+    order: int = 2
 
     def __post_init__(self):
         if not self.mach > 0.0:
@@ -75,10 +78,12 @@ class SolverConfig:
             raise ValueError("threads must be at least 1")
         if self.convergence_tol is not None and not self.convergence_tol > 0.0:
             raise ValueError("convergence_tol must be positive")
+        if self.order not in (1, 2):
+            raise ValueError("order must be 1 or 2")
 
     def to_dict(self) -> dict:
         return {k: getattr(self, k) for k in ("mach", "aoa_deg", "gamma", "cfl", "n_outer", "n_inner", "mode",
-                                               "threads", "convergence_tol")}
+                                               "threads", "convergence_tol", "order")}
 
 
 @dataclass
@@ -100,7 +105,7 @@ def _params(config: SolverConfig, instrument: bool = False, timing_skip: int = 0
     p.cfl = config.cfl
     for i, v in enumerate((fs.rho[0], fs.u1[0], fs.u2[0], fs.p[0])):
         p.fs[i] = float(v)
-    p.n_inner = config.n_inner
+    p.n_inner = config.n_inner if config.order == 2 else 0  # 0: first-order scheme on the device
     p.mode = MODES.index(config.mode)
     p.convergence_tol = config.convergence_tol if config.convergence_tol is not None else 0.0
     p.instrument = int(instrument)

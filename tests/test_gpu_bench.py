@@ -32,7 +32,9 @@ def test_bench_ours_contract(gpu):
     assert d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] == 3 and d["value"] > 0
     assert d["config"]["n_points"] == 40000 and "workload" in d["config"]
     assert d["e2e"]["h2d_bytes_per_step"] == 4 * 40000 * 8 and d["e2e"]["value"] > 0
-    assert d["gpu_launches"] == 3 * 28
+    # per step: 4 stages x (first order + 3 sweeps + flux + boundary + update)
+    # = 28 in second order; c1 is BASELINE's first-order config: 4 x 3 = 12
+    assert d["config"]["order"] == 1 and d["gpu_launches"] == 3 * 12
     for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
         assert k in d["roofline"]
     assert 0 < d["roofline"]["frac"] < 1

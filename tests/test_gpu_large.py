@@ -237,3 +237,24 @@ def test_c40k_reference_breakdown_reproduced(gpu):
     # positions in that 4096-point block's family edge list (solver.py:162-168)
     assert str(exc.value) == fail["message"]
     assert [int(i) for i in exc.value.indices] == fail["indices"]
+
+
+def test_c1_first_order_thousand_iterations_match_oracle(gpu):
+    """BASELINE configs[0]: 40K points, M 0.63, AoA 2, first order, 1000
+    iterations (the reference's solve() is second order only; the oracle's
+    first-order loop is pinned to the reference's operators in
+    tests/test_oracle_golden.py)."""
+    import os
+
+    cloud = generate_naca_cloud(400, 100, 1.06, 20.0)
+    conn = build_stencils(cloud)
+    cfg = SolverConfig(mach=0.63, aoa_deg=2.0, n_outer=1000, order=1)
+    init = initial_primitives(cfg, cloud)
+    res = solve(cfg, cloud, conn, initial_state=init, instrument=False)
+    O.set_threads(os.cpu_count() or 1)
+    fs = free_stream(cfg.mach, cfg.aoa_deg)
+    hist, prims, _, its, _ = O.solve(O.Packed(conn), init.as_array(), [fs.rho[0], fs.u1[0], fs.u2[0], fs.p[0]], 1000,
+                                     n_inner=0)
+    assert res.iterations == its == 1000
+    assert np.max(np.abs(res.residue_history - hist) / hist) <= 1e-10
+    assert np.allclose(res.primitives.as_array(), prims, rtol=1e-10, atol=1e-12)

@@ -196,6 +196,27 @@ def test_inner_sweep_updates_shrink(gpu, small_naca, small_naca_conn):
     assert np.array_equal(g.qx, qx) and np.array_equal(g.qy, qy) and np.array_equal(np.asarray(r), ro)
 
 
+def test_first_order_scheme_matches_reference(gpu, small_naca, small_naca_conn):
+    """SolverConfig(order=1): the first-order scheme (qx = qy = 0, BASELINE
+    config 1) against a loop of the reference's own stage operators
+    (tests/golden/order1): history <= 1e-10 relative, state rtol 1e-10;
+    fused == split4 bitwise."""
+    A, _ = golden("order1")
+    for tag, (mach, aoa, iters) in {"m63a2": (0.63, 2.0, 200), "m85a1": (0.85, 1.0, 100)}.items():
+        res = solve(SolverConfig(mach=mach, aoa_deg=aoa, n_outer=iters, order=1), small_naca, small_naca_conn,
+                    instrument=False)
+        ref = A[f"{tag}.history"]
+        assert np.max(np.abs(res.residue_history - ref) / ref) <= 1e-10
+        assert np.allclose(res.primitives.as_array(), A[f"{tag}.prims"], rtol=1e-10, atol=1e-12)
+    a = solve(SolverConfig(mach=0.63, aoa_deg=2.0, n_outer=20, order=1, mode="split4"), small_naca, small_naca_conn,
+              instrument=False)
+    b = solve(SolverConfig(mach=0.63, aoa_deg=2.0, n_outer=20, order=1), small_naca, small_naca_conn,
+              instrument=False)
+    assert np.array_equal(a.residue_history, b.residue_history)
+    with pytest.raises(ValueError, match="order"):
+        SolverConfig(mach=0.63, order=3)
+
+
 def test_uniform_flow_residual_vanishes(gpu, small_naca, small_naca_conn):
     """Reference tests/test_solver.py:139-142."""
     prims = free_stream(0.63, 2.0, n=small_naca.n_points)

@@ -165,3 +165,21 @@ def test_config1_history_against_reference():
     n = 60
     hist, *_ = O.solve(O.Packed(build_stencils(cloud)), init.as_array(), fs_vec(meta["mach"], meta["aoa"]), n)
     assert np.all(np.abs(hist - A["history"][:n]) <= 1e-10 * A["history"][:n])
+
+
+def test_first_order_scheme_against_reference_operators(small_naca_conn):
+    """The first-order scheme (qx = qy = 0; BASELINE config 1) of the oracle
+    (n_inner = 0) against the same loop composed of the reference's own
+    stage operators (tests/golden/order1, tools/make_golden.py order1)."""
+    from paper_2108_07031_b200 import SolverConfig, generate_naca_cloud, initial_primitives
+
+    A, _ = golden("order1")
+    cloud = generate_naca_cloud(80, 30, 1.15, 20.0)
+    pk = O.Packed(small_naca_conn)
+    O.set_threads(8)
+    for tag, (mach, aoa, iters) in {"m63a2": (0.63, 2.0, 200), "m85a1": (0.85, 1.0, 100)}.items():
+        init = initial_primitives(SolverConfig(mach=mach, aoa_deg=aoa), cloud)
+        hist, prims, *_ = O.solve(pk, init.as_array(), fs_vec(mach, aoa), iters, n_inner=0)
+        ref = A[f"{tag}.history"]
+        assert np.all(np.abs(hist - ref) <= 1e-10 * ref)
+        assert np.allclose(prims, A[f"{tag}.prims"], rtol=1e-10, atol=1e-12)

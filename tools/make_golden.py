@@ -360,12 +360,52 @@ def _big(name, params, mach, aoa, iters, store_final=True):
     save(name, arrays, meta)
 
 
+def _first_order_loop(cloud, conn, mach, aoa, iters):
+    """The first-order scheme (qx = qy = 0; BASELINE config 1 "first-order",
+    SURVEY.md 8(d)) composed from the reference's own stage operators in the
+    order of its solve loop (solver.py:515-559): the reference solve() has no
+    order switch, so this loop is the oracle for the device's order=1 mode."""
+    cfg = SolverConfig(mach=mach, aoa_deg=aoa, cfl=0.2, n_outer=iters)
+    gamma = cfg.gamma
+    fs = free_stream(mach, aoa, gamma)
+    prims = _initial_primitives(cfg, cloud)
+    U = primitives_to_conserved(prims, gamma)
+    zero = np.zeros((4, cloud.n_points))
+    hist = []
+    for _ in range(iters):
+        dt = local_timestep(prims, conn, cfg.cfl, gamma)
+        U_outer = U
+        for stage in range(1, 5):
+            q = primitives_to_q(prims, gamma)
+            flow = FlowState(prims=prims, q=q, qx=zero, qy=zero)
+            R = apply_boundary(flow, flux_residual(flow, conn, "fused", gamma), conn, fs, gamma)
+            U = state_update_rk(U_outer, U, stage, dt, R)
+            prims = conserved_to_primitives(U, gamma)
+        hist.append(residue_norm(U, U_outer))
+    return np.array(hist), prims_arr(prims)
+
+
+def case_order1():
+    cloud = generate_naca_cloud(80, 30, 1.15, 20.0)
+    conn = build_stencils(cloud)
+    arrays, meta = {}, {"params": [80, 30, 1.15, 20.0], "note": "first-order loop of reference operators"}
+    for tag, (mach, aoa, iters) in {"m63a2": (0.63, 2.0, 200), "m85a1": (0.85, 1.0, 100)}.items():
+        t0 = time.perf_counter()
+        h, pr = _first_order_loop(cloud, conn, mach, aoa, iters)
+        meta[f"{tag}.seconds"] = time.perf_counter() - t0
+        meta[f"{tag}.iters"] = iters
+        arrays[f"{tag}.history"] = h
+        arrays[f"{tag}.prims"] = pr
+    save("order1", arrays, meta)
+
+
 def main(argv):
     cases = {
         "small": case_small,
         "hist2k": case_hist2k,
         "kinetics": case_kinetics,
         "lattice": case_lattice,
+        "order1": case_order1,
         "c40k": lambda: _big("c40k", (400, 100, 1.06), 0.63, 2.0, 1000),
         "c160k": lambda: _big("c160k", (800, 200, 1.03), 0.63, 2.0, 20, store_final=False),
         "c2p5m": lambda: _big("c2p5m", (3160, 790, 1.00734), 0.85, 1.0, 2, store_final=False),

@@ -543,11 +543,15 @@ void launch_fo_t(kmf_ctx *c, cudaStream_t s, double *G, Ctrl *ctl, int stage)
 
 template <bool XY, int NC, int U>
 void launch_sw_t(kmf_ctx *c, cudaStream_t s, const double *Gin, double *Gout, Ctrl *ctl, int stage, int slot,
-                 int want_res)
+                 int want_res, bool outp)
 {
-#define KMF_SW(TB, ST, MB)                                                                                  \
-    launch_ex(c->pdl, k_sweep<XY, NC, U, TB, ST, MB>, dim3(nblk(c->n, qg_points_per_block<NC, TB>())), dim3(TB), 0, \
-              s, c->dg(), (const double *)c->q.p, Gin, Gout, ctl, stage, slot, want_res)
+#define KMF_SW(TB, ST, MB)                                                                                       \
+    if (outp)                                                                                                   \
+        launch_ex(c->pdl, k_sweep<XY, NC, U, TB, ST, MB, true>, dim3(nblk(c->n, qg_points_per_block<NC, TB>())), \
+                  dim3(TB), 0, s, c->dg(), (const double *)c->q.p, Gin, Gout, ctl, stage, slot, want_res);       \
+    else                                                                                                        \
+        launch_ex(c->pdl, k_sweep<XY, NC, U, TB, ST, MB, false>, dim3(nblk(c->n, qg_points_per_block<NC, TB>())), \
+                  dim3(TB), 0, s, c->dg(), (const double *)c->q.p, Gin, Gout, ctl, stage, slot, want_res)
     KMF_TB_SWITCH(KMF_SW)
 #undef KMF_SW
 }
@@ -581,10 +585,12 @@ void launch_first_order(kmf_ctx *c, cudaStream_t s, double *G, Ctrl *ctl, int st
     KMF_QG_DISPATCH(launch_fo_t, c, s, G, ctl, stage);
 }
 
+// outp: write the plane gradient layout the flux / boundary kernels read
+// (the last sweep of a stage)
 void launch_sweep(kmf_ctx *c, cudaStream_t s, const double *Gin, double *Gout, Ctrl *ctl, int stage, int slot,
-                  int want_res)
+                  int want_res, bool outp)
 {
-    KMF_QG_DISPATCH(launch_sw_t, c, s, Gin, Gout, ctl, stage, slot, want_res);
+    KMF_QG_DISPATCH(launch_sw_t, c, s, Gin, Gout, ctl, stage, slot, want_res, outp);
 }
 
 // q-derivatives of one stage: first order into GA, sweeps ping-pong;
@@ -595,7 +601,7 @@ int launch_qgrad(kmf_ctx *c, cudaStream_t s, int stage, int n_inner, Ctrl *ctl, 
     double *cur = c->GA.p, *nxt = c->GB.p;
     int which = 0;
     for (int it = 0; it < n_inner; it++) {
-        launch_sweep(c, s, cur, nxt, ctl, stage, 1 + it, want_res);
+        launch_sweep(c, s, cur, nxt, ctl, stage, 1 + it, want_res, it + 1 == n_inner);
         std::swap(cur, nxt);
         which ^= 1;
     }
@@ -1177,8 +1183,9 @@ int kmf_last_indices(kmf_ctx *c, int64_t *idx, int64_t cap)
 // ------------------------------------------------------- context operators
 
 namespace {
-// ps = 2: one derivative (dev = G or G + 1) of the interleaved gradients;
-// ps = 4, fs = 1: the per-point q records
+// SoA by default; ps = 2: one derivative (dev = G or G + 1) of the
+// component-major gradients; ps = 4, fs = 1: the per-point q records;
+// ps = 4, fs = 2: two components of one derivative in a gradient plane
 int upload_fields(kmf_ctx *c, const double *h, int nc, double *dev, int ps = 1, long long fs = -1)
 {
     CK(cudaMemcpyAsync(c->stage_buf.p, h, sizeof(double) * nc * (size_t)c->n, cudaMemcpyHostToDevice, c->s0));
@@ -1187,13 +1194,26 @@ int upload_fields(kmf_ctx *c, const double *h, int nc, double *dev, int ps = 1, 
     CK(cudaGetLastError());
     return KMF_OK;
 }
-int download_fields(kmf_ctx *c, const double *dev, int nc, double *h, int ps = 1)
+int download_fields(kmf_ctx *c, const double *dev, int nc, double *h, int ps = 1, long long fs = -1)
 {
-    k_from_dev<<<nblk(c->n), kTB, 0, c->s0>>>(c->n, (long long)ps * c->ld, ps, nc, dev,
+    k_from_dev<<<nblk(c->n), kTB, 0, c->s0>>>(c->n, fs < 0 ? (long long)ps * c->ld : fs, ps, nc, dev,
                                               c->has_perm ? c->perm.p : nullptr, c->stage_buf.p);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(h, c->stage_buf.p, sizeof(double) * nc * (size_t)c->n, cudaMemcpyDeviceToHost, c->s0));
     CK(cudaStreamSynchronize(c->s0));
+    return KMF_OK;
+}
+// one derivative (d = 0: qx, 1: qy; host (4, n)) in the plane gradient layout
+int upload_grad(kmf_ctx *c, const double *h, int d, double *G)
+{
+    for (int p = 0; p < 2; p++)
+        if (int rc = upload_fields(c, h + 2 * (size_t)p * c->n, 2, G + 4 * (size_t)p * c->ld + d, 4, 2)) return rc;
+    return KMF_OK;
+}
+int download_grad(kmf_ctx *c, const double *G, int d, double *h)
+{
+    for (int p = 0; p < 2; p++)
+        if (int rc = download_fields(c, G + 4 * (size_t)p * c->ld + d, 2, h + 2 * (size_t)p * c->n, 4, 2)) return rc;
     return KMF_OK;
 }
 int reset_ctrl(kmf_ctx *c)
@@ -1260,7 +1280,7 @@ int kmf_op_q_derivatives(kmf_ctx *c, const double *q, int n_inner, const double 
     double *cur = c->GA.p, *nxt = c->GB.p;
     for (int it = 0; it < n_inner; it++) {
         CK(cudaMemsetAsync(&c->ctrl.p->resmax, 0, sizeof(unsigned long long), c->s0));
-        launch_sweep(c, c->s0, cur, nxt, c->ctrl.p, 0, 1 + it, 1);
+        launch_sweep(c, c->s0, cur, nxt, c->ctrl.p, 0, 1 + it, 1, it + 1 == n_inner);
         CK(cudaGetLastError());
         if (inner_residuals) {
             unsigned long long b = 0;
@@ -1270,8 +1290,8 @@ int kmf_op_q_derivatives(kmf_ctx *c, const double *q, int n_inner, const double 
         }
         std::swap(cur, nxt);
     }
-    if ((rc = download_fields(c, cur, 4, qx, 2))) return rc;
-    return download_fields(c, cur + 1, 4, qy, 2);
+    if ((rc = download_grad(c, cur, 0, qx))) return rc;  // plane layout (last sweep)
+    return download_grad(c, cur, 1, qy);
 }
 
 namespace {
@@ -1279,8 +1299,8 @@ int upload_flow(kmf_ctx *c, const double *q, const double *qx, const double *qy)
 {
     int rc = upload_fields(c, q, 4, c->q.p, 4, 1);
     if (rc) return rc;
-    if ((rc = upload_fields(c, qx, 4, c->GA.p, 2))) return rc;
-    return upload_fields(c, qy, 4, c->GA.p + 1, 2);
+    if ((rc = upload_grad(c, qx, 0, c->GA.p))) return rc;  // plane layout (flux / boundary input)
+    return upload_grad(c, qy, 1, c->GA.p);
 }
 }  // namespace
 

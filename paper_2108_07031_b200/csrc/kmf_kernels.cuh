@@ -6,8 +6,8 @@
 //     R[4], dt, flags; the fields the stencil gathers are packed per point
 //     instead: q as one 32-byte record q[4*i + c] (one 256-bit load per
 //     neighbour, qload), the q gradients G with the two derivatives of a
-//     component interleaved, (qx_c, qy_c) of slot i as one double2 at
-//     G2[c*ld + i] (gload), and (x, y) as one double2 (pxy);
+//     component interleaved (two layouts, see gload_cm / gload), and
+//     (x, y) as one double2 (pxy);
 //   * the full stencil is stored as sliced ELLPACK with slice height 32
 //     (one warp): neighbour slot s of point i lives at
 //     eoff[i/32] + s*32 + i%32, so the per-slot gathers of a warp are one
@@ -151,14 +151,66 @@ KMF_HD void qstore(double *__restrict__ q, int i, const double (&v)[4])
     reinterpret_cast<Q4 *>(q)[i] = r;
 }
 
-// (qx_k, qy_k) of slot i in the interleaved gradient layout
-KMF_HD double2 gload(const double *__restrict__ G, int ld, int k, int i)
+// Two gradient layouts.  The q-gradient kernels iterate in the
+// component-major one, (qx_k, qy_k) of slot i as one double2 at
+// G2[k*ld + i] (gload_cm / gstore_cm: four 128-bit loads per neighbour);
+// the LAST sweep of a stage writes the plane layout the flux and boundary
+// kernels read, two planes of 32-byte records (qx_2h, qy_2h, qx_2h+1,
+// qy_2h+1) at Q4 index h*ld + i (gload / gload_nc: two 256-bit loads per
+// neighbour).  Measured: the plane layout is 3 % faster for the flux and
+// 2-3 % slower for the sweeps (profiles/r1_summary.md).
+KMF_HD double2 gload_cm(const double *__restrict__ G, int ld, int k, int i)
 {
     return reinterpret_cast<const double2 *>(G)[k * ld + i];
 }
-KMF_HD void gstore(double *__restrict__ G, int ld, int k, int i, double gx, double gy)
+KMF_HD void gstore_cm(double *__restrict__ G, int ld, int k, int i, double gx, double gy)
 {
     reinterpret_cast<double2 *>(G)[k * ld + i] = make_double2(gx, gy);
+}
+KMF_HD double2 gload(const double *__restrict__ G, int ld, int k, int i)
+{
+    return reinterpret_cast<const double2 *>(G)[2 * ((k >> 1) * ld + i) + (k & 1)];
+}
+// components k0 .. k0+NC-1 (k0 even for NC >= 2) of slot i, plane layout
+template <int NC>
+KMF_HD void gload_nc(const double *__restrict__ G, int ld, int i, int k0, double (&gx)[NC], double (&gy)[NC])
+{
+    if (NC >= 2) {
+#pragma unroll
+        for (int h = 0; h < NC / 2; h++) {
+            const Q4 v = reinterpret_cast<const Q4 *>(G)[((k0 >> 1) + h) * ld + i];
+            gx[2 * h] = v.v[0];
+            gy[2 * h] = v.v[1];
+            gx[(2 * h + 1) % NC] = v.v[2];
+            gy[(2 * h + 1) % NC] = v.v[3];
+        }
+    } else {
+        const double2 v = gload(G, ld, k0, i);
+        gx[0] = v.x;
+        gy[0] = v.y;
+    }
+}
+// store components k0 .. k0+NC-1 of slot i in the plane (P) or the
+// component-major layout
+template <int NC, bool P>
+KMF_HD void gstore_nc(double *__restrict__ G, int ld, int i, int k0, const double (&gx)[NC], const double (&gy)[NC])
+{
+    if (P && NC >= 2) {
+#pragma unroll
+        for (int h = 0; h < NC / 2; h++) {
+            Q4 v;
+            v.v[0] = gx[2 * h];
+            v.v[1] = gy[2 * h];
+            v.v[2] = gx[(2 * h + 1) % NC];
+            v.v[3] = gy[(2 * h + 1) % NC];
+            reinterpret_cast<Q4 *>(G)[((k0 >> 1) + h) * ld + i] = v;
+        }
+    } else if (P) {
+        reinterpret_cast<double2 *>(G)[2 * ((k0 >> 1) * ld + i) + (k0 & 1)] = make_double2(gx[0], gy[0]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < NC; k++) gstore_cm(G, ld, k0 + k, i, gx[k], gy[k]);
+    }
 }
 
 // Programmatic dependent launch (kernels launched with the PDL attribute,
@@ -268,7 +320,7 @@ KMF_HD void qg_gather(QgSlot<NC, WG> &o, const DG &g, const double *__restrict__
 #pragma unroll
     for (int k = 0; k < NC; k++) {
         if (WG) {
-            const double2 v = gload(G, ld, k0 + k, j);
+            const double2 v = gload_cm(G, ld, k0 + k, j);
             o.gx[k] = v.x;
             o.gy[k] = v.y;
         }
@@ -383,14 +435,14 @@ __global__ void __launch_bounds__(TB, (MB ? MB : (NC == 4 && TB == 128 ? 8 : 0))
     const double sxx = g.fsum[i], sxy = g.fsum[ld + i], syy = g.fsum[2 * ld + i], det = g.fsum[3 * ld + i];
 #pragma unroll
     for (int k = 0; k < NC; k++) {
-        gstore(G, ld, k0 + k, i, DIV(SUB(MUL(syy, sx[k]), MUL(sxy, sy[k])), det),
-               DIV(SUB(MUL(sxx, sy[k]), MUL(sxy, sx[k])), det));
+        gstore_cm(G, ld, k0 + k, i, DIV(SUB(MUL(syy, sx[k]), MUL(sxy, sy[k])), det),
+                  DIV(SUB(MUL(sxx, sy[k]), MUL(sxy, sx[k])), det));
     }
 }
 
 // lsq.py:214-227 one Jacobi sweep of the defect-corrected gradients --
 // bitwise.  With want_res the max |new - old| (lsq.py:238-243) is reduced.
-template <bool XY, int NC, int U, int TB = kTB, int ST = 0, int MB = 0>
+template <bool XY, int NC, int U, int TB = kTB, int ST = 0, int MB = 0, bool OUTP = false>
 __global__ void __launch_bounds__(TB, MB) k_sweep(DG g, const double *__restrict__ q,
                                                const double *__restrict__ Gin, double *__restrict__ Gout,
                                                Ctrl *c, int stage, int slot, int want_res)
@@ -414,7 +466,7 @@ __global__ void __launch_bounds__(TB, MB) k_sweep(DG g, const double *__restrict
         qload_nc<NC>(q, i, k0, qi);
 #pragma unroll
         for (int k = 0; k < NC; k++) {
-            const double2 v = gload(Gin, ld, k0 + k, i);
+            const double2 v = gload_cm(Gin, ld, k0 + k, i);
             gxi[k] = v.x;
             gyi[k] = v.y;
             sx[k] = 0.0;
@@ -455,7 +507,7 @@ __global__ void __launch_bounds__(TB, MB) k_sweep(DG g, const double *__restrict
 #pragma unroll
                 for (int k = 0; k < NC; k++) {
                     qj[u][k] = q[4 * jj[u] + k0 + k];
-                    const double2 v = gload(Gin, ld, k0 + k, jj[u]);
+                    const double2 v = gload_cm(Gin, ld, k0 + k, jj[u]);
                     gxj[u][k] = v.x;
                     gyj[u][k] = v.y;
                 }
@@ -481,11 +533,16 @@ __global__ void __launch_bounds__(TB, MB) k_sweep(DG g, const double *__restrict
         }
         const double sxx = g.fsum[i], sxy = g.fsum[ld + i], syy = g.fsum[2 * ld + i],
                      det = g.fsum[3 * ld + i];
+        double gxn[NC], gyn[NC];
 #pragma unroll
         for (int k = 0; k < NC; k++) {
-            double nx_ = DIV(SUB(MUL(syy, sx[k]), MUL(sxy, sy[k])), det);
-            double ny_ = DIV(SUB(MUL(sxx, sy[k]), MUL(sxy, sx[k])), det);
-            gstore(Gout, ld, k0 + k, i, nx_, ny_);
+            gxn[k] = DIV(SUB(MUL(syy, sx[k]), MUL(sxy, sy[k])), det);
+            gyn[k] = DIV(SUB(MUL(sxx, sy[k]), MUL(sxy, sx[k])), det);
+        }
+        gstore_nc<NC, OUTP>(Gout, ld, i, k0, gxn, gyn);  // OUTP: the stage's last sweep
+#pragma unroll
+        for (int k = 0; k < NC; k++) {
+            const double nx_ = gxn[k], ny_ = gyn[k];
             if (want_res) {
                 rmax = fmax(rmax, fabs(nx_ - gxi[k]));
                 rmax = fmax(rmax, fabs(ny_ - gyi[k]));

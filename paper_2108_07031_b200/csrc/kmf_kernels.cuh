@@ -1087,7 +1087,6 @@ __global__ void __launch_bounds__(kTB) k_update(DG g, double *__restrict__ Uo, d
         for (int k = 0; k < 4; k++) out[k * ld + i] = un[k];
         double qq[4];
         p2q(rho, u1, u2, p, gamma, qq);
-#pragma unroll
         qstore(q, i, qq);
         if (STAGE == 4) {
             dt[i] = timestep(rho, u1, u2, p, gamma, cfl, g.dmin[i]);
@@ -1246,7 +1245,6 @@ __global__ void k_refresh(DG g, const double *__restrict__ Uo, double *__restric
     for (int k = 0; k < 4; k++) u[k] = Uo[k * ld + i];
     u2p(u, gamma, rho, u1, u2, p);
     p2q(rho, u1, u2, p, gamma, qq);
-#pragma unroll
     qstore(q, i, qq);
     dt[i] = timestep(rho, u1, u2, p, gamma, cfl, g.dmin[i]);
 }

@@ -923,8 +923,6 @@ int get_graph(kmf_ctx *c, const kmf_params *p, int unroll, double *hist, int his
     return KMF_OK;
 }
 
-kmf_ctx *g_default_ctx = nullptr;
-
 void record_error(kmf_ctx *c, int code, int iteration, int stage, int context, long long count, const char *msg)
 {
     if (!c) return;
@@ -1084,13 +1082,11 @@ int kmf_run(kmf_ctx *c, const kmf_params *p, int n_iter, double *history, int *i
     for (double &s : c->stage_sec) s = 0.0;
 
     const int skip = std::max(0, std::min(p->timing_skip, n_iter));
-    int done = 0;
     if (p->instrument) {
         // timed iterations launch eagerly with events around every group
         for (int it = 0; it < n_iter; it++) {
             enqueue_iteration(c, p, c->history.p, 1, n_iter, it >= skip ? ITER_INSTRUMENT : ITER_PLAIN);
         }
-        done = n_iter;
     } else {
         const int U = 8;
         int full = n_iter / U, rest = n_iter % U;
@@ -1104,9 +1100,7 @@ int kmf_run(kmf_ctx *c, const kmf_params *p, int n_iter, double *history, int *i
             if (rc) return rc;
             for (int k = 0; k < rest; k++) CK(cudaGraphLaunch(c->exec1, c->s0));
         }
-        done = n_iter;
     }
-    (void)done;
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(c->s0));
     Ctrl fin;

@@ -161,6 +161,10 @@ def test_cli_solve_and_bench_outputs(gpu, tmp_path, capsys):
     assert len(list(csv.DictReader(open(out / "history.csv")))) == 5
     assert (out / "wall.csv").read_text().startswith("x,y,cp\n")
     assert "iters = 5" in (out / "config.txt").read_text()
+    o1 = tmp_path / "run1"
+    assert main(["solve", "--grid", str(grid), "--out", str(o1), "--iters", "3", "--order", "1"]) == 0
+    assert "order = 1" in (o1 / "config.txt").read_text()
+    assert len(list(csv.DictReader(open(o1 / "history.csv")))) == 3
     b = tmp_path / "bench"
     assert main(["bench", "--grid", str(grid), "--out", str(b), "--iters", "4", "--warmup", "1",
                  "--modes", "fused,split4"]) == 0

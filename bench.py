@@ -1,7 +1,11 @@
 #!/usr/bin/env python
 """Benchmark: q-LSKUM outer iterations on B200 (driver contract, one JSON line).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c5]
+
+With --gpus N > 1 and no torchrun environment, bench.py launches itself
+under torchrun with N ranks on this node (one GPU per rank); under torchrun
+WORLD_SIZE must equal N.
 
 A step is one outer iteration of the solver (local time step + 4 SSP-RK
 stages of q-variables, q-derivatives with 3 inner sweeps, flux residual with
@@ -10,7 +14,9 @@ NACA 0012 cloud.  The default workload is BASELINE.json configs[4], the
 configuration the metric's 1/2/4/8-B200 sweep and the paper's best
 published RDP (3.41e-8 s, C++ on V100) are quoted on:
 39,992,976 points, M 0.63, AoA 2 deg, second order, n_inner 3, fused; it
-fits one B200 (~24 GB).  --config c2 is configs[1] (160K points).
+fits one B200 (~24 GB).  --config c1..c4 select the other BASELINE configs
+(c1 = configs[0] in the reference's own second-order scheme; c1o1 the same
+cloud in the first-order scheme configs[0] names, SolverConfig(order=1)).
 
 Reported (ours):
   value          point-iterations/s with the state resident in HBM, each step
@@ -24,6 +30,7 @@ Reported (ours):
                  HBM (MEASURED_PEAKS.json) -- it is FP64-bound, so
                  roofline_fp64 reports executed DP-pipe instructions against
                  the FP64 peak measured in the same run (DFMA probe);
+                 roofline_qgrad the first-order and sweep kernels against HBM;
   cpu_baseline   the CPU oracle (C restatement of the reference, OpenMP over
                  all host cores) on a bounded sample: whole iterations of the
                  whole cloud up to 2.5M points, a geometric slab (owned points
@@ -52,14 +59,17 @@ sys.path.insert(0, str(ROOT))
 
 CONFIGS = {
     # name: (chord_points, layers, growth, mach, aoa, description)
-    "c1": (400, 100, 1.06, 0.63, 2.0, "NACA0012 40K (400x100, g=1.06) M0.63 AoA2 first order (qx = qy = 0)"),
+    "c1": (400, 100, 1.06, 0.63, 2.0, "NACA0012 40K (400x100, g=1.06) M0.63 AoA2 second order n_inner=3"),
+    "c1o1": (400, 100, 1.06, 0.63, 2.0, "NACA0012 40K (400x100, g=1.06) M0.63 AoA2 first order (qx = qy = 0)"),
     "c2": (800, 200, 1.03, 0.63, 2.0, "NACA0012 160K (800x200, g=1.03) M0.63 AoA2 second order n_inner=3"),
     "c3": (3160, 790, 1.00734, 0.85, 1.0, "NACA0012 2.5M (3160x790, g=1.00734) M0.85 AoA1 second order"),
     "c4": (6324, 1581, 1.003647, 0.63, 2.0, "NACA0012 10M (6324x1581, g=1.003647) M0.63 AoA2 second order"),
     "c5": (12648, 3162, 1.001821, 0.63, 2.0, "NACA0012 40M (12648x3162, g=1.001821) M0.63 AoA2 second order"),
 }
-# BASELINE configs[0] is the first-order scheme (SolverConfig.order = 1)
-ORDER = {"c1": 1}
+# BASELINE configs[0] names the first-order scheme; the reference's solve()
+# has none, so c1 runs the reference's second-order scheme
+# and c1o1 the first-order extension (SolverConfig.order = 1)
+ORDER = {"c1o1": 1}
 # best published RDP for this metric, C++ optimised on V100,
 # NACA 0012 40M points -> point-iterations/s
 PUBLISHED = {"c5": 1.0 / 3.41e-8}
@@ -67,9 +77,11 @@ PUBLISHED = {"c5": 1.0 / 3.41e-8}
 CPU_SLAB_POINTS = int(os.environ.get("KMF_CPU_SLAB", 1_250_000))
 METRIC = "point-iterations/sec (RDP = 1/value s/point/iter), NACA0012 q-LSKUM"
 UNIT = "point-iterations/s"
-# algorithmic work of flux_residual interior per point-stage
+# algorithmic bytes per point of one launch of the interior
+# flux, first-order q-gradient and Jacobi sweep kernels
 FLUX_BYTES_PER_POINT = 337
-FLUX_DP_OPS_PER_POINT = 13214
+FO_BYTES_PER_POINT = 208
+SWEEP_BYTES_PER_POINT = 272
 # algorithmic bytes / DP ops of one whole point-iteration
 # (timestep, 4 x [q, first order, 3 sweeps, flux, update], residue)
 ITER_BYTES_PER_POINT = 6440
@@ -83,6 +95,25 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return ws, rank, local
+
+
+def self_launch(args) -> int:
+    """--gpus N > 1 outside torchrun: relaunch this script under torchrun
+    with N ranks on this node (127.0.0.1 rendezvous); rank 0 prints the
+    JSON line.  NCCL's INFO log (communicator size and transport per rank)
+    goes to stderr so stdout keeps the one JSON line."""
+    import socket
+
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve())] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    return subprocess.call(cmd, env=env)
 
 
 def dist_init(ws):
@@ -258,6 +289,20 @@ def cpu_baseline(conn, cfg, init, target_s=12.0):
                       f"over {threads} threads"}
 
 
+def qgrad_roofline(n_pts, fo_s, sweep_s, peak, peak_kind, share):
+    """First-order and sweep kernels against HBM: SURVEY 8(d)'s algorithmic
+    bytes per point (208 / 272) x the points one launch covers, divided by
+    the launch's average duration (event nodes on its stream)."""
+    fo = FO_BYTES_PER_POINT * n_pts / fo_s / 1e9
+    sw = SWEEP_BYTES_PER_POINT * n_pts / sweep_s / 1e9
+    return {"bound": "hbm", "unit": "GB/s", "peak": peak, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+            "first_order": {"kernel": "k_first_order", "bytes_per_point": FO_BYTES_PER_POINT, "launch_us": fo_s * 1e6,
+                            "achieved": fo, "frac": fo / peak},
+            "sweep": {"kernel": "k_sweep", "bytes_per_point": SWEEP_BYTES_PER_POINT, "launch_us": sweep_s * 1e6,
+                      "achieved": sw, "frac": sw / peak},
+            "share_of_step": share}
+
+
 def measured_peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -265,16 +310,17 @@ def measured_peaks():
     return {"hbm_gbs": 6650.0}, "fallback"
 
 
-def roofline_fp64(counts, n_cloud, n_flux, launch_s, dfma_rate, algo_ops, probe_tflops):
+def roofline_fp64(counts, n_cloud, n_flux, launch_s, dfma_rate, probe_tflops):
     """The binding roofline of the flux kernel: executed DP-pipe thread
-    instructions (DFMA + DMUL + DADD, ncu count of this build) per second
-    against the DFMA peak measured in the same run.  The SURVEY's
-    algorithmic count (13,214 DP ops/point with libdevice-cost
-    transcendentals) is reported beside it: the kernel executes fewer
-    because of the shared decodes and lean transcendentals."""
+    instructions (DFMA + DMUL + DADD, ncu count of this build, per point of
+    the cloud) per second against the DFMA instruction peak measured in the
+    same run.  (SURVEY 8(d)'s 13,214 "DP ops"/point weighs each libdevice
+    transcendental by its instruction count -- exp 18, erf 25, log 28,
+    div/sqrt 10 -- which this kernel does not execute: its lean
+    exp/erf/rcp/rsqrt and shared per-state constants take 4.7K DP-pipe
+    instructions per point, so that count is not a rate against the pipe.)"""
     out = {"bound": "fp64", "unit": "T DP-pipe thread-inst/s", "peak": dfma_rate,
-           "peak_source": f"DFMA probe in this run: {probe_tflops:.2f} TFLOP/s = {dfma_rate:.2f} T DFMA/s",
-           "algorithmic_ops_per_point": FLUX_DP_OPS_PER_POINT, "algorithmic_achieved": algo_ops}
+           "peak_source": f"DFMA probe in this run: {probe_tflops:.2f} TFLOP/s = {dfma_rate:.2f} T DFMA/s"}
     if counts:
         dp_pt = counts["dp_thread_inst_per_launch"] / n_cloud  # counted single-GPU over the whole cloud
         ach = dp_pt * n_flux / launch_s / 1e12
@@ -288,6 +334,9 @@ def roofline_fp64(counts, n_cloud, n_flux, launch_s, dfma_rate, algo_ops, probe_
 
 def run_ours(args):
     ws, rank, local = dist_env()
+    if ws > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     dist = dist_init(ws)
     from paper_2108_07031_b200 import _lib
     from paper_2108_07031_b200._device import DeviceConnectivity
@@ -305,8 +354,11 @@ def run_ours(args):
         # all-reduce inside the iteration graph (paper_2108_07031_b200/dist.py)
         from paper_2108_07031_b200.dist import RankSolver
 
-        rs = RankSolver(conn, dist, n_inner=cfg.n_inner, device=local)
+        rs = RankSolver(conn, dist, n_inner=cfg.n_inner, device=local, scheme=args.partition)
         dev = rs.dev
+        part = rs.rp.part
+        print(f"[bench] rank {rank}: {part.n_owned} owned + {part.global_ids.size - part.n_owned} halo points "
+              f"({args.partition}), interior pass {part.interior_end[-1]} points", file=sys.stderr, flush=True)
         local_init = np.ascontiguousarray(init.as_array()[:, rs.rp.part.global_ids])
     else:
         t = time.perf_counter()
@@ -322,20 +374,24 @@ def run_ours(args):
     dev.set_state(local_init)
     W, K = max(args.warmup, 0), args.steps
     step_ms = np.zeros(max(K, W, 1))
-    flux_ms = np.zeros_like(step_ms)
+    kern_ms = np.zeros((step_ms.size, _lib.BENCH_KERNELS))  # interior flux, first order, sweeps
     lps = C.c_int(0)
     if W:
         _lib.check(L.kmf_bench_steps(dev.handle, C.byref(params), W, L2_FLUSH_BYTES, _lib.dptr(step_ms),
-                                     _lib.dptr(flux_ms), C.byref(lps)), "warm-up")
+                                     _lib.dptr(kern_ms), C.byref(lps)), "warm-up")
     barrier(dist)
     with Clocks(local) as clk:
         _lib.check(L.kmf_bench_steps(dev.handle, C.byref(params), K, L2_FLUSH_BYTES, _lib.dptr(step_ms),
-                                     _lib.dptr(flux_ms), C.byref(lps)), "timed steps")
+                                     _lib.dptr(kern_ms), C.byref(lps)), "timed steps")
     barrier(dist)
     total_s = allreduce_max(dist, float(step_ms[:K].sum()) * 1e-3)
     value = n * K / total_s  # every step advances all n points once (strong scaling over ranks)
-    flux_launch_s = float(flux_ms[:K].sum()) * 1e-3 / (4 * K)
-    stage_share = float(flux_ms[:K].sum() / step_ms[:K].sum())
+    kern_s = kern_ms[:K].sum(axis=0) * 1e-3
+    n_sweeps = cfg.n_inner if cfg.order == 2 else 0
+    flux_launch_s = float(kern_s[0]) / (4 * K)
+    fo_launch_s = float(kern_s[1]) / (4 * K) if n_sweeps else 0.0
+    sweep_launch_s = float(kern_s[2]) / (4 * n_sweeps * K) if n_sweeps else 0.0
+    stage_share = float(kern_s[0] / (step_ms[:K].sum() * 1e-3))
 
     # ---- end to end through the C ABI with pinned host buffers ------------
     host_in = _lib.pinned((4, n_local))
@@ -369,7 +425,7 @@ def run_ours(args):
     n_flux = rs.rp.part.n_owned if ws > 1 else n  # points one flux launch covers
     achieved_gbs = FLUX_BYTES_PER_POINT * n_flux / flux_launch_s / 1e9
     dfma_rate = peak_fp64.value / 2.0  # DP-pipe instructions/s (TFLOP/s / 2)
-    achieved_ops = FLUX_DP_OPS_PER_POINT * n_flux / flux_launch_s / 1e12
+    n_grad = (rs.rp.part.layer_counts[-1] if ws > 1 else n)  # q-gradient launches cover owned + halo layers
     # executed DP-pipe instructions and DRAM traffic of one flux launch,
     # measured once per kernel build by ncu (tools/flux_counts.sh)
     traffic, counts = None, None
@@ -396,7 +452,8 @@ def run_ours(args):
         "config": {"workload": CONFIGS[args.config][5], "config_key": args.config, "n_points": n,
                    "n_edges": int(conn.full.idx.size), "n_inner": cfg.n_inner, "order": cfg.order, "mode": cfg.mode,
                    "l2": "flushed between timed steps (256 MiB memset on the solver stream)",
-                   "parallelism": f"partition x{ws} (deep halo, NCCL)" if ws > 1 else "single GPU",
+                   "parallelism": (f"partition x{ws} ({args.partition}, deep halo, NCCL halo exchange overlapped "
+                                   "with the interior pass)") if ws > 1 else "single GPU",
                    "point_order": args.order},
         "rdp_s_per_point_iter": 1.0 / value,
         "e2e": e2e,
@@ -413,7 +470,9 @@ def run_ours(args):
             "frac": iter_bytes * value / ws / 1e9 / hbm_peak,
             "note": "whole outer iteration against the HBM roofline implied by SURVEY 8(d)'s 6.44 KB per "
                     "point-iteration (north star), per GPU"},
-        "roofline_fp64": roofline_fp64(counts, n, n_flux, flux_launch_s, dfma_rate, achieved_ops, peak_fp64.value),
+        "roofline_fp64": roofline_fp64(counts, n, n_flux, flux_launch_s, dfma_rate, peak_fp64.value),
+        "roofline_qgrad": qgrad_roofline(n_grad, fo_launch_s, sweep_launch_s, hbm_peak, peak_kind, float(
+            kern_s[1] + kern_s[2]) / (step_ms[:K].sum() * 1e-3)) if n_sweeps else None,
         "clocks": clk.summary(),
     }
     if not args.no_cpu_baseline and ws == 1:
@@ -444,7 +503,8 @@ def run_reference(args):
     sec = time.perf_counter() - t
     value = npts * K / sec
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": W,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": K,
+        "warmup": W,
         "ms_per_step": 1e3 * sec / K, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": value / PUBLISHED[args.config] if args.config in PUBLISHED else None,
         "dtype": "f64", "data": "synthetic (procedurally generated NACA 0012 O-cloud)",
@@ -467,11 +527,18 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", choices=tuple(CONFIGS), default="c5",
                     help="c5 (default): 40M points, BASELINE configs[4]; c2: 160K, configs[1]")
+    ap.add_argument("--partition", choices=("sectors", "bands"), default="sectors",
+                    help="ownership scheme of the multi-GPU partition (partition.py)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--order", choices=("natural", "hilbert", "ringtile2", "ringtile4", "ringtile8"),
                     default=os.environ.get("KMF_ORDER", "natural"),
                     help="device point order (bitwise neutral, locality only)")
     args = ap.parse_args()
+    ws = os.environ.get("WORLD_SIZE")
+    if ws is None and args.gpus > 1 and args.impl == "ours":
+        sys.exit(self_launch(args))
+    if ws is not None and int(ws) != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws} (launch N ranks for --gpus N)")
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -216,19 +216,26 @@ const char *kmf_strerror(void);
 
 /* ---- multi-GPU partition (paper_2108_07031_b200/partition.py) ------------ *
  * A partitioned context holds its rank's owned points (local slots
- * 0..n_owned-1) followed by an (n_inner+2)-layer halo.  Flux, boundary and
- * update launches cover the owned points; the q-gradient launches the whole
- * local set; after every stage the halo q is refreshed from its owners;
- * the residue limbs are summed across ranks before the iteration close, so
- * every rank's arithmetic -- and the history -- is bitwise the single-GPU
- * one.  send_slots/recv_slots are concatenated per peer (peer_ranks order):
- * owned local slots to send, halo local slots to fill. */
-int kmf_set_partition(kmf_ctx *ctx, int64_t n_owned, int64_t n_global, int rank, int nranks, int npeers,
-                      const int *peer_ranks, const int64_t *send_counts, const int64_t *send_slots,
-                      const int64_t *recv_counts, const int64_t *recv_slots);
-/* NCCL transport (one process per GPU): halo send/recv and the limb
- * all-reduce are captured in the iteration graph; kmf_run then works as for
- * a single domain.  libnccl.so.2 is loaded at run time. */
+ * 0..n_owned-1, ordered by DEPTH = hop distance to the nearest halo slot,
+ * deepest first) followed by `depth` halo layers L1..Ldepth (depth >=
+ * n_inner + 2).  layer_end[k] = n_owned + |L1..Lk| (k = 0..depth);
+ * interior_end[k] = owned slots at depth >= k (k = 0..depth+1).  Per stage
+ * each kernel runs an INTERIOR pass over the owned slots deep enough not to
+ * read this stage's halo data -- overlapping the halo exchange -- and a BAND
+ * pass over the rest after it; flux, boundary and update cover the owned
+ * points; the residue limbs are summed across ranks before the iteration
+ * close, so every rank's arithmetic -- and the history -- is bitwise the
+ * single-GPU one.  send_slots/recv_slots are concatenated per peer
+ * (peer_ranks order): owned local slots to send, halo local slots to fill. */
+int kmf_set_partition(kmf_ctx *ctx, int64_t n_owned, int64_t n_global, int rank, int nranks, int depth,
+                      const int64_t *layer_end, const int64_t *interior_end, int npeers, const int *peer_ranks,
+                      const int64_t *send_counts, const int64_t *send_slots, const int64_t *recv_counts,
+                      const int64_t *recv_slots);
+/* NCCL transport (one process per GPU): inside the iteration graph the halo
+ * exchange (pack, grouped send/recv per peer, unpack) of every stage runs on
+ * a forked stream concurrently with the next stage's interior pass, and the
+ * limb all-reduce precedes the iteration close; kmf_run then works as for a
+ * single domain.  libnccl.so.2 is loaded at run time. */
 int kmf_nccl_get_unique_id(void *out128);
 int kmf_nccl_init(kmf_ctx *ctx, const void *id128, int rank, int nranks);
 /* one process driving all ranks' contexts (same or peer GPUs): halo moves
@@ -238,18 +245,29 @@ int kmf_run_group(kmf_ctx **ctxs, int nctx, const kmf_params *p, int n_iter, dou
 
 /* ---- measurement support (bench.py) -------------------------------------- */
 
-/* n_steps outer iterations, each one CUDA-graph launch bracketed by CUDA
- * events on the context stream (step_ms[i]); a flush_bytes memset between
- * steps evicts L2 outside the timed region; flux_ms[i] sums the four
- * interior flux_residual launches of step i, timed on their own stream. */
+/* 2 x n_steps outer iterations.  First n_steps plain CUDA-graph launches of
+ * one iteration, each bracketed by CUDA events on the context stream
+ * (step_ms[i]); a flush_bytes memset between steps evicts L2 outside the
+ * timed region.  Then n_steps launches of the same iteration with event
+ * nodes around its launch groups: kernel_ms[KMF_BENCH_KERNELS*i+k] sums
+ * step i's launches of kernel class k (0 interior flux_residual, 1
+ * first-order q-gradients, 2 Jacobi sweeps), timed on their own stream;
+ * *launches_per_step counts this library's kernel launches per iteration. */
+#define KMF_BENCH_KERNELS 3
 int kmf_bench_steps(kmf_ctx *ctx, const kmf_params *p, int n_steps, int64_t flush_bytes, double *step_ms,
-                    double *flux_ms, int *launches_per_step);
+                    double *kernel_ms, int *launches_per_step);
 /* measured FP64 (DFMA) pipe peak of the current device, TFLOP/s */
 int kmf_fp64_peak(double *tflops);
 /* device transcendentals of the flux path on host inputs (accuracy tests):
- * which 0 exp, 1 erf, 2 reciprocal, 3 reciprocal square root, 4 table exp,
- * 5 table exp without clamps (arguments <= 0) */
+ * which 0 and 4 table exp, 1 erf (the kernel's branch-free |s| < 1
+ * polynomial and tail), 2 reciprocal, 3 reciprocal square root, 5 table exp
+ * without clamps (arguments <= 0) */
 int kmf_fastmath_probe(int64_t n, const double *x, int which, double *out);
+/* the flux kernel's edge-state path on q vectors (4, n) (test probe of the
+ * tolerance arithmetic, state.py:141-163 + kinetics.py:71-106): its decode
+ * -> prims (4, n) (p = rho / (2 beta)) and its four split fluxes x+, x-, y+,
+ * y- -> flux (16, n), family f in rows 4f..4f+3 */
+int kmf_probe_edge_state(int64_t n, const double *q, double gamma, double *prims, double *flux);
 /* pinned host memory for host-buffer (end-to-end) transfers */
 void *kmf_host_alloc(int64_t bytes);
 void kmf_host_free(void *p);

@@ -134,7 +134,7 @@ class DeviceConnectivity:
         if rc == _lib.KMF_EPOSITIVITY:
             info = _lib.ErrorInfo()
             _lib.lib().kmf_last_error(self._h, C.byref(info))
-            self.raise_positivity(info.context, info.stage, which=params.n_inner & 1, mode=params.mode,
+            self.raise_positivity(info.context, info.stage, which=_lib.DIAG_LAST_RUN, mode=params.mode,
                                   prefix=f"iteration {info.iteration}: ", gamma=params.gamma)
         _lib.check(rc, "kmf_run")
         return hist[: done.value].copy(), done.value, bool(conv.value)

@@ -16,6 +16,8 @@ import numpy as np
 LIB_PATH = Path(__file__).resolve().parent / "libkmf_b200.so"
 
 KMF_OK, KMF_EPOSITIVITY, KMF_EINVAL, KMF_ECUDA, KMF_ENCCL = 0, 1, 2, 3, 4
+BENCH_KERNELS = 3  # KMF_BENCH_KERNELS: interior flux, first order, sweeps
+DIAG_LAST_RUN = 2  # kmf_diag_* `which`: the final gradients of the last run
 
 (CTX_NONE, CTX_INITIAL, CTX_FLUX_XP, CTX_FLUX_XM, CTX_FLUX_YP, CTX_FLUX_YM,
  CTX_WALL_TANGENT, CTX_WALL_NORMAL, CTX_OUTER_TANGENT, CTX_OUTER_NORMAL,
@@ -117,8 +119,9 @@ def lib():
         "kmf_bench_steps": (C.c_int, [vp, C.POINTER(Params), C.c_int, C.c_int64, _dp, _dp, C.POINTER(C.c_int)]),
         "kmf_fp64_peak": (C.c_int, [_dp]),
         "kmf_fastmath_probe": (C.c_int, [C.c_int64, _dp, C.c_int, _dp]),
-        "kmf_set_partition": (C.c_int, [vp, C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int),
-                                        _i64p, _i64p, _i64p, _i64p]),
+        "kmf_probe_edge_state": (C.c_int, [C.c_int64, _dp, C.c_double, _dp, _dp]),
+        "kmf_set_partition": (C.c_int, [vp, C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_int, _i64p, _i64p, C.c_int,
+                                        C.POINTER(C.c_int), _i64p, _i64p, _i64p, _i64p]),
         "kmf_nccl_get_unique_id": (C.c_int, [C.c_void_p]),
         "kmf_nccl_init": (C.c_int, [vp, C.c_void_p, C.c_int, C.c_int]),
         "kmf_run_group": (C.c_int, [C.POINTER(vp), C.c_int, C.POINTER(Params), C.c_int, _dp, C.POINTER(C.c_int),
@@ -142,6 +145,7 @@ EXPORTED = (
     "kmf_op_boundary", "kmf_op_primitives_to_q", "kmf_op_q_to_primitives",
     "kmf_op_primitives_to_conserved", "kmf_op_conserved_to_primitives", "kmf_op_split_flux",
     "kmf_op_full_flux", "kmf_op_state_update", "kmf_op_residue", "kmf_bench_steps", "kmf_fp64_peak", "kmf_fastmath_probe",
+    "kmf_probe_edge_state",
     "kmf_host_alloc", "kmf_host_free", "kmf_set_partition", "kmf_nccl_get_unique_id", "kmf_nccl_init",
     "kmf_run_group",
 )

@@ -4,7 +4,7 @@
 // arch=compute_100a,code=sm_100a -O3 -lineinfo -fmad=false).
 #include "../../include/kmf_b200.h"
 #include "kmf_kernels.cuh"
-#include "kmf_flux3.cuh"
+#include "kmf_flux.cuh"
 
 #include <cuda_runtime.h>
 #include <dlfcn.h>
@@ -18,6 +18,8 @@
 #include <cstring>
 #include <string>
 #include <vector>
+
+
 
 using namespace kmf;
 
@@ -74,9 +76,46 @@ struct DBuf {
 
 struct GraphKey {
     double gamma, cfl, fs[4], tol;
-    int n_inner, mode, unroll, cap, base;
+    int n_inner, mode, unroll, cap, base, how;
     const void *hist;
     bool operator==(const GraphKey &o) const { return std::memcmp(this, &o, sizeof o) == 0; }
+};
+
+// Timed launch groups inside a captured iteration graph: external event
+// record nodes around each group, read back after the replay.
+enum {
+    KC_QGRAD = 0,   // instrument: q_derivatives (first order + sweeps)
+    KC_FLUXBND,     // instrument: flux_residual (interior flux + boundary closure)
+    KC_UPDATE,      // instrument: state_update (+ fused q_variables, timestep, residue)
+    KC_FLUX,        // bench: interior flux kernel launches
+    KC_FO,          // bench: first-order q-gradient launches
+    KC_SWEEP,       // bench: Jacobi sweep launches
+    KC_N
+};
+
+struct EvPair {
+    int cls;
+    cudaEvent_t a, b;
+};
+
+// One instantiated iteration graph (`unroll` outer iterations) and the
+// event pairs captured into it.
+struct Graph {
+    cudaGraphExec_t exec = nullptr;
+    GraphKey key{};
+    std::vector<EvPair> ev;
+    int launches = 0;  // kernels of this library per captured iteration
+    void reset()
+    {
+        if (exec) cudaGraphExecDestroy(exec);
+        exec = nullptr;
+        for (auto &e : ev) {
+            cudaEventDestroy(e.a);
+            cudaEventDestroy(e.b);
+        }
+        ev.clear();
+    }
+    ~Graph() { reset(); }
 };
 
 }  // namespace
@@ -85,17 +124,10 @@ struct kmf_ctx {
     int device = 0;
     int n = 0, ld = 0;
     bool xy = true;  // offsets recomputed from coordinates
-    int qg_nc = 2;   // q-gradient components per thread (KMF_QG_NC)
-    int qg_unroll = 1;  // q-gradient edge unroll (KMF_QG_UNROLL)
-    int qg_tb = 128;    // q-gradient block size (KMF_QG_TB)
-    bool pdl = false;   // programmatic dependent launch in the iteration graph (KMF_PDL)
-    int qg_minb = 1;    // min resident blocks of the staged 256-thread q-gradient kernels (KMF_QG_MINB)
-    int qg_stage = 0;   // stage ELL index slices in shared memory (KMF_QG_STAGE)
-    int flux_impl = 3;  // interior flux kernel shape (KMF_FLUX_IMPL): 1 per-flux, 2 pair, 3 lock-step
-    int flux_minb = 3;  // interior flux blocks per SM (KMF_FLUX_MINB)
+    int qg_nc = 2;   // q-gradient components per thread (4 above 100K points)
     bool has_perm = false;
-    cudaStream_t s0 = nullptr, s1 = nullptr;
-    cudaEvent_t fork = nullptr, join = nullptr;
+    cudaStream_t s0 = nullptr, s1 = nullptr, s2 = nullptr;  // solver, boundary branch, halo exchange
+    cudaEvent_t fork = nullptr, join = nullptr, xfork = nullptr, xjoin = nullptr;
 
     // geometry
     DBuf<double> x, y, pxy, dmin, fsum, fcoef, edx, edy;
@@ -119,33 +151,40 @@ struct kmf_ctx {
     bool have_state = false, pending_init = false;
     double state_gamma = 1.4;
 
-    // graphs
-    cudaGraphExec_t exec1 = nullptr, execU = nullptr;
-    GraphKey key1{}, keyU{};
+    // graphs: 1 iteration, 8 iterations, bench (1 iteration with kernel events)
+    Graph g1, gU, gB;
+    std::vector<EvPair> *cap_ev = nullptr;  // event list of the graph being captured
+    int nlaunch = 0;                        // kernel launches enqueued (counted while capturing)
+    int cap_how = 0;
 
     // instrumentation
     double stage_sec[6] = {0, 0, 0, 0, 0, 0};
-    cudaEvent_t ev[18] = {};
-    cudaEvent_t evb[8] = {};   // bench: around the 4 interior flux launches
-    cudaEvent_t evs[2] = {};   // bench: around one step
-    cudaGraphExec_t execB = nullptr;
-    GraphKey keyB{};
+    cudaEvent_t evs[2] = {};  // bench: around one step
     DBuf<unsigned char> flush;
 
     // last error
     kmf_error_info err{};
     std::vector<long long> err_idx;
-    int last_G = 0;  // which gradient buffer holds the final gradients of the last stage
+    const double *G_last = nullptr;  // final gradients of the last stage enqueued (diagnostics)
 
-    // partition (multi-GPU, partition.py): owned points first, halo after
+    // partition (multi-GPU, partition.py): owned points first, ordered by
+    // depth (hop distance to the nearest halo slot, deepest first), then the
+    // halo layers 1..depth
     bool dist_on = false;
-    int n_owned = 0, rank = 0, nranks = 1;
+    int n_owned = 0, rank = 0, nranks = 1, depth = 0;
     long long n_global = 0;
+    std::vector<int> layer_end;     // [k]: n_owned + |L1..Lk|, k = 0..depth
+    std::vector<int> interior_end;  // [k]: owned slots at depth >= k, k = 0..depth+1
     std::vector<int> peer_rank;
     std::vector<long long> send_off, send_cnt, recv_off, recv_cnt;  // points, per peer
     long long send_total = 0, recv_total = 0;
     DBuf<int> ps_slot, ps_base, ps_stride, pr_slot, pr_base, pr_stride;
     DBuf<double> sendbuf, recvbuf;
+    // one gradient buffer per level (first order, sweep 1..): the band pass
+    // reads lower levels at slots the interior pass already advanced, so the
+    // single-domain ping-pong (GA, GB) would have been overwritten
+    static constexpr int kMaxLevels = 8;
+    DBuf<double> Glev[kMaxLevels];
     void *nccl = nullptr;  // ncclComm_t when the NCCL transport is initialised
     void (*nccl_destroy)(void *) = nullptr;
 
@@ -154,7 +193,6 @@ struct kmf_ctx {
         DG g;
         g.n = n;
         g.ld = ld;
-        g.n_act = dist_on ? n_owned : n;
         g.n_norm = dist_on ? (int)n_global : n;
         g.x = x.p;
         g.y = y.p;
@@ -187,22 +225,25 @@ struct kmf_ctx {
         }
         return b;
     }
+    int n_act() const { return dist_on ? n_owned : n; }
+    // gradient buffer of level k (0 first order, s = sweep s)
+    double *gbuf(int k) { return dist_on ? Glev[k].p : ((k & 1) ? GB.p : GA.p); }
+    void drop_graphs()
+    {
+        g1.reset();
+        gU.reset();
+        gB.reset();
+    }
     ~kmf_ctx()
     {
         if (nccl && nccl_destroy) nccl_destroy(nccl);
-        if (exec1) cudaGraphExecDestroy(exec1);
-        if (execU) cudaGraphExecDestroy(execU);
-        if (execB) cudaGraphExecDestroy(execB);
-        for (auto &e : ev)
-            if (e) cudaEventDestroy(e);
-        for (auto &e : evb)
-            if (e) cudaEventDestroy(e);
+        drop_graphs();
         for (auto &e : evs)
             if (e) cudaEventDestroy(e);
-        if (fork) cudaEventDestroy(fork);
-        if (join) cudaEventDestroy(join);
-        if (s0) cudaStreamDestroy(s0);
-        if (s1) cudaStreamDestroy(s1);
+        for (cudaEvent_t e : {fork, join, xfork, xjoin})
+            if (e) cudaEventDestroy(e);
+        for (cudaStream_t s : {s0, s1, s2})
+            if (s) cudaStreamDestroy(s);
     }
 };
 
@@ -482,133 +523,134 @@ int build_context(kmf_ctx *c, const kmf_geometry *g)
     CK(cudaMemset(c->ctrl.p, 0, sizeof(Ctrl)));
     CK(cudaMemset(c->R.p, 0, sizeof(double) * 4 * ld));
     CK(c->diag.alloc(std::max<long long>(E, std::max(std::max(c->bedges[0], c->bedges[1]), c->bedges[2])) + 1));
-    CK(cudaStreamCreateWithFlags(&c->s0, cudaStreamNonBlocking));
-    CK(cudaStreamCreateWithFlags(&c->s1, cudaStreamNonBlocking));
-    CK(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
-    for (auto &e : c->ev) CK(cudaEventCreate(&e));
-    for (auto &e : c->evb) CK(cudaEventCreate(&e));
+    for (cudaStream_t *s : {&c->s0, &c->s1, &c->s2}) CK(cudaStreamCreateWithFlags(s, cudaStreamNonBlocking));
+    for (cudaEvent_t *e : {&c->fork, &c->join, &c->xfork, &c->xjoin})
+        CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     for (auto &e : c->evs) CK(cudaEventCreate(&e));
+    // one thread per point (all 4 components) from 160K points up: -6 %
+    // q-gradient time at 160K / 2.5M / 10M against 2 threads per point;
+    // small clouds keep 2 threads per point (more threads in flight)
+    c->qg_nc = n > 100000 ? 4 : 2;
     return KMF_OK;
 }
 
+
 // ------------------------------------------------------------ stage launch
-// Kernel launch with programmatic stream serialization (PDL) when enabled:
-// the kernel may start its geometry prologue while the previous kernel of
-// the stream drains (the kernels synchronise with pdl_wait before touching
-// solver state).  Captured into the iteration graph as programmatic edges.
-template <typename... KArgs, typename... Args>
-void launch_ex(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
-               Args &&...args)
-{
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = grid;
-    cfg.blockDim = block;
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = pdl ? 1 : 0;
-    cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
-}
 
-// block size variants (KMF_QG_TB = 128, 256, 512)
-#define KMF_TB_SWITCH(KCALL)                            \
-    switch (c->qg_tb + c->qg_stage) {                   \
-    case 256: KCALL(256, 0, 0); break;                  \
-    case 512: KCALL(512, 0, 0); break;                  \
-    case 129: KCALL(128, 1, 0); break;                  \
-    case 130: KCALL(128, 2, 0); break;                  \
-    case 257:                                           \
-        if (c->qg_minb == 4) KCALL(256, 1, 4);          \
-        else if (c->qg_minb == 3) KCALL(256, 1, 3);     \
-        else KCALL(256, 1, 0);                          \
-        break;                                          \
-    case 258: KCALL(256, 2, 0); break;                  \
-    case 513: KCALL(512, 1, 0); break;                  \
-    default: KCALL(128, 0, 0); break;                   \
+// Kernel `k` of a stage (0 first order, 1..n_inner the sweeps; the flux is
+// k = n_inner + 1 in the second-order scheme and k = 0 in the first-order
+// one, where it reads q only) over the slots of one pass.  Single domain:
+// one pass over every slot.  Partition: kernel k at
+// slot i reads data produced k+1 hops away, so it runs in the INTERIOR pass
+// -- before this stage's halo exchange has arrived -- on the owned slots at
+// depth >= k + 2 (a prefix: owned slots are ordered by depth), and in the
+// BAND pass, after the exchange, on the rest of the slots where it is exact
+// (owned slots for the flux, halo layers <= depth - 1 - k otherwise).
+void stage_range(const kmf_ctx *c, int k, bool flux, bool band, int &lo, int &hi)
+{
+    if (!c->dist_on) {
+        lo = 0;
+        hi = band ? 0 : c->n;
+        return;
     }
-
-template <bool XY, int NC, int U>
-void launch_fo_t(kmf_ctx *c, cudaStream_t s, double *G, Ctrl *ctl, int stage)
-{
-#define KMF_FO(TB, ST, MB)                                                                                        \
-    launch_ex(c->pdl, k_first_order<XY, NC, U, TB, ST, MB>, dim3(nblk(c->n, qg_points_per_block<NC, TB>())), dim3(TB), \
-              0, s, c->dg(), (const double *)c->q.p, G, ctl, stage)
-    KMF_TB_SWITCH(KMF_FO)
-#undef KMF_FO
+    const int cut = c->interior_end[std::min(k + 2, c->depth + 1)];
+    const int end = flux ? c->n_owned : c->layer_end[std::max(0, c->depth - 1 - k)];
+    lo = band ? cut : 0;
+    hi = band ? std::max(cut, end) : cut;
 }
 
-template <bool XY, int NC, int U>
-void launch_sw_t(kmf_ctx *c, cudaStream_t s, const double *Gin, double *Gout, Ctrl *ctl, int stage, int slot,
-                 int want_res, bool outp)
+// Event pair around a launch group while capturing a timed graph.
+struct Mark {
+    kmf_ctx *c;
+    int cls;
+    bool on;
+    cudaEvent_t a = nullptr;
+    Mark(kmf_ctx *c_, int cls_, bool on_) : c(c_), cls(cls_), on(on_ && c_->cap_ev)
+    {
+        if (!on) return;
+        cudaEventCreate(&a);
+        cudaEventRecordWithFlags(a, c->s0, cudaEventRecordExternal);
+    }
+    ~Mark()
+    {
+        if (!on) return;
+        cudaEvent_t b;
+        cudaEventCreate(&b);
+        cudaEventRecordWithFlags(b, c->s0, cudaEventRecordExternal);
+        c->cap_ev->push_back(EvPair{cls, a, b});
+    }
+};
+
+enum { ITER_PLAIN = 0, ITER_INSTRUMENT = 1, ITER_BENCH = 2 };
+
+template <bool XY, int NC>
+void launch_fo_t(kmf_ctx *c, cudaStream_t s, int lo, int hi, double *G, Ctrl *ctl, int stage)
 {
-#define KMF_SW(TB, ST, MB)                                                                                       \
-    if (outp)                                                                                                   \
-        launch_ex(c->pdl, k_sweep<XY, NC, U, TB, ST, MB, true>, dim3(nblk(c->n, qg_points_per_block<NC, TB>())), \
-                  dim3(TB), 0, s, c->dg(), (const double *)c->q.p, Gin, Gout, ctl, stage, slot, want_res);       \
-    else                                                                                                        \
-        launch_ex(c->pdl, k_sweep<XY, NC, U, TB, ST, MB, false>, dim3(nblk(c->n, qg_points_per_block<NC, TB>())), \
-                  dim3(TB), 0, s, c->dg(), (const double *)c->q.p, Gin, Gout, ctl, stage, slot, want_res)
-    KMF_TB_SWITCH(KMF_SW)
-#undef KMF_SW
+    if (hi <= lo) return;
+    c->nlaunch++;
+    k_first_order<XY, NC><<<nblk(hi - range_base(lo), qg_points_per_block<NC>()), kTB, 0, s>>>(
+        c->dg(), lo, hi, (const double *)c->q.p, G, ctl, stage);
 }
 
-// q-gradient launch shape: KMF_QG_NC components per thread (1, 2, 4) and
-// KMF_QG_UNROLL edge unroll (1, 2, 4; 8 = pipelined slot loop); connectivities whose offsets are not
-// x[j]-x[i] use the stored-offset variant (NC 2, U 1).
-#define KMF_QG_DISPATCH(CALL, ...)                                          \
-    do {                                                                    \
-        if (!c->xy) {                                                       \
-            CALL<false, 2, 1>(__VA_ARGS__);                                 \
-            break;                                                          \
-        }                                                                   \
-        switch (c->qg_nc * 10 + c->qg_unroll) {                             \
-        case 11: CALL<true, 1, 1>(__VA_ARGS__); break;                      \
-        case 12: CALL<true, 1, 2>(__VA_ARGS__); break;                      \
-        case 14: CALL<true, 1, 4>(__VA_ARGS__); break;                      \
-        case 21: CALL<true, 2, 1>(__VA_ARGS__); break;                      \
-        case 22: CALL<true, 2, 2>(__VA_ARGS__); break;                      \
-        case 24: CALL<true, 2, 4>(__VA_ARGS__); break;                      \
-        case 41: CALL<true, 4, 1>(__VA_ARGS__); break;                      \
-        case 42: CALL<true, 4, 2>(__VA_ARGS__); break;                      \
-        case 48: CALL<true, 4, 8>(__VA_ARGS__); break;                      \
-        case 28: CALL<true, 2, 8>(__VA_ARGS__); break;                      \
-        default: CALL<true, 4, 4>(__VA_ARGS__); break;                      \
-        }                                                                   \
+template <bool XY, int NC>
+void launch_sw_t(kmf_ctx *c, cudaStream_t s, int lo, int hi, const double *Gin, double *Gout, Ctrl *ctl, int stage,
+                 int slot, int want_res, bool outp)
+{
+    if (hi <= lo) return;
+    c->nlaunch++;
+    const int nb = nblk(hi - range_base(lo), qg_points_per_block<NC>());
+    if (outp)
+        k_sweep<XY, NC, true><<<nb, kTB, 0, s>>>(c->dg(), lo, hi, (const double *)c->q.p, Gin, Gout, ctl, stage, slot,
+                                                 want_res);
+    else
+        k_sweep<XY, NC, false><<<nb, kTB, 0, s>>>(c->dg(), lo, hi, (const double *)c->q.p, Gin, Gout, ctl, stage,
+                                                  slot, want_res);
+}
+
+// q-gradient launch shape: offsets from coordinates (XY) or stored in the
+// ELL table; 4 or 2 components per thread
+#define KMF_QG_DISPATCH(CALL, ...)                                  \
+    do {                                                            \
+        if (!c->xy)                                                 \
+            CALL<false, 2>(__VA_ARGS__);                            \
+        else if (c->qg_nc == 4)                                     \
+            CALL<true, 4>(__VA_ARGS__);                             \
+        else                                                        \
+            CALL<true, 2>(__VA_ARGS__);                             \
     } while (0)
 
-void launch_first_order(kmf_ctx *c, cudaStream_t s, double *G, Ctrl *ctl, int stage)
+void launch_first_order(kmf_ctx *c, cudaStream_t s, int lo, int hi, double *G, Ctrl *ctl, int stage)
 {
-    KMF_QG_DISPATCH(launch_fo_t, c, s, G, ctl, stage);
+    KMF_QG_DISPATCH(launch_fo_t, c, s, lo, hi, G, ctl, stage);
 }
 
 // outp: write the plane gradient layout the flux / boundary kernels read
 // (the last sweep of a stage)
-void launch_sweep(kmf_ctx *c, cudaStream_t s, const double *Gin, double *Gout, Ctrl *ctl, int stage, int slot,
-                  int want_res, bool outp)
+void launch_sweep(kmf_ctx *c, cudaStream_t s, int lo, int hi, const double *Gin, double *Gout, Ctrl *ctl, int stage,
+                  int slot, int want_res, bool outp)
 {
-    KMF_QG_DISPATCH(launch_sw_t, c, s, Gin, Gout, ctl, stage, slot, want_res, outp);
+    KMF_QG_DISPATCH(launch_sw_t, c, s, lo, hi, Gin, Gout, ctl, stage, slot, want_res, outp);
 }
 
-// q-derivatives of one stage: first order into GA, sweeps ping-pong;
-// returns the buffer holding the result (0 = GA, 1 = GB).
-int launch_qgrad(kmf_ctx *c, cudaStream_t s, int stage, int n_inner, Ctrl *ctl, int want_res)
+// q-derivatives of one stage over one pass: level 0 (first order), then
+// the n_inner sweeps, level k reading level k-1; returns the final level.
+double *launch_qgrad(kmf_ctx *c, cudaStream_t s, int stage, int n_inner, Ctrl *ctl, bool band, bool timed)
 {
-    launch_first_order(c, s, c->GA.p, ctl, stage);
-    double *cur = c->GA.p, *nxt = c->GB.p;
-    int which = 0;
-    for (int it = 0; it < n_inner; it++) {
-        launch_sweep(c, s, cur, nxt, ctl, stage, 1 + it, want_res, it + 1 == n_inner);
-        std::swap(cur, nxt);
-        which ^= 1;
+    int lo, hi;
+    {
+        Mark m(c, KC_FO, timed);
+        stage_range(c, 0, false, band, lo, hi);
+        launch_first_order(c, s, lo, hi, c->gbuf(0), ctl, stage);
     }
-    return which;
+    Mark m(c, KC_SWEEP, timed);
+    for (int it = 0; it < n_inner; it++) {
+        stage_range(c, 1 + it, false, band, lo, hi);
+        launch_sweep(c, s, lo, hi, c->gbuf(it), c->gbuf(it + 1), ctl, stage, 1 + it, 0, it + 1 == n_inner);
+    }
+    return c->gbuf(n_inner);
 }
 
-// beta^(-1/(gamma-1)) evaluation of the fast decode (kmf_fastmath.cuh):
+// beta^(-1/(gamma-1)) evaluation of the decode (kmf_flux.cuh fdecode):
 // 1 for gamma = 7/5, 2 for gamma = 5/3, 0 otherwise (log/exp)
 inline int gamma_kind(double gamma)
 {
@@ -617,94 +659,43 @@ inline int gamma_kind(double gamma)
     return 0;
 }
 
-template <bool XY, int MINB, bool PAIR, int GK>
-void launch_flux_t(kmf_ctx *c, cudaStream_t s, const double *G, int mode, double gamma, int zero_bnd, Ctrl *ctl,
-                   int stage)
+template <bool XY, int GK>
+void launch_flux_t(kmf_ctx *c, cudaStream_t s, int lo, int hi, const double *G, int mode, double gamma, int zero_bnd,
+                   Ctrl *ctl, int stage)
 {
+    if (hi <= lo) return;
     DG g = c->dg();
     const double inv_gm1 = 1.0 / (gamma - 1.0), c_i0 = (2.0 - gamma) / (gamma - 1.0);
     double *R = c->R.p;
     const double *q = c->q.p;
-    if (PAIR) {
-        const int nb = nblk(c->n, kTB / 2);
-        if (mode == 0) {
-            k_flux2<XY, -1, MINB, GK><<<nb, kTB, 0, s>>>(g, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage);
-        } else {
-            k_flux2<XY, 0, MINB, GK><<<nb, kTB, 0, s>>>(g, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage);
-            k_flux2<XY, 1, MINB, GK><<<nb, kTB, 0, s>>>(g, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage);
-            k_flux2<XY, 2, MINB, GK><<<nb, kTB, 0, s>>>(g, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage);
-            k_flux2<XY, 3, MINB, GK><<<nb, kTB, 0, s>>>(g, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage);
-        }
-        return;
-    }
-    const int nb = nblk(c->n);
-    if (c->flux_impl >= 3) {
-        // 3 lock-step; 4 + next-edge L1 prefetch; 5 lean arithmetic (table
-        // exp, FMA perturbations); 6 = 4 + 5.  The prefetch only changes
-        // the schedule, so split4 uses the same arithmetic variant as fused
-        // and the two modes stay bitwise equal.
-        // 7 = 5 + the next edge's gathers in registers (PF = 2).
-        const bool lean = c->flux_impl >= 5, pf = c->flux_impl == 4 || c->flux_impl == 6;
-        const bool rp = c->flux_impl == 7 && XY;
-#define KMF_F3(FAM, PF, LEAN)                                                                                 \
-    launch_ex(c->pdl, k_flux3<XY, FAM, MINB, GK, PF, LEAN>, dim3(nb), dim3(kTB), 0, s, g, q, G, R, inv_gm1, c_i0, \
-              zero_bnd, ctl, stage)
-        if (mode == 0) {
-            if (rp) KMF_F3(-1, 2, true);
-            else if (lean && pf) KMF_F3(-1, 1, true);
-            else if (lean) KMF_F3(-1, 0, true);
-            else if (pf) KMF_F3(-1, 1, false);
-            else KMF_F3(-1, 0, false);
-        } else if (lean) {
-            KMF_F3(0, 0, true);
-            KMF_F3(1, 0, true);
-            KMF_F3(2, 0, true);
-            KMF_F3(3, 0, true);
-        } else {
-            KMF_F3(0, 0, false);
-            KMF_F3(1, 0, false);
-            KMF_F3(2, 0, false);
-            KMF_F3(3, 0, false);
-        }
-#undef KMF_F3
-        return;
-    }
+    const int nb = nblk(hi - range_base(lo));
+    c->nlaunch += mode == 0 ? 1 : 4;
     if (mode == 0) {
-        k_flux<XY, -1, MINB, GK><<<nb, kTB, 0, s>>>(g, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage);
+        k_flux<XY, -1, GK><<<nb, kTB, 0, s>>>(g, lo, hi, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage);
     } else {
-        k_flux<XY, 0, MINB, GK><<<nb, kTB, 0, s>>>(g, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage);
-        k_flux<XY, 1, MINB, GK><<<nb, kTB, 0, s>>>(g, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage);
-        k_flux<XY, 2, MINB, GK><<<nb, kTB, 0, s>>>(g, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage);
-        k_flux<XY, 3, MINB, GK><<<nb, kTB, 0, s>>>(g, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage);
+        // split4 (the paper's "optimised" variant): one kernel per family,
+        // R accumulated x+, x-, y+, y- (solver.py:218-229)
+        k_flux<XY, 0, GK><<<nb, kTB, 0, s>>>(g, lo, hi, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage);
+        k_flux<XY, 1, GK><<<nb, kTB, 0, s>>>(g, lo, hi, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage);
+        k_flux<XY, 2, GK><<<nb, kTB, 0, s>>>(g, lo, hi, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage);
+        k_flux<XY, 3, GK><<<nb, kTB, 0, s>>>(g, lo, hi, q, G, R, inv_gm1, c_i0, zero_bnd, ctl, stage);
     }
 }
 
-// interior flux kernel shape: KMF_FLUX_IMPL 1 (thread per point) or 2
-// (thread pair per point); KMF_FLUX_MINB 3 or 4 resident 128-thread blocks/SM
-void launch_flux(kmf_ctx *c, cudaStream_t s, const double *G, int mode, double gamma, int zero_bnd, Ctrl *ctl,
-                 int stage)
+void launch_flux(kmf_ctx *c, cudaStream_t s, int lo, int hi, const double *G, int mode, double gamma, int zero_bnd,
+                 Ctrl *ctl, int stage)
 {
-#define KMF_FLUX_ARGS c, s, G, mode, gamma, zero_bnd, ctl, stage
     const int gk = gamma_kind(gamma);
+#define KMF_FLUX_ARGS c, s, lo, hi, G, mode, gamma, zero_bnd, ctl, stage
     if (!c->xy) {
-        launch_flux_t<false, 3, false, 0>(KMF_FLUX_ARGS);
-        return;
+        if (gk == 1) launch_flux_t<false, 1>(KMF_FLUX_ARGS);
+        else if (gk == 2) launch_flux_t<false, 2>(KMF_FLUX_ARGS);
+        else launch_flux_t<false, 0>(KMF_FLUX_ARGS);
+    } else {
+        if (gk == 1) launch_flux_t<true, 1>(KMF_FLUX_ARGS);
+        else if (gk == 2) launch_flux_t<true, 2>(KMF_FLUX_ARGS);
+        else launch_flux_t<true, 0>(KMF_FLUX_ARGS);
     }
-    if (c->flux_impl == 2) {
-        if (gk == 1) launch_flux_t<true, 4, true, 1>(KMF_FLUX_ARGS);
-        else if (gk == 2) launch_flux_t<true, 4, true, 2>(KMF_FLUX_ARGS);
-        else launch_flux_t<true, 4, true, 0>(KMF_FLUX_ARGS);
-        return;
-    }
-    if (c->flux_minb == 3) {
-        if (gk == 1) launch_flux_t<true, 3, false, 1>(KMF_FLUX_ARGS);
-        else if (gk == 2) launch_flux_t<true, 3, false, 2>(KMF_FLUX_ARGS);
-        else launch_flux_t<true, 3, false, 0>(KMF_FLUX_ARGS);
-        return;
-    }
-    if (gk == 1) launch_flux_t<true, 4, false, 1>(KMF_FLUX_ARGS);
-    else if (gk == 2) launch_flux_t<true, 4, false, 2>(KMF_FLUX_ARGS);
-    else launch_flux_t<true, 4, false, 0>(KMF_FLUX_ARGS);
 #undef KMF_FLUX_ARGS
 }
 
@@ -712,47 +703,37 @@ void launch_boundary(kmf_ctx *c, cudaStream_t s, const double *G, const double f
                      int stage)
 {
     if (c->nb == 0) return;
+    c->nlaunch++;
     const double inv_gm1 = 1.0 / (gamma - 1.0), c_i0 = (2.0 - gamma) / (gamma - 1.0);
     const int warps_per_block = kTB / 32;
     const int nbk = (c->nb + warps_per_block - 1) / warps_per_block;
+#define KMF_BND(GK)                                                                                                \
+    k_boundary<GK><<<nbk, kTB, 0, s>>>(c->dg(), c->db(), c->q.p, G, c->R.p, inv_gm1, c_i0, fs[0], fs[1], fs[2], \
+                                       fs[3], ctl, stage)
     switch (gamma_kind(gamma)) {
-    case 1:
-        k_boundary<1><<<nbk, kTB, 0, s>>>(c->dg(), c->db(), c->q.p, G, c->R.p, inv_gm1, c_i0, fs[0], fs[1], fs[2],
-                                          fs[3], ctl, stage);
-        break;
-    case 2:
-        k_boundary<2><<<nbk, kTB, 0, s>>>(c->dg(), c->db(), c->q.p, G, c->R.p, inv_gm1, c_i0, fs[0], fs[1], fs[2],
-                                          fs[3], ctl, stage);
-        break;
-    default:
-        k_boundary<0><<<nbk, kTB, 0, s>>>(c->dg(), c->db(), c->q.p, G, c->R.p, inv_gm1, c_i0, fs[0], fs[1], fs[2],
-                                          fs[3], ctl, stage);
+    case 1: KMF_BND(1); break;
+    case 2: KMF_BND(2); break;
+    default: KMF_BND(0);
     }
+#undef KMF_BND
 }
 
 void launch_update(kmf_ctx *c, cudaStream_t s, int stage, double gamma, double cfl, IterOut io)
 {
     DG g = c->dg();
-    const int nb = nblk(c->n);
+    const int hi = c->n_act(), nb = nblk(hi);
     Ctrl *ctl = c->ctrl.p;
     double *Uo = c->Uo.p, *Us = c->Us.p, *dt = c->dt.p, *q = c->q.p;
     const double *R = c->R.p;
+    c->nlaunch++;
     switch (stage) {
-    case 1: k_update<1><<<nb, kTB, 0, s>>>(g, Uo, Us, R, dt, q, gamma, cfl, ctl, io); break;
-    case 2: k_update<2><<<nb, kTB, 0, s>>>(g, Uo, Us, R, dt, q, gamma, cfl, ctl, io); break;
-    case 3: k_update<3><<<nb, kTB, 0, s>>>(g, Uo, Us, R, dt, q, gamma, cfl, ctl, io); break;
-    default: k_update<4><<<nb, kTB, 0, s>>>(g, Uo, Us, R, dt, q, gamma, cfl, ctl, io); break;
+    case 1: k_update<1><<<nb, kTB, 0, s>>>(g, 0, hi, Uo, Us, R, dt, q, gamma, cfl, ctl, io); break;
+    case 2: k_update<2><<<nb, kTB, 0, s>>>(g, 0, hi, Uo, Us, R, dt, q, gamma, cfl, ctl, io); break;
+    case 3: k_update<3><<<nb, kTB, 0, s>>>(g, 0, hi, Uo, Us, R, dt, q, gamma, cfl, ctl, io); break;
+    default: k_update<4><<<nb, kTB, 0, s>>>(g, 0, hi, Uo, Us, R, dt, q, gamma, cfl, ctl, io); break;
     }
 }
 
-// One outer iteration (solver.py:515-559) enqueued on s0; the boundary
-// closure runs on a forked branch concurrently with the interior flux.
-enum { ITER_PLAIN = 0, ITER_INSTRUMENT = 1, ITER_BENCH = 2 };
-
-// ITER_INSTRUMENT: eager launches with events around every group, one sync
-// per iteration, per-stage seconds accumulated (solver.py:461-474).
-// ITER_BENCH: captured into a graph with external event-record nodes around
-// each interior flux launch (the roofline kernel, timed on its own stream).
 // ------------------------------------------------------------- NCCL (dlopen)
 // The library does not link NCCL: the multi-process transport resolves it at
 // run time (libnccl.so.2, torch's or the system's), so single-GPU use never
@@ -799,101 +780,149 @@ NcclApi &nccl_api()
 // halo pack on the owner side: q of the points each peer needs
 void enqueue_pack(kmf_ctx *c, cudaStream_t s)
 {
-    if (c->send_total)
+    if (c->send_total && ++c->nlaunch)
         k_halo_pack<<<nblk(c->send_total), kTB, 0, s>>>((int)c->send_total, c->ps_slot.p, c->ps_base.p,
                                                         c->ps_stride.p, c->q.p, c->ld, c->sendbuf.p);
 }
 
 void enqueue_unpack(kmf_ctx *c, cudaStream_t s)
 {
-    if (c->recv_total)
+    if (c->recv_total && ++c->nlaunch)
         k_halo_unpack<<<nblk(c->recv_total), kTB, 0, s>>>((int)c->recv_total, c->pr_slot.p, c->pr_base.p,
                                                           c->pr_stride.p, c->recvbuf.p, c->q.p, c->ld);
 }
 
-// NCCL transport: one grouped send/recv per peer of each rank's halo q, and
-// the exact residue limbs all-reduced before the iteration close; all on the
-// solver stream, so the whole iteration stays one graph.
-void enqueue_exchange_nccl(kmf_ctx *c)
+// NCCL halo exchange on stream s: pack, one grouped send/recv per peer, unpack
+ncclResult_t enqueue_exchange_nccl(kmf_ctx *c, cudaStream_t s)
 {
     NcclApi &api = nccl_api();
     ncclComm_t comm = (ncclComm_t)c->nccl;
-    enqueue_pack(c, c->s0);
+    enqueue_pack(c, s);
     api.GroupStart();
     for (size_t k = 0; k < c->peer_rank.size(); k++) {
         if (c->send_cnt[k])
-            api.Send(c->sendbuf.p + 4 * c->send_off[k], 4 * c->send_cnt[k], ncclDouble, c->peer_rank[k], comm, c->s0);
+            api.Send(c->sendbuf.p + 4 * c->send_off[k], 4 * c->send_cnt[k], ncclDouble, c->peer_rank[k], comm, s);
         if (c->recv_cnt[k])
-            api.Recv(c->recvbuf.p + 4 * c->recv_off[k], 4 * c->recv_cnt[k], ncclDouble, c->peer_rank[k], comm, c->s0);
+            api.Recv(c->recvbuf.p + 4 * c->recv_off[k], 4 * c->recv_cnt[k], ncclDouble, c->peer_rank[k], comm, s);
     }
-    api.GroupEnd();
-    enqueue_unpack(c, c->s0);
+    ncclResult_t r = api.GroupEnd();
+    enqueue_unpack(c, s);
+    return r;
 }
 
-void enqueue_close_nccl(kmf_ctx *c, IterOut io)
-{
-    NcclApi &api = nccl_api();
-    api.AllReduce(c->ctrl.p->limbs, c->ctrl.p->limbs, kLimbs, ncclUint64, ncclSum, (ncclComm_t)c->nccl, c->s0);
-    k_close<<<1, kTB, 0, c->s0>>>(c->ctrl.p, (int)c->n_global, io);
-}
+// ---------------------------------------------------------- one RK stage
+// Per stage (solver.py:524-549) on s0:
+//   interior pass: q-gradients, interior flux            (no halo data read)
+//   [partition: wait for the halo q exchanged after the previous update]
+//   band pass: q-gradients, boundary closure on a forked branch, band flux
+//   update (+ stage 4: residue limbs; partition: limb all-reduce, close)
+//   [NCCL partition: fork the halo exchange of the new q onto s2; the next
+//    stage's interior pass overlaps it]
+// Single domain: the band pass is empty and the boundary branch runs beside
+// the interior flux.  `xchg_pending` tracks a forked exchange inside the
+// graph being captured (joined by the next stage's band pass or at the end
+// of the capture).
+struct StageCtx {
+    const kmf_params *p;
+    IterOut io;
+    int how;
+    bool xchg_pending;
+};
 
-// One RK stage (solver.py:524-549) on s0 (boundary on a forked branch).
-void enqueue_stage(kmf_ctx *c, const kmf_params *p, int stage, IterOut io, int how)
+void enqueue_head(kmf_ctx *c, StageCtx &sc, int stage, double *&G)
 {
+    const kmf_params *p = sc.p;
     Ctrl *ctl = c->ctrl.p;
-    const bool inst = how == ITER_INSTRUMENT, bench = how == ITER_BENCH;
-    cudaEvent_t *e = &c->ev[4 * (stage - 1)];
-    if (inst) cudaEventRecord(e[0], c->s0);
-    // n_inner = 0: the first-order scheme (qx = qy = 0 -> q~ = q bitwise)
-    int which = 0;
-    if (p->n_inner > 0)
-        which = launch_qgrad(c, c->s0, stage, p->n_inner, ctl, 0);
-    else
-        cudaMemsetAsync(c->GA.p, 0, sizeof(double) * 8 * (size_t)c->ld, c->s0);
-    const double *G = which ? c->GB.p : c->GA.p;
-    c->last_G = which;
-    if (inst) cudaEventRecord(e[1], c->s0);
-    cudaEventRecord(c->fork, c->s0);
-    cudaStreamWaitEvent(c->s1, c->fork, 0);
-    launch_boundary(c, c->s1, G, p->fs, p->gamma, ctl, stage);
-    cudaEventRecord(c->join, c->s1);
-    if (bench) cudaEventRecordWithFlags(c->evb[2 * (stage - 1)], c->s0, cudaEventRecordExternal);
-    launch_flux(c, c->s0, G, p->mode, p->gamma, 0, ctl, stage);
-    if (bench) cudaEventRecordWithFlags(c->evb[2 * (stage - 1) + 1], c->s0, cudaEventRecordExternal);
-    cudaStreamWaitEvent(c->s0, c->join, 0);
-    if (inst) cudaEventRecord(e[2], c->s0);
-    io.close_in_kernel = c->dist_on ? 0 : 1;
-    launch_update(c, c->s0, stage, p->gamma, p->cfl, io);
-    if (inst) cudaEventRecord(e[3], c->s0);
-}
-
-void enqueue_iteration(kmf_ctx *c, const kmf_params *p, double *hist, int hist_base, int cap, int how)
-{
-    const bool inst = how == ITER_INSTRUMENT;
-    IterOut io{hist, hist_base, cap, p->convergence_tol, 1};
-    const bool nccl = c->dist_on && c->nccl;
-    for (int stage = 1; stage <= 4; stage++) {
-        enqueue_stage(c, p, stage, io, how);
-        if (nccl) enqueue_exchange_nccl(c);
-    }
-    if (nccl) enqueue_close_nccl(c, io);
-    if (inst) {
-        // residue_norm and the iteration close run inside the stage-4 update
-        cudaEventSynchronize(c->ev[15]);
-        for (int s = 0; s < 4; s++) {
-            float a = 0, b = 0, d = 0;
-            cudaEventElapsedTime(&a, c->ev[4 * s], c->ev[4 * s + 1]);
-            cudaEventElapsedTime(&b, c->ev[4 * s + 1], c->ev[4 * s + 2]);
-            cudaEventElapsedTime(&d, c->ev[4 * s + 2], c->ev[4 * s + 3]);
-            c->stage_sec[2] += a * 1e-3;
-            c->stage_sec[3] += b * 1e-3;
-            c->stage_sec[4] += d * 1e-3;
+    const bool inst = sc.how == ITER_INSTRUMENT, bench = sc.how == ITER_BENCH;
+    {
+        Mark m(c, KC_QGRAD, inst);
+        if (p->n_inner > 0) {
+            G = launch_qgrad(c, c->s0, stage, p->n_inner, ctl, false, bench);
+        } else {  // n_inner = 0: the first-order scheme (qx = qy = 0 -> q~ = q bitwise)
+            G = c->gbuf(0);
+            cudaMemsetAsync(G, 0, sizeof(double) * 8 * (size_t)c->ld, c->s0);
         }
     }
+    Mark m(c, KC_FLUXBND, inst);
+    if (!c->dist_on) {
+        cudaEventRecord(c->fork, c->s0);
+        cudaStreamWaitEvent(c->s1, c->fork, 0);
+        launch_boundary(c, c->s1, G, p->fs, p->gamma, ctl, stage);
+        cudaEventRecord(c->join, c->s1);
+    }
+    int lo, hi;
+    stage_range(c, p->n_inner > 0 ? p->n_inner + 1 : 0, true, false, lo, hi);
+    Mark mf(c, KC_FLUX, bench);
+    launch_flux(c, c->s0, lo, hi, G, p->mode, p->gamma, 0, ctl, stage);
 }
 
-int get_graph(kmf_ctx *c, const kmf_params *p, int unroll, double *hist, int hist_base, int cap,
-              cudaGraphExec_t *exec, GraphKey *key, int how = ITER_PLAIN)
+void enqueue_tail(kmf_ctx *c, StageCtx &sc, int stage, const double *G)
+{
+    const kmf_params *p = sc.p;
+    Ctrl *ctl = c->ctrl.p;
+    const bool inst = sc.how == ITER_INSTRUMENT, bench = sc.how == ITER_BENCH;
+    if (c->dist_on) {
+        if (sc.xchg_pending) {
+            cudaStreamWaitEvent(c->s0, c->xjoin, 0);
+            sc.xchg_pending = false;
+        }
+        {
+            Mark m(c, KC_QGRAD, inst);
+            if (p->n_inner > 0) launch_qgrad(c, c->s0, stage, p->n_inner, ctl, true, bench);
+        }
+        Mark m(c, KC_FLUXBND, inst);
+        cudaEventRecord(c->fork, c->s0);
+        cudaStreamWaitEvent(c->s1, c->fork, 0);
+        launch_boundary(c, c->s1, G, p->fs, p->gamma, ctl, stage);
+        cudaEventRecord(c->join, c->s1);
+        int lo, hi;
+        stage_range(c, p->n_inner > 0 ? p->n_inner + 1 : 0, true, true, lo, hi);
+        {
+            Mark mf(c, KC_FLUX, bench);
+            launch_flux(c, c->s0, lo, hi, G, p->mode, p->gamma, 0, ctl, stage);
+        }
+        cudaStreamWaitEvent(c->s0, c->join, 0);
+    } else {
+        Mark m(c, KC_FLUXBND, inst);
+        cudaStreamWaitEvent(c->s0, c->join, 0);
+    }
+    c->G_last = G;
+    Mark m(c, KC_UPDATE, inst);
+    IterOut io = sc.io;
+    io.close_in_kernel = c->dist_on ? 0 : 1;
+    launch_update(c, c->s0, stage, p->gamma, p->cfl, io);
+}
+
+// NCCL partition: the iteration close after the stage-4 update (exact limb
+// all-reduce, then k_close) and the halo exchange forked onto s2.
+void enqueue_after_update_nccl(kmf_ctx *c, StageCtx &sc, int stage)
+{
+    NcclApi &api = nccl_api();
+    if (stage == 4) {
+        api.AllReduce(c->ctrl.p->limbs, c->ctrl.p->limbs, kLimbs, ncclUint64, ncclSum, (ncclComm_t)c->nccl, c->s0);
+        k_close<<<1, kTB, 0, c->s0>>>(c->ctrl.p, (int)c->n_global, sc.io);
+        c->nlaunch++;
+    }
+    cudaEventRecord(c->xfork, c->s0);
+    cudaStreamWaitEvent(c->s2, c->xfork, 0);
+    enqueue_exchange_nccl(c, c->s2);
+    cudaEventRecord(c->xjoin, c->s2);
+    sc.xchg_pending = true;
+}
+
+void enqueue_iteration(kmf_ctx *c, StageCtx &sc)
+{
+    const bool nccl = c->dist_on && c->nccl;
+    for (int stage = 1; stage <= 4; stage++) {
+        double *G = nullptr;
+        enqueue_head(c, sc, stage, G);
+        enqueue_tail(c, sc, stage, G);
+        if (nccl) enqueue_after_update_nccl(c, sc, stage);
+    }
+}
+
+int get_graph(kmf_ctx *c, const kmf_params *p, int unroll, double *hist, int hist_base, int cap, Graph &gr,
+              int how = ITER_PLAIN)
 {
     GraphKey k;
     std::memset(&k, 0, sizeof k);
@@ -906,20 +935,37 @@ int get_graph(kmf_ctx *c, const kmf_params *p, int unroll, double *hist, int his
     k.unroll = unroll;
     k.cap = cap;
     k.base = hist_base;
+    k.how = how;
     k.hist = hist;
-    if (*exec && *key == k) return KMF_OK;
-    if (*exec) {
-        cudaGraphExecDestroy(*exec);
-        *exec = nullptr;
-    }
+    if (gr.exec && gr.key == k) return KMF_OK;
+    gr.reset();
     cudaGraph_t graph;
+    c->cap_ev = how == ITER_PLAIN ? nullptr : &gr.ev;
+    StageCtx sc{p, IterOut{hist, hist_base, cap, p->convergence_tol, 1}, how, false};
+    c->nlaunch = 0;
     CK(cudaStreamBeginCapture(c->s0, cudaStreamCaptureModeThreadLocal));
-    for (int u = 0; u < unroll; u++) enqueue_iteration(c, p, hist, hist_base, cap, how);
-    CK(cudaStreamEndCapture(c->s0, &graph));
-    cudaError_t e = cudaGraphInstantiate(exec, graph, 0);
+    for (int u = 0; u < unroll; u++) enqueue_iteration(c, sc);
+    if (sc.xchg_pending) cudaStreamWaitEvent(c->s0, c->xjoin, 0);  // join the last exchange
+    cudaError_t ce = cudaStreamEndCapture(c->s0, &graph);
+    c->cap_ev = nullptr;
+    CK(ce);
+    cudaError_t e = cudaGraphInstantiate(&gr.exec, graph, 0);
     cudaGraphDestroy(graph);
     CK(e);
-    *key = k;
+    gr.key = k;
+    gr.launches = c->nlaunch / unroll;
+    return KMF_OK;
+}
+
+// per-class milliseconds of the last replay of a timed graph
+int graph_times(const Graph &gr, double out[KC_N])
+{
+    for (int k = 0; k < KC_N; k++) out[k] = 0.0;
+    for (const EvPair &e : gr.ev) {
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, e.a, e.b));
+        out[e.cls] += ms;
+    }
     return KMF_OK;
 }
 
@@ -933,6 +979,68 @@ void record_error(kmf_ctx *c, int code, int iteration, int stage, int context, l
     c->err.count = count;
     c->err.n_indices = (long long)c->err_idx.size();
     std::snprintf(c->err.message, sizeof c->err.message, "%s", msg);
+}
+
+// first raise site of a failing stage in reference order: interior flux
+// (solver.py:540) < boundary (:541) < decode (:547)
+int first_context(unsigned mask)
+{
+    const int order[] = {KMF_CTX_FLUX_XP, KMF_CTX_WALL_TANGENT, KMF_CTX_WALL_NORMAL, KMF_CTX_OUTER_TANGENT,
+                         KMF_CTX_OUTER_NORMAL, KMF_CTX_C2P_DENSITY, KMF_CTX_C2P_PRESSURE};
+    for (int o : order)
+        if (mask & (1u << o)) return o;
+    return 0;
+}
+
+int check_params(const kmf_ctx *c, const kmf_params *p)
+{
+    if (p->n_inner < 0 || !(p->gamma > 1.0 && p->gamma < 2.0) || !(p->cfl > 0.0 && p->cfl <= 1.0) ||
+        (p->mode != 0 && p->mode != 1)) {
+        set_msg("kmf_run: invalid parameters");
+        return KMF_EINVAL;
+    }
+    if (c->dist_on && p->n_inner + 2 > c->depth) {
+        set_msg("kmf_run: n_inner %d needs a halo of depth %d, the partition has %d", p->n_inner, p->n_inner + 2,
+                c->depth);
+        return KMF_EINVAL;
+    }
+    return KMF_OK;
+}
+
+// U, q, dt of the first iteration (solver.py:502-506, :520) from the pending
+// initial primitives (every local slot, halo included), or q, dt refreshed
+// from U when continuing -- then, under a partition, the halo q refreshed
+// from its owners (halo slots are never updated locally).
+int seed_state(kmf_ctx *c, double gamma, double cfl)
+{
+    DG g = c->dg();
+    if (c->pending_init) {
+        k_init<<<nblk(c->n), kTB, 0, c->s0>>>(g, c->P0.p, c->has_perm ? c->perm.p : nullptr, c->Uo.p, c->q.p,
+                                              c->dt.p, gamma, cfl);
+        c->pending_init = false;
+    } else {
+        k_refresh<<<nblk(c->n_act()), kTB, 0, c->s0>>>(g, c->n_act(), c->Uo.p, c->q.p, c->dt.p, gamma, cfl);
+        if (c->dist_on && c->nccl) {
+            if (enqueue_exchange_nccl(c, c->s0) != ncclSuccess) {
+                set_msg("seed_state: NCCL halo exchange failed");
+                return KMF_ENCCL;
+            }
+        }
+    }
+    CK(cudaGetLastError());
+    c->state_gamma = gamma;
+    return KMF_OK;
+}
+
+int reset_run_ctrl(kmf_ctx *c)
+{
+    Ctrl init;
+    std::memset(&init, 0, sizeof init);
+    init.iter = 1;
+    init.epoch = 1;
+    CK(cudaMemcpyAsync(c->ctrl.p, &init, sizeof init, cudaMemcpyHostToDevice, c->s0));
+    CK(cudaStreamSynchronize(c->s0));  // `init` is a stack temporary
+    return KMF_OK;
 }
 
 }  // namespace
@@ -962,50 +1070,10 @@ int kmf_create(kmf_ctx **out, const kmf_geometry *g, int device)
     CK(cudaSetDevice(device));
     kmf_ctx *c = new kmf_ctx();
     c->device = device;
-    if (const char *e = std::getenv("KMF_QG_NC")) {
-        int v = std::atoi(e);
-        if (v == 1 || v == 2 || v == 4) c->qg_nc = v;
-    }
-    if (const char *e = std::getenv("KMF_QG_UNROLL")) {
-        int v = std::atoi(e);
-        if (v == 1 || v == 2 || v == 4 || v == 8) c->qg_unroll = v;  // 8: pipelined slot loop (NC 2, 4)
-    }
-    if (const char *e = std::getenv("KMF_QG_TB")) c->qg_tb = std::atoi(e);
-    if (const char *e = std::getenv("KMF_PDL")) c->pdl = std::atoi(e) != 0;
-    if (const char *e = std::getenv("KMF_QG_MINB")) c->qg_minb = std::atoi(e);
     int rc = build_context(c, g);
     if (rc != KMF_OK) {
         delete c;
         return rc;
-    }
-    // q-gradient ELL index staging: 1 = cooperative loads (-6.5 % at 2.5M,
-    // +7 % at 160K: costs L1 capacity), 2 = one TMA bulk copy per block
-    // (default at every size: -8.5 % at 2.5M / 10M, and with the pre-halved
-    // offsets it enables -11 % at 40K); KMF_QG_STAGE overrides
-    c->qg_stage = 2;
-    if (const char *e = std::getenv("KMF_QG_STAGE")) c->qg_stage = std::atoi(e);
-    // with the TMA index staging and pre-halved offsets: one thread per point
-    // (NC = 4) in 128-thread blocks from 160K points up (-6 % q-gradient
-    // time at 160K / 2.5M / 10M); small clouds keep 2 threads per point
-    if (c->n > 100000 && !std::getenv("KMF_QG_NC")) c->qg_nc = 4;
-    // software-pipelined slot loop (gathers of slot s+1 in flight while slot
-    // s is evaluated; U = 8): -8 % q-gradient time at 40K / 2.5M / 10M,
-    // -3 % at 160K (variants measured: kmf_kernels.cuh qg_pipeline).
-    if (!std::getenv("KMF_QG_UNROLL") && c->qg_stage == 2 && (c->qg_nc == 2 || c->qg_nc == 4)) c->qg_unroll = 8;
-    // 5: lean arithmetic (table exp, FMA perturbations, select-free family
-    // accumulation): -4.3 % flux time at 160K; 6: + next-edge L1 prefetch
-    // (4 blocks/SM); 7: 5 + the next edge's gathers in registers, 3 blocks/SM
-    // (168 registers): -5 % flux time against 6 at 2.5M / 10M, -2.4 %
-    // against 5 at 160K, neutral at 40K -- the default at every size
-    c->flux_impl = c->xy ? 7 : 5;
-    c->flux_minb = 3;
-    if (const char *e = std::getenv("KMF_FLUX_MINB")) {
-        int v = std::atoi(e);
-        if (v == 3 || v == 4) c->flux_minb = v;
-    }
-    if (const char *e = std::getenv("KMF_FLUX_IMPL")) {
-        int v = std::atoi(e);
-        if (v >= 1 && v <= 7) c->flux_impl = v;
     }
     *out = c;
     return KMF_OK;
@@ -1031,25 +1099,6 @@ int kmf_set_state(kmf_ctx *c, const double *prims)
     return KMF_OK;
 }
 
-namespace {
-// U, q, dt of the first iteration (solver.py:502-506, :520) from the pending
-// initial primitives, or q, dt refreshed from U when continuing.
-int seed_state(kmf_ctx *c, double gamma, double cfl)
-{
-    DG g = c->dg();
-    if (c->pending_init) {
-        k_init<<<nblk(c->n), kTB, 0, c->s0>>>(g, c->P0.p, c->has_perm ? c->perm.p : nullptr, c->Uo.p, c->q.p,
-                                              c->dt.p, gamma, cfl);
-        c->pending_init = false;
-    } else {
-        k_refresh<<<nblk(c->n), kTB, 0, c->s0>>>(g, c->Uo.p, c->q.p, c->dt.p, gamma, cfl);
-    }
-    CK(cudaGetLastError());
-    c->state_gamma = gamma;
-    return KMF_OK;
-}
-}  // namespace
-
 int kmf_run(kmf_ctx *c, const kmf_params *p, int n_iter, double *history, int *iters_done, int *converged)
 {
     if (!c || !p || n_iter < 0) return KMF_EINVAL;
@@ -1057,11 +1106,7 @@ int kmf_run(kmf_ctx *c, const kmf_params *p, int n_iter, double *history, int *i
         set_msg("kmf_run: no state (call kmf_set_state first)");
         return KMF_EINVAL;
     }
-    if (p->n_inner < 0 || !(p->gamma > 1.0 && p->gamma < 2.0) || !(p->cfl > 0.0 && p->cfl <= 1.0) ||
-        (p->mode != 0 && p->mode != 1)) {
-        set_msg("kmf_run: invalid parameters");
-        return KMF_EINVAL;
-    }
+    if (int rc = check_params(c, p)) return rc;
     if (c->dist_on && !c->nccl) {
         set_msg("kmf_run: partitioned context without NCCL (use kmf_nccl_init or kmf_run_group)");
         return KMF_EINVAL;
@@ -1074,33 +1119,40 @@ int kmf_run(kmf_ctx *c, const kmf_params *p, int n_iter, double *history, int *i
     if (n_iter == 0) return KMF_OK;
     if (int rc = seed_state(c, p->gamma, p->cfl)) return rc;
     if ((int)c->history.n < n_iter) CK(c->history.alloc(n_iter));
-    Ctrl init;
-    std::memset(&init, 0, sizeof init);
-    init.iter = 1;
-    init.epoch = 1;
-    CK(cudaMemcpyAsync(c->ctrl.p, &init, sizeof init, cudaMemcpyHostToDevice, c->s0));
+    if (int rc = reset_run_ctrl(c)) return rc;
     for (double &s : c->stage_sec) s = 0.0;
 
-    const int skip = std::max(0, std::min(p->timing_skip, n_iter));
-    if (p->instrument) {
-        // timed iterations launch eagerly with events around every group
-        for (int it = 0; it < n_iter; it++) {
-            enqueue_iteration(c, p, c->history.p, 1, n_iter, it >= skip ? ITER_INSTRUMENT : ITER_PLAIN);
-        }
-    } else {
+    // graphs of U iterations (U = 8, then 1 for the rest); the timed
+    // iterations of an instrumented run replay graphs with event nodes
+    // around each stage's launch groups and read them after every replay
+    const int skip = p->instrument ? std::max(0, std::min(p->timing_skip, n_iter)) : n_iter;
+    auto replay = [&](int count, int how) -> int {
         const int U = 8;
-        int full = n_iter / U, rest = n_iter % U;
-        if (full) {
-            int rc = get_graph(c, p, U, c->history.p, 1, n_iter, &c->execU, &c->keyU);
-            if (rc) return rc;
-            for (int k = 0; k < full; k++) CK(cudaGraphLaunch(c->execU, c->s0));
+        int full = count / U, rest = count % U;
+        for (int pass = 0; pass < 2; pass++) {
+            const int reps = pass ? rest : full, unroll = pass ? 1 : U;
+            if (!reps) continue;
+            Graph &gr = pass ? c->g1 : c->gU;
+            if (int rc = get_graph(c, p, unroll, c->history.p, 1, n_iter, gr, how)) return rc;
+            for (int k = 0; k < reps; k++) {
+                CK(cudaGraphLaunch(gr.exec, c->s0));
+                if (how == ITER_INSTRUMENT) {
+                    CK(cudaStreamSynchronize(c->s0));
+                    double t[KC_N];
+                    if (int rc = graph_times(gr, t)) return rc;
+                    // STAGE_NAMES: timestep, q_variables, q_derivatives, flux_residual,
+                    // state_update, residue -- timestep, q_variables and residue run
+                    // fused inside the update kernels and are reported there
+                    c->stage_sec[2] += t[KC_QGRAD] * 1e-3;
+                    c->stage_sec[3] += t[KC_FLUXBND] * 1e-3;
+                    c->stage_sec[4] += t[KC_UPDATE] * 1e-3;
+                }
+            }
         }
-        if (rest) {
-            int rc = get_graph(c, p, 1, c->history.p, 1, n_iter, &c->exec1, &c->key1);
-            if (rc) return rc;
-            for (int k = 0; k < rest; k++) CK(cudaGraphLaunch(c->exec1, c->s0));
-        }
-    }
+        return KMF_OK;
+    };
+    if (int rc = replay(skip, ITER_PLAIN)) return rc;
+    if (int rc = replay(n_iter - skip, ITER_INSTRUMENT)) return rc;
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(c->s0));
     Ctrl fin;
@@ -1113,19 +1165,7 @@ int kmf_run(kmf_ctx *c, const kmf_params *p, int n_iter, double *history, int *i
     if (iters_done) *iters_done = completed;
     if (converged) *converged = status == 2;
     if (status == 1) {
-        // pick the first raise site in reference order within the failing
-        // stage: interior flux (solver.py:540) < boundary (:541) < decode (:547)
-        unsigned m = fin.ctx_mask;
-        int ctx = 0;
-        const int order[] = {KMF_CTX_FLUX_XP, KMF_CTX_WALL_TANGENT, KMF_CTX_WALL_NORMAL, KMF_CTX_OUTER_TANGENT,
-                             KMF_CTX_OUTER_NORMAL, KMF_CTX_C2P_DENSITY, KMF_CTX_C2P_PRESSURE};
-        for (int o : order)
-            if (m & (1u << o)) {
-                ctx = o;
-                break;
-            }
-        c->last_G = 0;
-        record_error(c, KMF_EPOSITIVITY, fin.err_iter, fin.err_stage, ctx, 0, "positivity");
+        record_error(c, KMF_EPOSITIVITY, fin.err_iter, fin.err_stage, first_context(fin.ctx_mask), 0, "positivity");
         return KMF_EPOSITIVITY;
     }
     return KMF_OK;
@@ -1245,7 +1285,7 @@ int kmf_op_first_order(kmf_ctx *c, const double *q, double *qx, double *qy)
     int rc = upload_fields(c, q, 4, c->q.p, 4, 1);
     if (rc) return rc;
     if ((rc = reset_ctrl(c))) return rc;
-    launch_first_order(c, c->s0, c->GA.p, c->ctrl.p, 0);
+    launch_first_order(c, c->s0, 0, c->n, c->GA.p, c->ctrl.p, 0);
     CK(cudaGetLastError());
     if ((rc = download_fields(c, c->GA.p, 4, qx, 2))) return rc;
     return download_fields(c, c->GA.p + 1, 4, qy, 2);
@@ -1269,12 +1309,12 @@ int kmf_op_q_derivatives(kmf_ctx *c, const double *q, int n_inner, const double 
         if ((rc = upload_fields(c, pqx, 4, c->GA.p, 2))) return rc;
         if ((rc = upload_fields(c, pqy, 4, c->GA.p + 1, 2))) return rc;
     } else {
-        launch_first_order(c, c->s0, c->GA.p, c->ctrl.p, 0);
+        launch_first_order(c, c->s0, 0, c->n, c->GA.p, c->ctrl.p, 0);
     }
     double *cur = c->GA.p, *nxt = c->GB.p;
     for (int it = 0; it < n_inner; it++) {
         CK(cudaMemsetAsync(&c->ctrl.p->resmax, 0, sizeof(unsigned long long), c->s0));
-        launch_sweep(c, c->s0, cur, nxt, c->ctrl.p, 0, 1 + it, 1, it + 1 == n_inner);
+        launch_sweep(c, c->s0, 0, c->n, cur, nxt, c->ctrl.p, 0, 1 + it, 1, it + 1 == n_inner);
         CK(cudaGetLastError());
         if (inner_residuals) {
             unsigned long long b = 0;
@@ -1312,12 +1352,12 @@ int kmf_op_flux_residual(kmf_ctx *c, const double *q, const double *qx, const do
     if ((rc = reset_ctrl(c))) return rc;
     c->err = kmf_error_info{};
     c->err_idx.clear();
-    launch_flux(c, c->s0, c->GA.p, mode, gamma, 1, c->ctrl.p, 0);
+    launch_flux(c, c->s0, 0, c->n, c->GA.p, mode, gamma, 1, c->ctrl.p, 0);
     CK(cudaGetLastError());
     Ctrl fin;
     if ((rc = read_ctrl(c, &fin))) return rc;
     if (fin.state & 1ull) {
-        c->last_G = 0;
+        c->G_last = c->GA.p;
         record_error(c, KMF_EPOSITIVITY, 0, 0, KMF_CTX_FLUX_XP, 0, "positivity");
         return KMF_EPOSITIVITY;
     }
@@ -1340,28 +1380,29 @@ int kmf_op_boundary(kmf_ctx *c, const double *q, const double *qx, const double 
     Ctrl fin;
     if ((rc = read_ctrl(c, &fin))) return rc;
     if (fin.state & 1ull) {
-        unsigned m = fin.ctx_mask;
-        int ctx = KMF_CTX_WALL_TANGENT;
-        const int order[] = {KMF_CTX_WALL_TANGENT, KMF_CTX_WALL_NORMAL, KMF_CTX_OUTER_TANGENT, KMF_CTX_OUTER_NORMAL};
-        for (int o : order)
-            if (m & (1u << o)) {
-                ctx = o;
-                break;
-            }
-        c->last_G = 0;
-        record_error(c, KMF_EPOSITIVITY, 0, 0, ctx, 0, "positivity");
+        const int ctx = first_context(fin.ctx_mask & ~(1u << KMF_CTX_FLUX_XP));
+        c->G_last = c->GA.p;
+        record_error(c, KMF_EPOSITIVITY, 0, 0, ctx ? ctx : KMF_CTX_WALL_TANGENT, 0, "positivity");
         return KMF_EPOSITIVITY;
     }
     return download_fields(c, c->R.p, 4, R);
 }
 
+// the gradient buffer a positivity diagnostic reads: 0 GA, 1 GB, 2 the
+// final gradients of the last stage enqueued (run / run_group failures)
+static const double *diag_grad(kmf_ctx *c, int which)
+{
+    if (which == 2 && c->G_last) return c->G_last;
+    return which == 1 ? c->GB.p : c->GA.p;
+}
+
 // flags for every caller-CSR edge of the full stencil computed from the
-// device's current q and the gradient buffer `which` (0 GA, 1 GB)
+// device's current q and the gradient buffer `which` (diag_grad)
 int kmf_diag_flux(kmf_ctx *c, int which, uint8_t *flags)
 {
     if (!c || !flags) return KMF_EINVAL;
     CK(cudaSetDevice(c->device));
-    const double *G = which ? c->GB.p : c->GA.p;
+    const double *G = diag_grad(c, which);
     if (c->xy)
         k_diag_flux<true><<<nblk(c->n), kTB, 0, c->s0>>>(c->dg(), c->q.p, G, c->diag.p);
     else
@@ -1379,7 +1420,7 @@ int kmf_diag_frame(kmf_ctx *c, int which, int fam, uint8_t *flags)
     if (!c || !flags || fam < 0 || fam > 2) return KMF_EINVAL;
     if (c->nb == 0) return KMF_OK;
     CK(cudaSetDevice(c->device));
-    const double *G = which ? c->GB.p : c->GA.p;
+    const double *G = diag_grad(c, which);
     k_diag_frame<<<nblk(c->nb), kTB, 0, c->s0>>>(c->dg(), c->db(), fam, c->q.p, G, c->diag.p);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(flags, c->diag.p, (size_t)c->bedges[fam], cudaMemcpyDeviceToHost, c->s0));
@@ -1395,6 +1436,7 @@ int kmf_diag_stage_state(kmf_ctx *c, int stage, double *U)
     CK(cudaSetDevice(c->device));
     return download_fields(c, stage == 4 ? c->Uo.p : c->Us.p, 4, U);
 }
+
 
 // ------------------------------------------------------ point operators
 
@@ -1509,7 +1551,7 @@ int kmf_op_split_flux(int64_t n, const double *prims, int axis, int sign, double
     TMP_OR_FAIL(dp, double, 4 * n);
     TMP_OR_FAIL(dg, double, 4 * n);
     CK(cudaMemcpy(dp, prims, sizeof(double) * 4 * n, cudaMemcpyHostToDevice));
-    k_op_split_flux<<<nblk(n), kTB>>>((int)n, dp, axis, (double)sign, gamma, dg);
+    k_op_split_flux<<<nblk(n), kTB>>>((int)n, dp, axis, (double)sign, (2.0 - gamma) / (gamma - 1.0), dg);
     CK(cudaGetLastError());
     CK(cudaMemcpy(G, dg, sizeof(double) * 4 * n, cudaMemcpyDeviceToHost));
     return KMF_OK;
@@ -1579,53 +1621,56 @@ int kmf_op_residue(int64_t n, const double *Un, const double *Uold, double *out)
 
 extern "C" {
 
-// Timed outer iterations for bench.py: each step = one graph launch of one
-// outer iteration on the context stream, bracketed by CUDA events; between
-// steps a `flush_bytes` memset on the same stream evicts L2 (outside the
-// timed events).  flux_ms[i] = summed duration of the 4 interior flux
-// launches of step i (events on the flux kernel's own stream).
+// Timed outer iterations for bench.py.  Pass 1: n_steps plain iteration
+// graphs (no timing nodes inside), each bracketed by CUDA events on the
+// context stream -> step_ms[i]; between steps a `flush_bytes` memset on the
+// same stream evicts L2 outside the timed events.  Pass 2: n_steps more with
+// the kernel-timing graph (event nodes around the launch groups, on their
+// own stream) -> kernel_ms[KMF_BENCH_KERNELS * i + k] = step i's summed
+// launches of kernel class k (0 interior flux, 1 first-order q-gradients,
+// 2 Jacobi sweeps); the event nodes never perturb step_ms.
 int kmf_bench_steps(kmf_ctx *c, const kmf_params *p, int n_steps, int64_t flush_bytes, double *step_ms,
-                    double *flux_ms, int *launches_per_step)
+                    double *kernel_ms, int *launches_per_step)
 {
-    if (!c || !p || n_steps < 1 || !step_ms || !flux_ms) return KMF_EINVAL;
+    if (!c || !p || n_steps < 1 || !step_ms || !kernel_ms) return KMF_EINVAL;
     if (!c->have_state) {
         set_msg("kmf_bench_steps: no state");
         return KMF_EINVAL;
     }
+    if (int rc = check_params(c, p)) return rc;
     CK(cudaSetDevice(c->device));
     if (int rc = seed_state(c, p->gamma, p->cfl)) return rc;
-    if ((int)c->history.n < n_steps) CK(c->history.alloc(n_steps));
+    if ((int)c->history.n < 2 * n_steps) CK(c->history.alloc(2 * n_steps));
     if (flush_bytes > 0 && (int64_t)c->flush.n < flush_bytes) CK(c->flush.alloc((size_t)flush_bytes));
-    Ctrl init;
-    std::memset(&init, 0, sizeof init);
-    init.iter = 1;
-    init.epoch = 1;
-    CK(cudaMemcpyAsync(c->ctrl.p, &init, sizeof init, cudaMemcpyHostToDevice, c->s0));
+    if (int rc = reset_run_ctrl(c)) return rc;
     kmf_params q = *p;
     q.convergence_tol = 0.0;
-    if (int rc = get_graph(c, &q, 1, c->history.p, 1, n_steps, &c->execB, &c->keyB, ITER_BENCH)) return rc;
-    for (int i = 0; i < n_steps; i++) {
-        if (flush_bytes > 0) CK(cudaMemsetAsync(c->flush.p, i & 0xff, (size_t)flush_bytes, c->s0));
-        CK(cudaEventRecord(c->evs[0], c->s0));
-        CK(cudaGraphLaunch(c->execB, c->s0));
-        CK(cudaEventRecord(c->evs[1], c->s0));
-        CK(cudaEventSynchronize(c->evs[1]));
-        float ms = 0;
-        CK(cudaEventElapsedTime(&ms, c->evs[0], c->evs[1]));
-        step_ms[i] = ms;
-        double f = 0;
-        for (int s = 0; s < 4; s++) {
-            float a = 0;
-            CK(cudaEventElapsedTime(&a, c->evb[2 * s], c->evb[2 * s + 1]));
-            f += a;
+    for (int pass = 0; pass < 2; pass++) {
+        Graph &gr = pass ? c->gB : c->g1;
+        if (int rc = get_graph(c, &q, 1, c->history.p, 1, 2 * n_steps, gr, pass ? ITER_BENCH : ITER_PLAIN))
+            return rc;
+        for (int i = 0; i < n_steps; i++) {
+            if (flush_bytes > 0) CK(cudaMemsetAsync(c->flush.p, i & 0xff, (size_t)flush_bytes, c->s0));
+            CK(cudaEventRecord(c->evs[0], c->s0));
+            CK(cudaGraphLaunch(gr.exec, c->s0));
+            CK(cudaEventRecord(c->evs[1], c->s0));
+            CK(cudaEventSynchronize(c->evs[1]));
+            if (pass == 0) {
+                float ms = 0;
+                CK(cudaEventElapsedTime(&ms, c->evs[0], c->evs[1]));
+                step_ms[i] = ms;
+                continue;
+            }
+            double t[KC_N];
+            if (int rc = graph_times(gr, t)) return rc;
+            kernel_ms[KMF_BENCH_KERNELS * i + 0] = t[KC_FLUX];
+            kernel_ms[KMF_BENCH_KERNELS * i + 1] = t[KC_FO];
+            kernel_ms[KMF_BENCH_KERNELS * i + 2] = t[KC_SWEEP];
         }
-        flux_ms[i] = f;
     }
     Ctrl fin;
     CK(cudaMemcpy(&fin, c->ctrl.p, sizeof fin, cudaMemcpyDeviceToHost));
-    if (launches_per_step)
-        *launches_per_step = 4 * ((p->n_inner ? 1 + p->n_inner : 0) + (p->mode ? 4 : 1) + (c->nb > 0 ? 1 : 0) + 1) +  // the iteration close is fused into update<4>
-                             ((c->dist_on && c->nccl) ? 4 * ((c->send_total ? 1 : 0) + (c->recv_total ? 1 : 0)) + 1 : 0);
+    if (launches_per_step) *launches_per_step = c->g1.launches;
     if ((fin.state & 3ull) == 1ull) {
         set_msg("kmf_bench_steps: positivity failure at iteration %d", fin.err_iter);
         return KMF_EPOSITIVITY;
@@ -1678,9 +1723,7 @@ void kmf_host_free(void *p)
     if (p) cudaFreeHost(p);
 }
 
-}  // extern "C"
-
-extern "C" int kmf_fastmath_probe(int64_t n, const double *x, int which, double *out)
+int kmf_fastmath_probe(int64_t n, const double *x, int which, double *out)
 {
     if (n <= 0 || !x || !out || which < 0 || which > 5) return KMF_EINVAL;
     if (int rc = ensure_device()) return rc;
@@ -1694,23 +1737,61 @@ extern "C" int kmf_fastmath_probe(int64_t n, const double *x, int which, double 
     return KMF_OK;
 }
 
+int kmf_probe_edge_state(int64_t n, const double *q, double gamma, double *prims, double *flux)
+{
+    if (n <= 0 || !q || !prims || !flux || !(gamma > 1.0 && gamma < 2.0)) return KMF_EINVAL;
+    if (int rc = ensure_device()) return rc;
+    Tmp tmp;
+    TMP_OR_FAIL(dq, double, 4 * n);
+    TMP_OR_FAIL(dp, double, 4 * n);
+    TMP_OR_FAIL(df, double, 16 * n);
+    CK(cudaMemcpy(dq, q, sizeof(double) * 4 * n, cudaMemcpyHostToDevice));
+    const double inv_gm1 = 1.0 / (gamma - 1.0), c_i0 = (2.0 - gamma) / (gamma - 1.0);
+    switch (gamma_kind(gamma)) {
+    case 1: k_probe_edge_state<1><<<nblk(n), kTB>>>((int)n, dq, inv_gm1, c_i0, dp, df); break;
+    case 2: k_probe_edge_state<2><<<nblk(n), kTB>>>((int)n, dq, inv_gm1, c_i0, dp, df); break;
+    default: k_probe_edge_state<0><<<nblk(n), kTB>>>((int)n, dq, inv_gm1, c_i0, dp, df);
+    }
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(prims, dp, sizeof(double) * 4 * n, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(flux, df, sizeof(double) * 16 * n, cudaMemcpyDeviceToHost));
+    return KMF_OK;
+}
+
+}  // extern "C"
+
 // ============================================================ multi-GPU ABI
 
-extern "C" int kmf_set_partition(kmf_ctx *c, int64_t n_owned, int64_t n_global, int rank, int nranks, int npeers,
+extern "C" int kmf_set_partition(kmf_ctx *c, int64_t n_owned, int64_t n_global, int rank, int nranks, int depth,
+                                 const int64_t *layer_end, const int64_t *interior_end, int npeers,
                                  const int *peer_ranks, const int64_t *send_counts, const int64_t *send_slots,
                                  const int64_t *recv_counts, const int64_t *recv_slots)
 {
-    if (!c || n_owned <= 0 || n_owned > c->n || n_global < n_owned || npeers < 0 || rank < 0 || rank >= nranks)
+    if (!c || n_owned <= 0 || n_owned > c->n || n_global < n_owned || npeers < 0 || rank < 0 || rank >= nranks ||
+        depth < 1 || !layer_end || !interior_end)
         return KMF_EINVAL;
     if (c->has_perm) {
-        set_msg("kmf_set_partition: partitioned contexts use the natural local order");
+        set_msg("kmf_set_partition: partitioned contexts use the partition's local order");
         return KMF_EINVAL;
     }
+    // layer_end[k] = n_owned + |L1..Lk| (k = 0..depth, ending at n);
+    // interior_end[k] = owned slots at depth >= k (k = 0..depth+1), non-increasing
+    if (layer_end[0] != n_owned || layer_end[depth] != c->n || interior_end[0] != n_owned) {
+        set_msg("kmf_set_partition: layer / interior counts inconsistent with the context");
+        return KMF_EINVAL;
+    }
+    for (int k = 0; k < depth; k++)
+        if (layer_end[k + 1] < layer_end[k]) return KMF_EINVAL;
+    for (int k = 0; k <= depth; k++)
+        if (interior_end[k + 1] > interior_end[k] || interior_end[k + 1] < 0) return KMF_EINVAL;
     CK(cudaSetDevice(c->device));
     c->n_owned = (int)n_owned;
     c->n_global = n_global;
     c->rank = rank;
     c->nranks = nranks;
+    c->depth = depth;
+    c->layer_end.assign(layer_end, layer_end + depth + 1);
+    c->interior_end.assign(interior_end, interior_end + depth + 2);
     c->peer_rank.assign(peer_ranks, peer_ranks + npeers);
     c->send_off.assign(npeers, 0);
     c->send_cnt.assign(npeers, 0);
@@ -1752,11 +1833,13 @@ extern "C" int kmf_set_partition(kmf_ctx *c, int64_t n_owned, int64_t n_global, 
         return rc;
     CK(c->sendbuf.alloc(4 * (size_t)std::max<long long>(so, 1)));
     CK(c->recvbuf.alloc(4 * (size_t)std::max<long long>(ro, 1)));
+    if (depth - 1 > kmf_ctx::kMaxLevels) {
+        set_msg("kmf_set_partition: depth %d exceeds %d", depth, kmf_ctx::kMaxLevels + 1);
+        return KMF_EINVAL;
+    }
+    for (int k = 0; k < depth - 1; k++) CK(c->Glev[k].alloc(8 * (size_t)c->ld));  // levels 0..n_inner, n_inner <= depth - 2
     c->dist_on = true;
-    // graphs captured before the partition are stale
-    if (c->exec1) cudaGraphExecDestroy(c->exec1), c->exec1 = nullptr;
-    if (c->execU) cudaGraphExecDestroy(c->execU), c->execU = nullptr;
-    if (c->execB) cudaGraphExecDestroy(c->execB), c->execB = nullptr;
+    c->drop_graphs();  // graphs captured before the partition are stale
     return KMF_OK;
 }
 
@@ -1796,25 +1879,27 @@ extern "C" int kmf_nccl_init(kmf_ctx *c, const void *id128, int rank, int nranks
         NcclApi &a = nccl_api();
         if (a.CommDestroy) a.CommDestroy((ncclComm_t)p);
     };
-    if (c->exec1) cudaGraphExecDestroy(c->exec1), c->exec1 = nullptr;
-    if (c->execU) cudaGraphExecDestroy(c->execU), c->execU = nullptr;
-    if (c->execB) cudaGraphExecDestroy(c->execB), c->execB = nullptr;
-    // One eager round of the exact send/recv pattern and of the limb
-    // all-reduce before any graph capture: NCCL sets its P2P connections up
-    // lazily at first use, which must not happen inside stream capture.
-    // Nothing is unpacked and the all-reduce runs on scratch memory, so the
-    // solver state is untouched.
+    c->drop_graphs();
+    // One eager round of the exact send/recv pattern (on both streams the
+    // graphs use) and of the limb all-reduce before any graph capture: NCCL
+    // sets its P2P connections up lazily at first use, which must not happen
+    // inside stream capture.  Nothing is unpacked and the all-reduce runs on
+    // scratch memory, so the solver state is untouched.
     if (c->dist_on) {
-        api.GroupStart();
-        for (size_t k = 0; k < c->peer_rank.size(); k++) {
-            if (c->send_cnt[k])
-                api.Send(c->sendbuf.p + 4 * c->send_off[k], 4 * c->send_cnt[k], ncclDouble, c->peer_rank[k], comm,
-                         c->s0);
-            if (c->recv_cnt[k])
-                api.Recv(c->recvbuf.p + 4 * c->recv_off[k], 4 * c->recv_cnt[k], ncclDouble, c->peer_rank[k], comm,
-                         c->s0);
+        for (cudaStream_t s : {c->s0, c->s2}) {
+            api.GroupStart();
+            for (size_t k = 0; k < c->peer_rank.size(); k++) {
+                if (c->send_cnt[k])
+                    api.Send(c->sendbuf.p + 4 * c->send_off[k], 4 * c->send_cnt[k], ncclDouble, c->peer_rank[k],
+                             comm, s);
+                if (c->recv_cnt[k])
+                    api.Recv(c->recvbuf.p + 4 * c->recv_off[k], 4 * c->recv_cnt[k], ncclDouble, c->peer_rank[k],
+                             comm, s);
+            }
+            r = api.GroupEnd();
+            if (r != ncclSuccess) break;
+            CK(cudaStreamSynchronize(s));
         }
-        r = api.GroupEnd();
         DBuf<unsigned long long> scratch;
         CK(scratch.alloc(kLimbs));
         CK(cudaMemsetAsync(scratch.p, 0, sizeof(unsigned long long) * kLimbs, c->s0));
@@ -1829,11 +1914,14 @@ extern "C" int kmf_nccl_init(kmf_ctx *c, const void *id128, int rank, int nranks
 }
 
 // Single-process driver for several partitioned contexts (one per rank, on
-// the same or different GPUs): per stage every context runs its kernels,
-// then halo q moves by device-to-device / peer copies; the residue limbs
-// are summed on the host (exact integers) and every context closes the
+// the same or different GPUs) with the multi-process schedule: per stage
+// every context runs its interior pass, then the halo q packed after the
+// previous update moves by device / peer copies, then every context runs
+// its band pass and update and packs its new halo q.  The residue limbs are
+// summed on the host (exact integers) and every context closes the
 // iteration with the same total.  Used by the multi-rank parity tests on a
-// single GPU and as a one-process multi-GPU mode.
+// single GPU (the interior / band split is exercised exactly as under NCCL)
+// and as a one-process multi-GPU mode.
 extern "C" int kmf_run_group(kmf_ctx **ctxs, int nctx, const kmf_params *p, int n_iter, double *history,
                              int *iters_done, int *converged)
 {
@@ -1845,6 +1933,7 @@ extern "C" int kmf_run_group(kmf_ctx **ctxs, int nctx, const kmf_params *p, int 
             set_msg("kmf_run_group: contexts must be partitioned ranks 0..n-1 with state");
             return KMF_EINVAL;
         }
+        if (int rc = check_params(c, p)) return rc;
         byrank[c->rank] = c;
     }
     if (iters_done) *iters_done = 0;
@@ -1852,13 +1941,11 @@ extern "C" int kmf_run_group(kmf_ctx **ctxs, int nctx, const kmf_params *p, int 
     if (n_iter == 0) return KMF_OK;
     for (kmf_ctx *c : byrank) {
         CK(cudaSetDevice(c->device));
+        c->err = kmf_error_info{};
         if (int rc = seed_state(c, p->gamma, p->cfl)) return rc;
         if ((int)c->history.n < n_iter) CK(c->history.alloc(n_iter));
-        Ctrl init;
-        std::memset(&init, 0, sizeof init);
-        init.iter = 1;
-        init.epoch = 1;
-        CK(cudaMemcpy(c->ctrl.p, &init, sizeof init, cudaMemcpyHostToDevice));
+        if (int rc = reset_run_ctrl(c)) return rc;
+        enqueue_pack(c, c->s0);  // the halo q the first band pass reads (and a continuation needs)
     }
     auto sync_all = [&]() -> int {
         for (kmf_ctx *c : byrank) {
@@ -1867,32 +1954,45 @@ extern "C" int kmf_run_group(kmf_ctx **ctxs, int nctx, const kmf_params *p, int 
         }
         return KMF_OK;
     };
+    auto exchange = [&]() -> int {
+        if (int rc = sync_all()) return rc;
+        for (kmf_ctx *dst : byrank)
+            for (size_t k = 0; k < dst->peer_rank.size(); k++) {
+                kmf_ctx *src = byrank[dst->peer_rank[k]];
+                size_t j = 0;
+                while (j < src->peer_rank.size() && src->peer_rank[j] != dst->rank) j++;
+                if (j == src->peer_rank.size() || src->send_cnt[j] != dst->recv_cnt[k]) {
+                    set_msg("kmf_run_group: send/recv lists of ranks %d and %d disagree", src->rank, dst->rank);
+                    return KMF_EINVAL;
+                }
+                if (dst->recv_cnt[k])
+                    CK(cudaMemcpyPeer(dst->recvbuf.p + 4 * dst->recv_off[k], dst->device,
+                                      src->sendbuf.p + 4 * src->send_off[j], src->device,
+                                      sizeof(double) * 4 * dst->recv_cnt[k]));
+            }
+        for (kmf_ctx *c : byrank) {
+            CK(cudaSetDevice(c->device));
+            enqueue_unpack(c, c->s0);
+        }
+        return KMF_OK;
+    };
     for (int it = 0; it < n_iter; it++) {
         for (int stage = 1; stage <= 4; stage++) {
-            for (kmf_ctx *c : byrank) {
-                CK(cudaSetDevice(c->device));
-                IterOut io{c->history.p, 1, n_iter, p->convergence_tol, 0};
-                enqueue_stage(c, p, stage, io, ITER_PLAIN);
-                enqueue_pack(c, c->s0);
+            std::vector<double *> Gs(nctx, nullptr);
+            std::vector<StageCtx> sc;
+            for (kmf_ctx *c : byrank)
+                sc.push_back(StageCtx{p, IterOut{c->history.p, 1, n_iter, p->convergence_tol, 0}, ITER_PLAIN, false});
+            for (int r = 0; r < nctx; r++) {
+                CK(cudaSetDevice(byrank[r]->device));
+                enqueue_head(byrank[r], sc[r], stage, Gs[r]);  // interior pass: no halo data read
             }
-            if (int rc = sync_all()) return rc;
-            for (kmf_ctx *dst : byrank)
-                for (size_t k = 0; k < dst->peer_rank.size(); k++) {
-                    kmf_ctx *src = byrank[dst->peer_rank[k]];
-                    size_t j = 0;
-                    while (j < src->peer_rank.size() && src->peer_rank[j] != dst->rank) j++;
-                    if (j == src->peer_rank.size() || src->send_cnt[j] != dst->recv_cnt[k]) {
-                        set_msg("kmf_run_group: send/recv lists of ranks %d and %d disagree", src->rank, dst->rank);
-                        return KMF_EINVAL;
-                    }
-                    if (dst->recv_cnt[k])
-                        CK(cudaMemcpyPeer(dst->recvbuf.p + 4 * dst->recv_off[k], dst->device,
-                                          src->sendbuf.p + 4 * src->send_off[j], src->device,
-                                          sizeof(double) * 4 * dst->recv_cnt[k]));
-                }
-            for (kmf_ctx *c : byrank) {
+            if (int rc = exchange()) return rc;
+            for (int r = 0; r < nctx; r++) {
+                kmf_ctx *c = byrank[r];
                 CK(cudaSetDevice(c->device));
-                enqueue_unpack(c, c->s0);
+                enqueue_tail(c, sc[r], stage, Gs[r]);
+                enqueue_pack(c, c->s0);
+                CK(cudaGetLastError());
             }
         }
         // exact residue across ranks: integer limb sums
@@ -1932,6 +2032,9 @@ extern "C" int kmf_run_group(kmf_ctx **ctxs, int nctx, const kmf_params *p, int 
             err_it = f.err_iter;
             err_stage = f.err_stage;
         }
+        if ((f.state & 3ull) == 1ull)
+            record_error(c, KMF_EPOSITIVITY, f.err_iter, f.err_stage, first_context(f.ctx_mask), c->rank,
+                         "positivity");
         if (c->rank == 0) fin = f;
     }
     int completed = std::min(fin.iter - 1, n_iter);
@@ -1940,18 +2043,6 @@ extern "C" int kmf_run_group(kmf_ctx **ctxs, int nctx, const kmf_params *p, int 
     if (iters_done) *iters_done = completed;
     if (converged) *converged = (fin.state & 3ull) == 2ull;
     if (err_rank >= 0) {
-        kmf_ctx *c = byrank[err_rank];
-        Ctrl f;
-        CK(cudaMemcpy(&f, c->ctrl.p, sizeof f, cudaMemcpyDeviceToHost));
-        int ctx = 0;
-        const int order[] = {KMF_CTX_FLUX_XP, KMF_CTX_WALL_TANGENT, KMF_CTX_WALL_NORMAL, KMF_CTX_OUTER_TANGENT,
-                             KMF_CTX_OUTER_NORMAL, KMF_CTX_C2P_DENSITY, KMF_CTX_C2P_PRESSURE};
-        for (int o : order)
-            if (f.ctx_mask & (1u << o)) {
-                ctx = o;
-                break;
-            }
-        record_error(c, KMF_EPOSITIVITY, f.err_iter, f.err_stage, ctx, err_rank, "positivity");
         set_msg("positivity failure on rank %d", err_rank);
         return KMF_EPOSITIVITY;
     }

@@ -76,7 +76,6 @@ __device__ __forceinline__ void raise_err(Ctrl *c, int stage, int slot, int ctx)
 // Geometry as seen by the point kernels.
 struct DG {
     int n, ld;
-    int n_act;   // points the flux / update launches cover (owned points under a partition)
     int n_norm;  // residue normalisation (global point count under a partition)
     const double *__restrict__ x;
     const double *__restrict__ y;
@@ -213,66 +212,50 @@ KMF_HD void gstore_nc(double *__restrict__ G, int ld, int i, int k0, const doubl
     }
 }
 
-// Programmatic dependent launch (kernels launched with the PDL attribute,
-// launch_ex in kmf_b200.cu): pdl_trigger lets the next kernel of the
-// stream be scheduled while this grid's last wave drains; pdl_wait blocks
-// until the previous grid has completed and its writes are visible.  Each
-// kernel does its geometry-only prologue (indices, coordinates, TMA index
-// staging) before pdl_wait and touches solver state only after it.  Both
-// are no-ops for kernels launched without the attribute.
-KMF_HD void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-KMF_HD void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// ---------------------------------------------------------------------------
+// Launch ranges.  Every point kernel covers the device slots [lo, hi) of
+// its launch: the whole cloud on one GPU, the interior or the halo band of a
+// partition (local slots are ordered by depth, so
+// each pass is a contiguous range).  Blocks start at the 32-slot SELL slice
+// holding lo, so the slices (and their staged index runs) stay aligned.
+__host__ __device__ __forceinline__ int range_base(int lo) { return lo & ~31; }
 
 // ---------------------------------------------------------------------------
-// q-gradient kernels: NC components of one point per thread (NC = 1, 2, 4).
-// The four components of q are independent in every LS sum, so splitting
-// them over 4/NC threads keeps each sum sequential in CSR order (bitwise)
-// while multiplying the threads in flight.  A 128-thread block covers
-// 128*NC/4 points; warp w handles component group w % (4/NC) of the
-// 32-point SELL slice w / (4/NC), so slice-local ELL offsets stay coalesced.
-template <int NC, int TB = kTB>
-KMF_HD void qg_thread(int &i, int &k0)
+// q-gradient kernels: NC components of one point per thread (NC = 4 above
+// 100K points, 2 below).  The four components of q are independent in every
+// LS sum, so splitting them over 4/NC threads keeps each sum sequential in
+// CSR order (bitwise) while multiplying the threads in flight.  A 128-thread
+// block covers 128*NC/4 points; warp w handles component group w % (4/NC) of
+// the 32-point SELL slice w / (4/NC), so slice-local ELL offsets stay
+// coalesced.
+template <int NC>
+KMF_HD void qg_thread(int lo, int &i, int &k0)
 {
-    constexpr int CG = 4 / NC;            // component groups per point
-    constexpr int P = TB / CG;            // points per block
+    constexpr int CG = 4 / NC;   // component groups per point
+    constexpr int P = kTB / CG;  // points per block
     const int w = threadIdx.x >> 5;
-    i = blockIdx.x * P + (w / CG) * 32 + (threadIdx.x & 31);
+    i = range_base(lo) + blockIdx.x * P + (w / CG) * 32 + (threadIdx.x & 31);
     k0 = (w % CG) * NC;
 }
 
-template <int NC, int TB = kTB>
-constexpr int qg_points_per_block() { return TB * NC / 4; }
+template <int NC>
+__host__ __device__ constexpr int qg_points_per_block() { return kTB * NC / 4; }
 
-// Shared-memory staging of a q-gradient block's ELL index slices (ST = 1):
-// one cooperative coalesced pass at block start instead of one dependent
-// index round trip per slot.  SPB = slices per block.
-template <int SPB>
-KMF_HD bool qg_stage_indices(const DG &g, int *sidx, int cap, int &e0)
-{
-    const int ns = (g.n + 31) >> 5;
-    const int s0 = blockIdx.x * SPB;
-    e0 = g.eoff[s0];
-    const int esz = g.eoff[min(s0 + SPB, ns)] - e0;
-    const bool staged = esz <= cap;
-    if (staged)
-        for (int e = threadIdx.x; e < esz; e += blockDim.x) sidx[e] = g.eidx[e0 + e];
-    __syncthreads();
-    return staged;
-}
-
-// ST = 2: the same staging as ONE TMA bulk copy.  The block's slices are
-// contiguous in the ELL table (offsets are multiples of 32 entries, so
-// the source is 128 B aligned and the size a multiple of 128 B); one
-// thread arms an mbarrier with the byte count and issues
-// cp.async.bulk global -> shared, every thread waits on the barrier's
-// phase.  No register staging, no per-thread load/store round trips.
+// The block's ELL index slices are contiguous in the ELL table (slice
+// offsets are multiples of 32 entries, so the source is 128 B aligned and
+// the size a multiple of 128 B): ONE TMA bulk copy stages them in shared
+// memory.  One thread arms an mbarrier with the byte count and issues
+// cp.async.bulk global -> shared; every thread waits on the barrier's phase.
+// Replaces one dependent index round trip per slot by a shared-memory read.
+// SPB = slices per block.
 KMF_HD uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 template <int SPB>
-KMF_HD bool qg_stage_indices_tma(const DG &g, int *sidx, int cap, int &e0, unsigned long long *mbar)
+KMF_HD bool qg_stage_indices_tma(const DG &g, int lo, int *sidx, int cap, int &e0, unsigned long long *mbar)
 {
     const int ns = (g.n + 31) >> 5;
-    const int s0 = blockIdx.x * SPB;
+    const int s0 = (range_base(lo) >> 5) + blockIdx.x * SPB;
+    if (s0 >= ns) return false;
     e0 = g.eoff[s0];
     const int esz = g.eoff[min(s0 + SPB, ns)] - e0;
     const bool staged = esz <= cap && esz > 0;
@@ -301,21 +284,26 @@ KMF_HD bool qg_stage_indices_tma(const DG &g, int *sidx, int cap, int &e0, unsig
     return staged;
 }
 
-// U >= 8 selects the software-pipelined slot loop instead (qg_pipeline):
-// the gathers of a later slot are issued before slot s is evaluated, so the
-// HBM/L2 round trip overlaps the arithmetic; the sums keep their order.
+// One neighbour slot as the q-gradient kernels consume it: the neighbour's
+// coordinates (XY) or the stored offsets (!XY), its q components k0.. and
+// (WG, the sweeps) its gradients.
 template <int NC, bool WG>
 struct QgSlot {
     double x, y, q[NC], gx[WG ? NC : 1], gy[WG ? NC : 1];
 };
 
-template <int NC, bool WG>
+template <bool XY, int NC, bool WG>
 KMF_HD void qg_gather(QgSlot<NC, WG> &o, const DG &g, const double *__restrict__ q, const double *__restrict__ G,
-                      int ld, int k0, int j)
+                      int ld, int k0, int j, int ent)
 {
-    const double2 pj = g.pxy[j];
-    o.x = pj.x;
-    o.y = pj.y;
+    if (XY) {
+        const double2 pj = g.pxy[j];
+        o.x = pj.x;
+        o.y = pj.y;
+    } else {
+        o.x = g.edx[ent];
+        o.y = g.edy[ent];
+    }
     qload_nc<NC>(q, j, k0, o.q);
 #pragma unroll
     for (int k = 0; k < NC; k++) {
@@ -327,58 +315,41 @@ KMF_HD void qg_gather(QgSlot<NC, WG> &o, const DG &g, const double *__restrict__
     }
 }
 
-// Drives the pipelined slot loop: gather(slot, o) loads a slot, eval(o)
-// accumulates it, slots are evaluated strictly in order 0..d-1, and slot
-// s + P (P = U - 7) is gathered before slot s is evaluated.  ptxas places
-// those loads after the arithmetic of slot s (their consumers sit across the
-// back edge), so the round trip overlaps the loop tail and the other warps;
-// a two-buffer variant unrolled by two that interleaves them with the
-// arithmetic measured 4 % slower at 2.5M / 10M, two slots ahead (P = 2, 138
-// registers) 28 % slower.
-template <int U, class Slot, class Gather, class Eval>
+// Software-pipelined slot loop: slot s+1 is gathered before slot s is
+// evaluated, so the HBM/L2 round trip of the next neighbour overlaps the
+// arithmetic of this one; slots are evaluated strictly in order 0..d-1 (the
+// sums keep their order).  Measured variants (round 1): two slots ahead
+// (138 registers) +28 %, unrolled by two with the loads interleaved into
+// the arithmetic +4 %.
+template <class Slot, class Gather, class Eval>
 KMF_HD void qg_pipeline(int d, Gather gather, Eval eval)
 {
     if (d <= 0) return;
-    constexpr int P = U - 7;
-    Slot buf[P];
-#pragma unroll
-    for (int p = 0; p < P; p++) gather(min(p, d - 1), buf[p]);
+    Slot cur;
+    gather(0, cur);
     for (int s = 0; s < d; s++) {
         Slot nxt;
-        gather(min(s + P, d - 1), nxt);
-        eval(buf[0]);
-#pragma unroll
-        for (int p = 0; p + 1 < P; p++) buf[p] = buf[p + 1];
-        buf[P - 1] = nxt;
+        gather(min(s + 1, d - 1), nxt);  // past the last slot: a redundant reload
+        eval(cur);
+        cur = nxt;
     }
 }
 
-// The edge loop is unrolled by U: the U neighbour indices, then all their
-// gathers, are issued before any arithmetic (U-fold memory-level
-// parallelism); the accumulation itself stays strictly in slot order and
-// tail slots are predicated off, so the result is unchanged bit for bit.
-
 // lsq.py:164-175 first_order_q_gradients -- bitwise (CSR-order sums, no FMA)
-// TB: block size.  Larger blocks with a ring-tiled point order
-// (reorder.ring_tiles) put several radially stacked slices on one SM, so
-// the neighbour rings they share are fetched into L1 once.
-template <bool XY, int NC, int U, int TB = kTB, int ST = 0, int MB = 0>
-__global__ void __launch_bounds__(TB, (MB ? MB : (NC == 4 && TB == 128 ? 8 : 0))) k_first_order(DG g, const double *__restrict__ q,
-                                                     double *__restrict__ G, Ctrl *c, int stage)
+template <bool XY, int NC>
+__global__ void __launch_bounds__(kTB, NC == 4 ? 8 : 0) k_first_order(DG g, int lo, int hi,
+                                                                     const double *__restrict__ q,
+                                                                     double *__restrict__ G, Ctrl *c, int stage)
 {
-    pdl_trigger();
-    constexpr int SPB = TB * NC / 4 / 32, CAP = ST ? SPB * 32 * 24 : 1;
+    constexpr int SPB = qg_points_per_block<NC>() / 32, CAP = SPB * 32 * 24;
     __shared__ __align__(128) int sidx[CAP];
     __shared__ unsigned long long mbar;
     int e0 = 0;
-    const bool staged = ST == 2   ? qg_stage_indices_tma<SPB>(g, sidx, CAP, e0, &mbar)
-                        : ST == 1 ? qg_stage_indices<SPB>(g, sidx, CAP, e0)
-                                  : false;
-    pdl_wait();
+    const bool staged = qg_stage_indices_tma<SPB>(g, lo, sidx, CAP, e0, &mbar);
     if (c && should_skip(c, stage, 0)) return;
     int i, k0;
-    qg_thread<NC, TB>(i, k0);
-    if (i >= g.n) return;
+    qg_thread<NC>(lo, i, k0);
+    if (i < lo || i >= hi) return;
     const int ld = g.ld;
     double qi[NC], sx[NC], sy[NC];
     qload_nc<NC>(q, i, k0, qi);
@@ -389,49 +360,22 @@ __global__ void __launch_bounds__(TB, (MB ? MB : (NC == 4 && TB == 128 ? 8 : 0))
     }
     const double xi = g.x[i], yi = g.y[i];
     const int base = ell_base(g, i), d = g.deg[i];
-    if constexpr (U >= 8 && XY && ST == 2) {
-        using Slot = QgSlot<NC, false>;
-        qg_pipeline<U, Slot>(
-            d,
-            [&](int s, Slot &o) {
-                qg_gather(o, g, q, q, ld, k0, staged ? sidx[base + s * 32 - e0] : g.eidx[base + s * 32]);
-            },
-            [&](const Slot &o) {
-                const double dx = SUB(o.x, xi), dy = SUB(o.y, yi);
+    using Slot = QgSlot<NC, false>;
+    qg_pipeline<Slot>(
+        d,
+        [&](int s, Slot &o) {
+            const int ent = base + s * 32;
+            qg_gather<XY, NC, false>(o, g, q, q, ld, k0, staged ? sidx[ent - e0] : g.eidx[ent], ent);
+        },
+        [&](const Slot &o) {
+            const double dx = XY ? SUB(o.x, xi) : o.x, dy = XY ? SUB(o.y, yi) : o.y;  // geometry.py:382-383
 #pragma unroll
-                for (int k = 0; k < NC; k++) {
-                    const double dq = SUB(o.q[k], qi[k]);
-                    sx[k] = ADD(sx[k], MUL(dx, dq));
-                    sy[k] = ADD(sy[k], MUL(dy, dq));
-                }
-            });
-    } else
-    for (int s0 = 0; s0 < d; s0 += U) {
-        int jj[U], ent[U];
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-            ent[u] = base + min(s0 + u, d - 1) * 32;
-            jj[u] = (ST && staged) ? sidx[ent[u] - e0] : g.eidx[ent[u]];
-        }
-        double dx[U], dy[U], qj[U][NC];
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-            edge_offsets<XY>(g, ent[u], jj[u], xi, yi, dx[u], dy[u]);
-#pragma unroll
-            for (int k = 0; k < NC; k++) qj[u][k] = q[4 * jj[u] + k0 + k];
-        }
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-            if (s0 + u < d) {
-#pragma unroll
-                for (int k = 0; k < NC; k++) {
-                    double dq = SUB(qj[u][k], qi[k]);
-                    sx[k] = ADD(sx[k], MUL(dx[u], dq));
-                    sy[k] = ADD(sy[k], MUL(dy[u], dq));
-                }
+            for (int k = 0; k < NC; k++) {
+                const double dq = SUB(o.q[k], qi[k]);
+                sx[k] = ADD(sx[k], MUL(dx, dq));
+                sy[k] = ADD(sy[k], MUL(dy, dq));
             }
-        }
-    }
+        });
     const double sxx = g.fsum[i], sxy = g.fsum[ld + i], syy = g.fsum[2 * ld + i], det = g.fsum[3 * ld + i];
 #pragma unroll
     for (int k = 0; k < NC; k++) {
@@ -442,25 +386,23 @@ __global__ void __launch_bounds__(TB, (MB ? MB : (NC == 4 && TB == 128 ? 8 : 0))
 
 // lsq.py:214-227 one Jacobi sweep of the defect-corrected gradients --
 // bitwise.  With want_res the max |new - old| (lsq.py:238-243) is reduced.
-template <bool XY, int NC, int U, int TB = kTB, int ST = 0, int MB = 0, bool OUTP = false>
-__global__ void __launch_bounds__(TB, MB) k_sweep(DG g, const double *__restrict__ q,
+// OUTP: the stage's last sweep writes the plane layout the flux and
+// boundary kernels read.
+template <bool XY, int NC, bool OUTP>
+__global__ void __launch_bounds__(kTB) k_sweep(DG g, int lo, int hi, const double *__restrict__ q,
                                                const double *__restrict__ Gin, double *__restrict__ Gout,
                                                Ctrl *c, int stage, int slot, int want_res)
 {
-    pdl_trigger();
-    constexpr int SPB = TB * NC / 4 / 32, CAP = ST ? SPB * 32 * 24 : 1;
+    constexpr int SPB = qg_points_per_block<NC>() / 32, CAP = SPB * 32 * 24;
     __shared__ __align__(128) int sidx[CAP];
     __shared__ unsigned long long mbar;
     int e0 = 0;
-    const bool staged = ST == 2   ? qg_stage_indices_tma<SPB>(g, sidx, CAP, e0, &mbar)
-                        : ST == 1 ? qg_stage_indices<SPB>(g, sidx, CAP, e0)
-                                  : false;
-    pdl_wait();
+    const bool staged = qg_stage_indices_tma<SPB>(g, lo, sidx, CAP, e0, &mbar);
     if (c && should_skip(c, stage, slot)) return;
     int i, k0;
-    qg_thread<NC, TB>(i, k0);
+    qg_thread<NC>(lo, i, k0);
     double rmax = 0.0;
-    if (i < g.n) {
+    if (i >= lo && i < hi) {
         const int ld = g.ld;
         double qi[NC], gxi[NC], gyi[NC], sx[NC], sy[NC];
         qload_nc<NC>(q, i, k0, qi);
@@ -474,63 +416,24 @@ __global__ void __launch_bounds__(TB, MB) k_sweep(DG g, const double *__restrict
         }
         const double xi = g.x[i], yi = g.y[i];
         const int base = ell_base(g, i), d = g.deg[i];
-        if constexpr (U >= 8 && XY && ST == 2) {
-            using Slot = QgSlot<NC, true>;
-            qg_pipeline<U, Slot>(
-                d,
-                [&](int s, Slot &o) {
-                    qg_gather(o, g, q, Gin, ld, k0, staged ? sidx[base + s * 32 - e0] : g.eidx[base + s * 32]);
-                },
-                [&](const Slot &o) {
-                    const double dx = SUB(o.x, xi), dy = SUB(o.y, yi);
-                    const double hdx = MUL(0.5, dx), hdy = MUL(0.5, dy);
-#pragma unroll
-                    for (int k = 0; k < NC; k++) {
-                        const double dq = SUB(qtilde_h(o.q[k], o.gx[k], o.gy[k], hdx, hdy),
-                                              qtilde_h(qi[k], gxi[k], gyi[k], hdx, hdy));
-                        sx[k] = ADD(sx[k], MUL(dx, dq));
-                        sy[k] = ADD(sy[k], MUL(dy, dq));
-                    }
-                });
-        } else
-        for (int s0 = 0; s0 < d; s0 += U) {
-            int jj[U], ent[U];
-#pragma unroll
-            for (int u = 0; u < U; u++) {
-                ent[u] = base + min(s0 + u, d - 1) * 32;
-                jj[u] = (ST && staged) ? sidx[ent[u] - e0] : g.eidx[ent[u]];
-            }
-            double dx[U], dy[U], qj[U][NC], gxj[U][NC], gyj[U][NC];
-#pragma unroll
-            for (int u = 0; u < U; u++) {
-                edge_offsets<XY>(g, ent[u], jj[u], xi, yi, dx[u], dy[u]);
+        using Slot = QgSlot<NC, true>;
+        qg_pipeline<Slot>(
+            d,
+            [&](int s, Slot &o) {
+                const int ent = base + s * 32;
+                qg_gather<XY, NC, true>(o, g, q, Gin, ld, k0, staged ? sidx[ent - e0] : g.eidx[ent], ent);
+            },
+            [&](const Slot &o) {
+                const double dx = XY ? SUB(o.x, xi) : o.x, dy = XY ? SUB(o.y, yi) : o.y;
+                const double hdx = MUL(0.5, dx), hdy = MUL(0.5, dy);  // exact: see qtilde_h
 #pragma unroll
                 for (int k = 0; k < NC; k++) {
-                    qj[u][k] = q[4 * jj[u] + k0 + k];
-                    const double2 v = gload_cm(Gin, ld, k0 + k, jj[u]);
-                    gxj[u][k] = v.x;
-                    gyj[u][k] = v.y;
+                    const double dq = SUB(qtilde_h(o.q[k], o.gx[k], o.gy[k], hdx, hdy),
+                                          qtilde_h(qi[k], gxi[k], gyi[k], hdx, hdy));
+                    sx[k] = ADD(sx[k], MUL(dx, dq));
+                    sy[k] = ADD(sy[k], MUL(dy, dq));
                 }
-            }
-#pragma unroll
-            for (int u = 0; u < U; u++) {
-                if (s0 + u < d) {
-                    // pre-halved offsets on the HBM-streaming shapes (-5 % there);
-                    // the 160K shape keeps the plain form (ptxas schedules it better)
-                    const double hdx = MUL(0.5, dx[u]), hdy = MUL(0.5, dy[u]);
-#pragma unroll
-                    for (int k = 0; k < NC; k++) {
-                        double ti = ST ? qtilde_h(qj[u][k], gxj[u][k], gyj[u][k], hdx, hdy)
-                                       : qtilde(qj[u][k], gxj[u][k], gyj[u][k], dx[u], dy[u]);
-                        double t0 = ST ? qtilde_h(qi[k], gxi[k], gyi[k], hdx, hdy)
-                                       : qtilde(qi[k], gxi[k], gyi[k], dx[u], dy[u]);
-                        double dq = SUB(ti, t0);
-                        sx[k] = ADD(sx[k], MUL(dx[u], dq));
-                        sy[k] = ADD(sy[k], MUL(dy[u], dq));
-                    }
-                }
-            }
-        }
+            });
         const double sxx = g.fsum[i], sxy = g.fsum[ld + i], syy = g.fsum[2 * ld + i],
                      det = g.fsum[3 * ld + i];
         double gxn[NC], gyn[NC];
@@ -539,15 +442,16 @@ __global__ void __launch_bounds__(TB, MB) k_sweep(DG g, const double *__restrict
             gxn[k] = DIV(SUB(MUL(syy, sx[k]), MUL(sxy, sy[k])), det);
             gyn[k] = DIV(SUB(MUL(sxx, sy[k]), MUL(sxy, sx[k])), det);
         }
-        gstore_nc<NC, OUTP>(Gout, ld, i, k0, gxn, gyn);  // OUTP: the stage's last sweep
+        gstore_nc<NC, OUTP>(Gout, ld, i, k0, gxn, gyn);
+        if (want_res) {
+            bool nan = false;
 #pragma unroll
-        for (int k = 0; k < NC; k++) {
-            const double nx_ = gxn[k], ny_ = gyn[k];
-            if (want_res) {
-                rmax = fmax(rmax, fabs(nx_ - gxi[k]));
-                rmax = fmax(rmax, fabs(ny_ - gyi[k]));
-                if (isnan(nx_ - gxi[k]) || isnan(ny_ - gyi[k])) rmax = __longlong_as_double(0x7ff8000000000000ll);
+            for (int k = 0; k < NC; k++) {
+                const double ex = gxn[k] - gxi[k], ey = gyn[k] - gyi[k];
+                rmax = fmax(rmax, fmax(fabs(ex), fabs(ey)));
+                nan |= isnan(ex) || isnan(ey);
             }
+            if (nan) rmax = __longlong_as_double(0x7ff8000000000000ll);  // np.max propagates NaN
         }
     }
     if (want_res) {
@@ -557,423 +461,6 @@ __global__ void __launch_bounds__(TB, MB) k_sweep(DG g, const double *__restrict
             b = t > b ? t : b;
         }
         if ((threadIdx.x & 31) == 0) atomicMax(&c->resmax, b);
-    }
-}
-
-// ---------------------------------------------------------------------------
-// solver.py:162-235 flux_residual (interior rows).  FAM < 0: fused, all four
-// split families in one pass over the stencil; FAM = 0..3: split4, one
-// family per launch, R accumulated in the order x+, x-, y+, y-.
-//
-// Per edge the two perturbed states q~_i, q~_0 (solver.py:184-185, bitwise)
-// are decoded ONCE and shared by the x- and the y-family flux of that edge
-// (the reference decodes them once per family).  The LS derivative of each
-// family is accumulated as sum_e w_f(e) * dG_f(e) with the static weight
-// w_f(e) = cx_f*dx + cy_f*dy (cx, cy = rows of the inverse 2x2 matrix,
-// solver.py:192-195), in CSR order per family.  Fused and split4 run the
-// same per-edge code and add families in the same order: bitwise equal.
-template <bool XY, int FAM, int MINB, int GK>
-__global__ void __launch_bounds__(kTB, MINB) k_flux(DG g, const double *__restrict__ q,
-                                              const double *__restrict__ G, double *__restrict__ R,
-                                              double inv_gm1, double c_i0, int zero_boundary, Ctrl *c,
-                                              int stage)
-{
-    if (c && should_skip(c, stage, kSlotFlux)) return;
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= g.n_act) return;
-    const int ld = g.ld;
-    const bool interior = g.flag[i] == 0;
-    // The owner's q, gradients and family weights are re-read from L1 per
-    // edge (through a laundered index the compiler cannot hoist) instead of
-    // being pinned in 40 registers: the kernel is occupancy-bound.
-    double acc[4][4];
-#pragma unroll
-    for (int f = 0; f < 4; f++)
-#pragma unroll
-        for (int k = 0; k < 4; k++) acc[f][k] = 0.0;
-
-    const double xi = g.x[i], yi = g.y[i];
-    const int base = ell_base(g, i), d = g.deg[i];
-    bool bad = false;
-    for (int s = 0; s < d; s++) {
-        const int ent = base + s * 32;
-        const int j = g.eidx[ent];
-        double dx, dy;
-        edge_offsets<XY>(g, ent, j, xi, yi, dx, dy);
-        if (FAM == 0 && !(dx <= 0.0)) continue;
-        if (FAM == 1 && !(dx >= 0.0)) continue;
-        if (FAM == 2 && !(dy <= 0.0)) continue;
-        if (FAM == 3 && !(dy >= 0.0)) continue;
-        int io;
-        asm volatile("mov.b32 %0, %1;" : "=r"(io) : "r"(i));
-        double ti[4], t0[4];
-#pragma unroll
-        for (int k = 0; k < 4; k++) {
-            ti[k] = qtilde(q[4 * j + k], gload(G, ld, k, j).x, gload(G, ld, k, j).y, dx, dy);
-            t0[k] = qtilde(q[4 * io + k], gload(G, ld, k, io).x, gload(G, ld, k, io).y, dx, dy);
-        }
-        const double *cf = g.fcoef + io;  // cf[k * ld]: (cx, cy) of x+, x-, y+, y-
-        // solver.py:164 positivity (q4 >= 0, NaN caught by q_to_primitives)
-        if (!(ti[3] < 0.0) || !(t0[3] < 0.0)) {
-            bad = true;
-            continue;
-        }
-        if (!interior) continue;  // rows zeroed (solver.py:233-234)
-        FState si, s0;
-        fdecode<GK>(ti[0], ti[1], ti[2], ti[3], inv_gm1, c_i0, si);
-        fdecode<GK>(t0[0], t0[1], t0[2], t0[3], inv_gm1, c_i0, s0);
-        double gi[4], g0[4];
-        if (FAM < 2) {
-            // x family: x+ holds dx <= 0 (tie in both), x- dx >= 0
-            const bool primary_p = FAM < 0 ? (dx <= 0.0) : (FAM == 0);
-            const double sg = primary_p ? 1.0 : -1.0;
-            const double cx = primary_p ? cf[0 * ld] : cf[2 * ld];
-            const double cy = primary_p ? cf[1 * ld] : cf[3 * ld];
-            fsflux(si, false, sg, gi);
-            fsflux(s0, false, sg, g0);
-            const double w = fma(cx, dx, cy * dy);
-#pragma unroll
-            for (int k = 0; k < 4; k++) {
-                double a = fma(w, gi[k] - g0[k], primary_p ? acc[0][k] : acc[1][k]);
-                if (primary_p)
-                    acc[0][k] = a;
-                else
-                    acc[1][k] = a;
-            }
-            if (FAM < 0 && dx == 0.0) {  // tie: also in x-
-                fsflux(si, false, -1.0, gi);
-                fsflux(s0, false, -1.0, g0);
-                const double w2 = fma(cf[2 * ld], dx, cf[3 * ld] * dy);
-#pragma unroll
-                for (int k = 0; k < 4; k++) acc[1][k] = fma(w2, gi[k] - g0[k], acc[1][k]);
-            }
-        }
-        if (FAM < 0 || FAM >= 2) {
-            const bool primary_p = FAM < 0 ? (dy <= 0.0) : (FAM == 2);
-            const double sg = primary_p ? 1.0 : -1.0;
-            const double cx = primary_p ? cf[4 * ld] : cf[6 * ld];
-            const double cy = primary_p ? cf[5 * ld] : cf[7 * ld];
-            fsflux(si, true, sg, gi);
-            fsflux(s0, true, sg, g0);
-            const double w = fma(cx, dx, cy * dy);
-#pragma unroll
-            for (int k = 0; k < 4; k++) {
-                double a = fma(w, gi[k] - g0[k], primary_p ? acc[2][k] : acc[3][k]);
-                if (primary_p)
-                    acc[2][k] = a;
-                else
-                    acc[3][k] = a;
-            }
-            if (FAM < 0 && dy == 0.0) {
-                fsflux(si, true, -1.0, gi);
-                fsflux(s0, true, -1.0, g0);
-                const double w2 = fma(cf[6 * ld], dx, cf[7 * ld] * dy);
-#pragma unroll
-                for (int k = 0; k < 4; k++) acc[3][k] = fma(w2, gi[k] - g0[k], acc[3][k]);
-            }
-        }
-    }
-    if (bad && c) raise_err(c, stage, kSlotFlux, 2 /*KMF_CTX_FLUX_XP: refined on host*/);
-    if (interior) {
-#pragma unroll
-        for (int k = 0; k < 4; k++) {
-            double r;
-            if (FAM < 0)
-                r = ADD(ADD(ADD(acc[0][k], acc[1][k]), acc[2][k]), acc[3][k]);
-            else if (FAM == 0)
-                r = acc[0][k];
-            else
-                r = ADD(R[k * ld + i], acc[FAM][k]);
-            R[k * ld + i] = r;
-        }
-    } else if (zero_boundary && FAM <= 0) {
-#pragma unroll
-        for (int k = 0; k < 4; k++) R[k * ld + i] = 0.0;
-    }
-}
-
-// ---------------------------------------------------------------------------
-// flux_residual, pair layout: TWO threads per point, one per edge END.
-// Lane 2p+0 ("A") builds q~_i from the neighbour's data, lane 2p+1 ("B")
-// q~_0 from the owner's; each decodes ONE state and evaluates the x- and
-// y-family split fluxes of it; one xor-1 shuffle of four values gives A the
-// x-family difference dG = G(q~_i) - G(q~_0) and B the y-family one.  A
-// accumulates x+/x-, B y+/y-, each in CSR order.  Per-thread state is
-// halved (one decoded state, eight accumulators), so twice the threads are
-// resident.  Per-edge arithmetic is exactly k_flux's (same device
-// functions), fused == split4 bitwise as before.
-template <bool XY, int FAM, int MINB, int GK>
-__global__ void __launch_bounds__(kTB, MINB) k_flux2(DG g, const double *__restrict__ q,
-                                                     const double *__restrict__ G, double *__restrict__ R,
-                                                     double inv_gm1, double c_i0, int zero_boundary, Ctrl *c,
-                                                     int stage)
-{
-    if (c && should_skip(c, stage, kSlotFlux)) return;
-    const unsigned FULL = 0xffffffffu;
-    const int lane = threadIdx.x & 31;
-    const bool roleA = (lane & 1) == 0;  // A: neighbour end (x families); B: owner end (y families)
-    const int i = blockIdx.x * (kTB / 2) + (threadIdx.x >> 1);
-    const bool valid = i < g.n_act;
-    const int ld = g.ld;
-    const int ii = valid ? i : 0;
-    const bool interior = valid && g.flag[ii] == 0;
-    const int d = valid ? g.deg[ii] : 0;
-    const int dmax = __reduce_max_sync(FULL, d);
-    // owner data (used by B for q~_0; A keeps the same registers idle)
-    double qi[4], gxi[4], gyi[4];
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-        qi[k] = q[4 * ii + k];
-        gxi[k] = gload(G, ld, k, ii).x;
-        gyi[k] = gload(G, ld, k, ii).y;
-    }
-    // this lane's two families: A -> (x+, x-), B -> (y+, y-)
-    const double cP_x = interior ? g.fcoef[(roleA ? 0 : 4) * ld + ii] : 0.0;
-    const double cP_y = interior ? g.fcoef[(roleA ? 1 : 5) * ld + ii] : 0.0;
-    const double cM_x = interior ? g.fcoef[(roleA ? 2 : 6) * ld + ii] : 0.0;
-    const double cM_y = interior ? g.fcoef[(roleA ? 3 : 7) * ld + ii] : 0.0;
-    double accP[4] = {0.0, 0.0, 0.0, 0.0}, accM[4] = {0.0, 0.0, 0.0, 0.0};
-    const double xi = g.x[ii], yi = g.y[ii];
-    const int base = ell_base(g, ii);
-    bool bad = false;
-    for (int s = 0; s < dmax; s++) {
-        const bool live = s < d;
-        const int ent = base + min(s, d > 0 ? d - 1 : 0) * 32;
-        const int j = valid ? g.eidx[ent] : 0;
-        double dx, dy;
-        edge_offsets<XY>(g, ent, j, xi, yi, dx, dy);
-        bool member = live;
-        if (FAM == 0) member = member && (dx <= 0.0);
-        if (FAM == 1) member = member && (dx >= 0.0);
-        if (FAM == 2) member = member && (dy <= 0.0);
-        if (FAM == 3) member = member && (dy >= 0.0);
-        const int p = roleA ? j : ii;  // which end this lane perturbs
-        double t[4];
-#pragma unroll
-        for (int k = 0; k < 4; k++) {
-            const double qq = roleA ? q[4 * p + k] : qi[k];
-            const double gx = roleA ? gload(G, ld, k, p).x : gxi[k];
-            const double gy = roleA ? gload(G, ld, k, p).y : gyi[k];
-            t[k] = qtilde(qq, gx, gy, dx, dy);  // solver.py:184-185, bitwise
-        }
-        const double t4o = __shfl_xor_sync(FULL, t[3], 1);
-        const bool ok = (t[3] < 0.0) && (t4o < 0.0);
-        if (member && !ok) bad = true;
-        const bool work = member && ok && interior;
-        FState st;
-        fdecode<GK>(t[0], t[1], t[2], t[3], inv_gm1, c_i0, st);
-        double gxf[4], gyf[4], snd[4], rcv[4];
-        const bool px = dx <= 0.0, py = dy <= 0.0;
-        if (FAM < 2) fsflux(st, false, (FAM < 0 ? px : FAM == 0) ? 1.0 : -1.0, gxf);
-        if (FAM < 0 || FAM >= 2) fsflux(st, true, (FAM < 0 ? py : FAM == 2) ? 1.0 : -1.0, gyf);
-#pragma unroll
-        for (int k = 0; k < 4; k++) {
-            if (FAM < 0) snd[k] = roleA ? gyf[k] : gxf[k];
-            else snd[k] = FAM < 2 ? gxf[k] : gyf[k];
-            rcv[k] = __shfl_xor_sync(FULL, snd[k], 1);
-        }
-        // A owns the x families, B the y families
-        const bool mine = FAM < 0 ? true : (FAM < 2 ? roleA : !roleA);
-        if (work && mine) {
-            const bool plus = FAM < 0 ? (roleA ? px : py) : (FAM == 0 || FAM == 2);
-            const double w = plus ? fma(cP_x, dx, cP_y * dy) : fma(cM_x, dx, cM_y * dy);
-#pragma unroll
-            for (int k = 0; k < 4; k++) {
-                // dG = G(q~_i) - G(q~_0): A holds the i end, B the 0 end
-                const double own = (FAM < 0 ? (roleA ? gxf[k] : gyf[k]) : snd[k]);
-                const double dG = roleA ? own - rcv[k] : rcv[k] - own;
-                if (plus)
-                    accP[k] = fma(w, dG, accP[k]);
-                else
-                    accM[k] = fma(w, dG, accM[k]);
-            }
-        }
-        if (FAM < 0) {
-            // ties join both families of an axis (geometry.py:544-549)
-            const bool tie = live && ok && interior && (roleA ? dx == 0.0 : dy == 0.0);
-            if (__any_sync(FULL, live && (dx == 0.0 || dy == 0.0))) {
-                double gm[4];
-                const bool tx = dx == 0.0, ty = dy == 0.0;
-                // lanes evaluate the '-' flux of the axis their PAIR needs:
-                // the x- exchange serves A, the y- exchange serves B
-                if (__any_sync(FULL, tx)) {
-                    fsflux(st, false, -1.0, gm);
-#pragma unroll
-                    for (int k = 0; k < 4; k++) {
-                        const double o = __shfl_xor_sync(FULL, gm[k], 1);
-                        if (roleA && tie && tx) accM[k] = fma(fma(cM_x, dx, cM_y * dy), gm[k] - o, accM[k]);
-                    }
-                }
-                if (__any_sync(FULL, ty)) {
-                    fsflux(st, true, -1.0, gm);
-#pragma unroll
-                    for (int k = 0; k < 4; k++) {
-                        const double o = __shfl_xor_sync(FULL, gm[k], 1);
-                        if (!roleA && tie && ty) accM[k] = fma(fma(cM_x, dx, cM_y * dy), o - gm[k], accM[k]);
-                    }
-                }
-            }
-        }
-    }
-    if (__any_sync(FULL, bad) && c && lane == 0) raise_err(c, stage, kSlotFlux, 2);
-    // combine: R = ((x+ + x-) + y+) + y-, computed on the B lane
-    double r[4];
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-        const double mine = (FAM < 0) ? accP[k] + accM[k] : 0.0;  // A: x+ + x-
-        const double fromA = __shfl_xor_sync(FULL, mine, 1);
-        if (FAM < 0)
-            r[k] = (fromA + accP[k]) + accM[k];  // on B: ((x+ + x-) + y+) + y-
-        else if (FAM == 0 || FAM == 1)
-            r[k] = __shfl_xor_sync(FULL, FAM == 0 ? accP[k] : accM[k], 1);  // A's value onto B
-        else
-            r[k] = FAM == 2 ? accP[k] : accM[k];
-    }
-    if (!valid || roleA) return;
-    if (interior) {
-#pragma unroll
-        for (int k = 0; k < 4; k++) {
-            double v;
-            if (FAM < 0 || FAM == 0)
-                v = r[k];
-            else
-                v = ADD(R[k * ld + i], r[k]);
-            R[k * ld + i] = v;
-        }
-    } else if (zero_boundary && FAM <= 0) {
-#pragma unroll
-        for (int k = 0; k < 4; k++) R[k * ld + i] = 0.0;
-    }
-}
-
-// ---------------------------------------------------------------------------
-// solver.py:336-382 apply_boundary: wall / outer frame closures.  One warp
-// per boundary point; lanes stride over the frame edges of tplus, tminus
-// and the one-sided normal family; warp-tree sums (tolerance path).
-__device__ __forceinline__ double warp_sum(double v)
-{
-#pragma unroll
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
-
-template <int GK>
-__global__ void __launch_bounds__(kTB) k_boundary(DG g, DB b, const double *__restrict__ q,
-                                                  const double *__restrict__ G, double *__restrict__ R,
-                                                  double inv_gm1, double c_i0, double fsr, double fsu,
-                                                  double fsv, double fsp, Ctrl *c, int stage)
-{
-    if (c && should_skip(c, stage, kSlotFlux)) return;
-    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (w >= b.nb) return;  // whole warp leaves together
-    const int ld = g.ld;
-    const int pt = b.point[w];
-    const bool wall = b.type[w] == 1;
-    const double tx = b.frame[w], ty = b.frame[b.nb + w], nx = b.frame[2 * b.nb + w],
-                 ny = b.frame[3 * b.nb + w];
-    double qi[4], gxi[4], gyi[4];
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-        qi[k] = q[4 * pt + k];
-        gxi[k] = gload(G, ld, k, pt).x;
-        gyi[k] = gload(G, ld, k, pt).y;
-    }
-    // free-stream Maxwellian in this point's frame (solver.py:365-369)
-    double gfs[4] = {0, 0, 0, 0};
-    if (!wall) {
-        FState fs;
-        const double beta = fsr / (2.0 * fsp);
-        fs.rho = fsr;
-        fs.u1 = ADD(MUL(fsu, tx), MUL(fsv, ty));
-        fs.u2 = ADD(MUL(fsu, nx), MUL(fsv, ny));
-        fs.r = 1.0 / (2.0 * beta);
-        fs.sb = sqrt(beta);
-        fs.bc = rsqrt(beta) * kInv2SqrtPi;
-        fs.i0 = c_i0 * fs.r;
-        fsflux(fs, true, -1.0, gfs);
-    }
-    double acc[3][4];
-#pragma unroll
-    for (int f = 0; f < 3; f++)
-#pragma unroll
-        for (int k = 0; k < 4; k++) acc[f][k] = 0.0;
-    unsigned badmask = 0;
-#pragma unroll 1
-    for (int f = 0; f < 3; f++) {
-        const int e0 = b.ptr[f][w], e1 = b.ptr[f][w + 1];
-        const double ct = b.coef[(2 * f) * b.nb + w], cn = b.coef[(2 * f + 1) * b.nb + w];
-        for (int e = e0 + lane; e < e1; e += 32) {
-            const int j = b.idx[f][e];
-            const double dt = b.dt[f][e], dn = b.dn[f][e];
-            // solver.py:255-256 global offsets rebuilt from the rotated ones
-            const double dxg = ADD(MUL(dt, tx), MUL(dn, nx));
-            const double dyg = ADD(MUL(dt, ty), MUL(dn, ny));
-            double ti[4], t0[4];
-#pragma unroll
-            for (int k = 0; k < 4; k++) {
-                ti[k] = qtilde(q[4 * j + k], gload(G, ld, k, j).x, gload(G, ld, k, j).y, dxg, dyg);
-                t0[k] = qtilde(qi[k], gxi[k], gyi[k], dxg, dyg);
-            }
-            if (!(ti[3] < 0.0) || !(t0[3] < 0.0)) {
-                badmask |= 1u << f;
-                continue;
-            }
-            // _frame_q (solver.py:238-242): rotate the velocity pair
-            FState si, s0;
-            fdecode<GK>(ti[0], ADD(MUL(tx, ti[1]), MUL(ty, ti[2])), ADD(MUL(nx, ti[1]), MUL(ny, ti[2])), ti[3],
-                        inv_gm1, c_i0, si);
-            fdecode<GK>(t0[0], ADD(MUL(tx, t0[1]), MUL(ty, t0[2])), ADD(MUL(nx, t0[1]), MUL(ny, t0[2])), t0[3],
-                        inv_gm1, c_i0, s0);
-            double gi[4], g0[4], dg[4];
-            if (f < 2) {
-                const double sg = f == 0 ? 1.0 : -1.0;
-                fsflux(si, false, sg, gi);
-                fsflux(s0, false, sg, g0);
-#pragma unroll
-                for (int k = 0; k < 4; k++) dg[k] = gi[k] - g0[k];
-            } else if (wall) {
-                fsflux(si, true, -1.0, gi);
-                fsflux(s0, true, -1.0, g0);
-#pragma unroll
-                for (int k = 0; k < 4; k++) dg[k] = gi[k] - g0[k];
-            } else {
-                double gm[4];
-                fsflux(si, true, 1.0, gi);
-                fsflux(s0, true, 1.0, g0);
-                fsflux(si, true, -1.0, gm);
-#pragma unroll
-                for (int k = 0; k < 4; k++) dg[k] = (gi[k] - g0[k]) + (gm[k] - gfs[k]);
-            }
-            const double wgt = fma(ct, dt, cn * dn);
-#pragma unroll
-            for (int k = 0; k < 4; k++) acc[f][k] = fma(wgt, dg[k], acc[f][k]);
-        }
-    }
-#pragma unroll
-    for (int f = 0; f < 3; f++)
-#pragma unroll
-        for (int k = 0; k < 4; k++) acc[f][k] = warp_sum(acc[f][k]);
-    unsigned anybad = __reduce_or_sync(0xffffffffu, badmask);
-    if (lane == 0) {
-        if (anybad && c) {
-            if (anybad & 3u) raise_err(c, stage, kSlotFlux, wall ? 6 : 8);
-            if (anybad & 4u) raise_err(c, stage, kSlotFlux, wall ? 7 : 9);
-        }
-        double rows[4];
-#pragma unroll
-        for (int k = 0; k < 4; k++) {
-            double rt = acc[0][k] + acc[1][k];
-            if (wall)
-                rows[k] = rt + (k == 2 ? 0.0 : 2.0 * acc[2][k]);  // solver.py:303-309
-            else
-                rows[k] = rt + acc[2][k];  // solver.py:322-333
-        }
-        // _rotate_back solver.py:376-382
-        R[pt] = rows[0];
-        R[3 * ld + pt] = rows[3];
-        R[ld + pt] = ADD(MUL(tx, rows[1]), MUL(nx, rows[2]));
-        R[2 * ld + pt] = ADD(MUL(ty, rows[1]), MUL(ny, rows[2]));
     }
 }
 
@@ -1050,7 +537,7 @@ __device__ __noinline__ void close_iteration(Ctrl *c, const unsigned long long *
 }
 
 template <int STAGE>
-__global__ void __launch_bounds__(kTB) k_update(DG g, double *__restrict__ Uo, double *__restrict__ Us,
+__global__ void __launch_bounds__(kTB) k_update(DG g, int lo, int hi, double *__restrict__ Uo, double *__restrict__ Us,
                                                 const double *__restrict__ R, double *__restrict__ dt,
                                                 double *__restrict__ q, double gamma, double cfl, Ctrl *c,
                                                 IterOut io)
@@ -1063,10 +550,10 @@ __global__ void __launch_bounds__(kTB) k_update(DG g, double *__restrict__ Uo, d
         for (int t = threadIdx.x; t < kLimbs; t += blockDim.x) sl[t] = 0ull;
         __syncthreads();
     }
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = lo + blockIdx.x * blockDim.x + threadIdx.x;
     const int ld = g.ld;
     double dr2 = 0.0;
-    if (!skip && i < g.n_act) {
+    if (!skip && i < hi) {
         double uo[4], us[4], un[4];
         const double d = dt[i];
 #pragma unroll
@@ -1232,13 +719,14 @@ __global__ void k_init(DG g, const double *__restrict__ prims, const long long *
     dt[i] = timestep(rho, u1, u2, p, gamma, cfl, g.dmin[i]);
 }
 
-// continuation of a previous run: q and dt from the current U exactly as
-// the stage-4 update produced them (decode -> p2q / timestep, bitwise)
-__global__ void k_refresh(DG g, const double *__restrict__ Uo, double *__restrict__ q, double *__restrict__ dt,
-                          double gamma, double cfl)
+// continuation of a previous run: q and dt of slots [0, hi) from the current
+// U exactly as the stage-4 update produced them (decode -> p2q / timestep,
+// bitwise); under a partition the halo q then comes from its owners
+__global__ void k_refresh(DG g, int hi, const double *__restrict__ Uo, double *__restrict__ q,
+                          double *__restrict__ dt, double gamma, double cfl)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= g.n) return;
+    if (i >= hi) return;
     const int ld = g.ld;
     double u[4], qq[4], rho, u1, u2, p;
 #pragma unroll
@@ -1395,27 +883,6 @@ __global__ void k_op_u2p(int n, const double *U, double gamma, double *pr, unsig
     pr[3 * n + i] = p;
 }
 
-// kinetics.py:71-106 through the same device split flux the solver uses
-// (state primitives -> beta = rho/(2p) as the reference recomputes it)
-__global__ void k_op_split_flux(int n, const double *pr, int yaxis, double sg, double gamma, double *G)
-{
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    FState s;
-    s.rho = pr[i];
-    s.u1 = pr[n + i];
-    s.u2 = pr[2 * n + i];
-    const double p = pr[3 * n + i];
-    const double beta = s.rho / (2.0 * p);
-    s.r = 1.0 / (2.0 * beta);
-    s.sb = sqrt(beta);
-    s.bc = rsqrt(beta) * kInv2SqrtPi;
-    s.i0 = ((2.0 - gamma) / (gamma - 1.0)) * s.r;
-    double g[4];
-    fsflux(s, yaxis != 0, sg, g);
-    for (int k = 0; k < 4; k++) G[(long long)k * n + i] = g[k];
-}
-
 // kinetics.py:59-68
 __global__ void k_op_full_flux(int n, const double *pr, int yaxis, double gamma, double *F)
 {
@@ -1507,22 +974,3 @@ __global__ void k_fp64_peak(int iters, double seed, double *out)
 }
 }  // namespace kmf
 
-namespace kmf {
-// accuracy probe of the flux-path transcendentals (tests/test_gpu_fastmath.py)
-__global__ void k_fastmath_probe(int n, const double *x, int which, double *out)
-{
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const double v = x[i];
-    double r;
-    switch (which) {
-    case 0: r = fexp(v); break;
-    case 1: r = ferf(v, fexp(-(v * v))); break;
-    case 2: r = frcp(v); break;
-    case 4: r = fexp_tab(v, kExpT); break;
-    case 5: r = fexp_tab<false>(v, kExpT); break;
-    default: r = frsqrt(v); break;
-    }
-    out[i] = r;
-}
-}  // namespace kmf

@@ -9,11 +9,12 @@
 //    inputs these reproduce the reference bit for bit.
 //
 //  * TOLERANCE paths (perturbed-state decode and kinetic split fluxes inside
-//    flux_residual / apply_boundary): algebraically identical to the
-//    reference but re-associated for the FP64 pipe (reciprocal instead of
-//    three divisions, shared sqrt/rsqrt, explicit fma).  Deviation is a few
-//    ulp per flux value; the contract is
-//    |dR| <= 1e-11 * max(max|R_row|, 1) per call.
+//    flux_residual / apply_boundary, kmf_flux.cuh): algebraically identical
+//    to the reference but re-associated for the FP64 pipe (reciprocal
+//    instead of three divisions, shared sqrt/rsqrt, explicit fma, lean
+//    transcendentals of kmf_fastmath.cuh).  Deviation is a few ulp per flux
+//    value; the contract is |dR| <= 1e-11 * max(max|R_row|, 1)
+//    per call.
 //
 // The library is compiled with -fmad=false, so any fma() below is one the
 // source asked for explicitly; fused and split4 flux modes therefore share
@@ -106,64 +107,6 @@ KMF_HD double qtilde_h(double q, double gx, double gy, double hdx, double hdy)
     return SUB(q, ADD(MUL(hdx, gx), MUL(hdy, gy)));
 }
 
-// ------------------------------------------------------------- tolerance
-
-// Decoded perturbed edge state (state.py:141-163 restated for the FP64
-// pipe): beta = -q4/2, r = 1/(2 beta) = -1/q4, u = q*r, rho = exp(...).
-struct EState {
-    double rho, u1, u2, beta, r;
-};
-
-KMF_HD void decode(double q1, double q2, double q3, double q4, double inv_gm1, EState &s)
-{
-    s.beta = -0.5 * q4;
-    s.r = __drcp_rn(-q4);
-    s.u1 = q2 * s.r;
-    s.u2 = q3 * s.r;
-    double uu = fma(s.u1, s.u1, s.u2 * s.u2);
-    s.rho = exp(fma(s.beta, uu, fma(-log(s.beta), inv_gm1, q1)));
-}
-
-// Per-state quantities shared by every split flux of that state.
-struct EShared {
-    double sb;  // sqrt(beta)
-    double bc;  // 1/(2 sqrt(pi beta))
-    double i0;  // (2-gamma)/(2 beta (gamma-1))  kinetics.py:53-56
-};
-
-KMF_HD void shared_of(const EState &s, double c_i0, EShared &h)
-{
-    h.sb = sqrt(s.beta);
-    h.bc = rsqrt(s.beta) * kInv2SqrtPi;
-    h.i0 = c_i0 * s.r;
-}
-
-// kinetics.py:71-106 split_flux for one state.  yaxis selects G_y (normal
-// velocity u2), sg = +1 / -1 the half range.  Rows: x -> [rho m1, rho m2,
-// rho m1 ut, E], y -> [rho m1, rho m1 ut, rho m2, E].
-KMF_HD void sflux(const EState &s, const EShared &h, bool yaxis, double sg, double G[4])
-{
-    const double un = yaxis ? s.u2 : s.u1;
-    const double ut = yaxis ? s.u1 : s.u2;
-    const double r = s.r;  // 1/(2 beta)
-    double sarg = un * h.sb;
-    double E = erf(sarg);
-    double A = 0.5 * fma(sg, E, 1.0);
-    double B = exp(-(sarg * sarg)) * h.bc;
-    double sgB = sg * B;
-    double unsq = un * un;
-    double m1 = fma(un, A, sgB);
-    double m2 = fma(unsq + r, A, un * sgB);
-    double m3 = fma(fma(unsq, un, 3.0 * un * r), A, fma(2.0, r, unsq) * sgB);
-    double energy = s.rho * fma(fma(0.5 * ut, ut, fma(0.5, r, h.i0)), m1, 0.5 * m3);
-    double rm1 = s.rho * m1;
-    double rm2 = s.rho * m2;
-    G[0] = rm1;
-    G[1] = yaxis ? rm1 * ut : rm2;
-    G[2] = yaxis ? rm2 : rm1 * ut;
-    G[3] = energy;
-}
-
 // ------------------------------------------------- exact residue (fsum)
 //
 // Superaccumulator: a nonnegative double v = m * 2^(e2-1074), m < 2^53,
@@ -171,26 +114,5 @@ KMF_HD void sflux(const EState &s, const EShared &h, bool yaxis, double sg, doub
 // e2/32 .. e2/32+2.  Limb l weighs 2^(32 l - 1074).  Each limb absorbs
 // 2^32 additions before it could overflow (n <= 4e9 points).
 constexpr int kLimbs = 68;
-
-KMF_HD void accum_add(unsigned long long *limbs, double v)
-{
-    if (!(v > 0.0)) return;  // zeros (and the impossible negatives) add nothing
-    unsigned long long bits = (unsigned long long)__double_as_longlong(v);
-    int be = (int)(bits >> 52);
-    unsigned long long m = bits & ((1ull << 52) - 1);
-    int e2;
-    if (be == 0) {
-        e2 = 0;
-    } else {
-        m |= 1ull << 52;
-        e2 = be - 1;
-    }
-    int L = e2 >> 5, sh = e2 & 31;
-    unsigned long long lo = m << sh;                          // bits 0..63 of m<<sh
-    unsigned long long hi = sh ? (m >> (64 - sh)) : 0ull;      // bits 64..84
-    atomicAdd(&limbs[L], lo & 0xffffffffull);
-    atomicAdd(&limbs[L + 1], lo >> 32);
-    if (hi) atomicAdd(&limbs[L + 2], hi);
-}
 
 }  // namespace kmf

@@ -11,9 +11,13 @@ Two drivers share the partition of `partition.py` and the device kernels:
   (`kmf_nccl_init` + `kmf_run`).  torch.distributed only carries the NCCL
   unique id and the final error / state gathers (plumbing).
 
-In both, every rank runs the single-GPU arithmetic on its owned points, so
-the residue history is bitwise identical to `solver.solve` for any rank
-count (tests/test_gpu_dist.py, tests/test_partition.py).
+Both run the same per-stage schedule: an interior pass over the owned
+points that read no halo data of this stage, the halo exchange (under NCCL
+on a forked stream, overlapping the interior pass), then the band pass
+(partition.stage_ranges).  Every rank runs the single-GPU arithmetic on its
+owned points, so the residue history is bitwise identical to `solver.solve`
+for any rank count and ownership scheme (tests/test_gpu_dist.py,
+tests/test_partition.py).
 """
 
 from __future__ import annotations
@@ -25,13 +29,15 @@ import numpy as np
 from . import _lib
 from ._device import DeviceConnectivity
 from .geometry import Connectivity
-from .partition import LocalPart, build_part, owner_ranges, send_lists_for
+from .partition import LocalPart, build_part, owner_map, send_lists_for
 from .solver import SolverConfig, _params, initial_primitives
-from .state import PositivityError, Primitives, raise_decode_flags
+from .state import PositivityError, Primitives, prims_array, raise_decode_flags
 
 
 def attach_partition(dev: DeviceConnectivity, part: LocalPart) -> None:
     peers = sorted(set(part.send) | set(part.recv))
+    layer_end = np.ascontiguousarray(part.layer_counts, dtype=np.int64)
+    interior_end = np.ascontiguousarray(part.interior_end, dtype=np.int64)
     send_counts = np.array([part.send.get(p, np.empty(0)).size for p in peers], dtype=np.int64)
     recv_counts = np.array([part.recv.get(p, np.empty(0)).size for p in peers], dtype=np.int64)
     send = np.concatenate([part.send[p] for p in peers if p in part.send] or [np.empty(0, np.int64)]).astype(np.int64)
@@ -39,7 +45,8 @@ def attach_partition(dev: DeviceConnectivity, part: LocalPart) -> None:
     pr = (C.c_int * max(len(peers), 1))(*peers)
     keep = (send_counts, recv_counts, send, recv)
     _lib.check(
-        _lib.lib().kmf_set_partition(dev.handle, part.n_owned, part.n_global, part.rank, part.nranks, len(peers), pr,
+        _lib.lib().kmf_set_partition(dev.handle, part.n_owned, part.n_global, part.rank, part.nranks, part.depth,
+                                     _lib.i64ptr(layer_end), _lib.i64ptr(interior_end), len(peers), pr,
                                      _lib.i64ptr(keep[0]), _lib.i64ptr(keep[2]), _lib.i64ptr(keep[1]),
                                      _lib.i64ptr(keep[3])),
         "kmf_set_partition",
@@ -50,11 +57,13 @@ class RankPart:
     """One rank's partition and its device context."""
 
     def __init__(self, conn: Connectivity, rank: int, nranks: int, n_inner: int = 3, device: int | None = None,
-                 part: LocalPart | None = None):
+                 part: LocalPart | None = None, scheme: str = "bands", owner=None):
         depth = n_inner + 2
         if part is None:
-            part = build_part(conn, rank, nranks, depth)
-            part.send = send_lists_for(conn, rank, nranks, depth)
+            if owner is None:
+                owner = owner_map(conn.cloud, nranks, scheme)
+            part = build_part(conn, rank, nranks, depth, scheme, owner)
+            part.send = send_lists_for(conn, part, owner)
         self.part = part
         self.dev = DeviceConnectivity(part.conn, device=device)
         attach_partition(self.dev, part)
@@ -96,10 +105,17 @@ def _raise_merged_decode(fails, n_global: int) -> None:
 _C2P = (_lib.CTX_C2P_DENSITY, _lib.CTX_C2P_PRESSURE)
 
 
+def _check_depth(part: LocalPart, config) -> None:
+    n_inner = config.n_inner if getattr(config, "order", 2) == 2 else 0
+    if n_inner + 2 > part.depth:
+        raise ValueError(f"n_inner {n_inner} needs a halo of depth {n_inner + 2}; the partition was built with "
+                         f"depth {part.depth}")
+
+
 def _raise_rank_error(rp: RankPart, params) -> None:
     info = _rank_error(rp)
     try:
-        rp.dev.raise_positivity(info.context, info.stage, which=params.n_inner & 1, mode=params.mode,
+        rp.dev.raise_positivity(info.context, info.stage, which=_lib.DIAG_LAST_RUN, mode=params.mode,
                                 prefix=f"iteration {info.iteration}: ", gamma=params.gamma)
     except PositivityError as exc:
         idx = exc.indices
@@ -109,13 +125,14 @@ def _raise_rank_error(rp: RankPart, params) -> None:
 
 
 def solve_group(config: SolverConfig, cloud, conn: Connectivity, nranks: int, initial_state: Primitives | None = None,
-                devices=None):
-    """Partitioned solve in one process; returns (history, prims (4,n), U (4,n))."""
+                devices=None, scheme: str = "bands"):
+    """Partitioned solve in one process; returns (history, prims (4,n), U (4,n), converged)."""
     prims0 = (initial_state.copy() if initial_state is not None else initial_primitives(config, cloud))
     prims0.validate("initial state")
     devices = devices or [_lib.device_index()] * nranks
-    ranks = [RankPart(conn, r, nranks, config.n_inner, devices[r]) for r in range(nranks)]
-    g = prims0.as_array()
+    owner = owner_map(cloud, nranks, scheme)
+    ranks = [RankPart(conn, r, nranks, config.n_inner, devices[r], scheme=scheme, owner=owner) for r in range(nranks)]
+    g = prims_array(prims0)
     for rp in ranks:
         rp.set_state(g)
     p = _params(config)
@@ -125,7 +142,10 @@ def solve_group(config: SolverConfig, cloud, conn: Connectivity, nranks: int, in
     rc = _lib.lib().kmf_run_group(handles, nranks, C.byref(p), config.n_outer, _lib.dptr(hist), C.byref(done),
                                   C.byref(conv))
     if rc == _lib.KMF_EPOSITIVITY:
-        failed = [(rp, info) for rp in ranks for info in [_rank_error(rp)] if info.code == _lib.KMF_EPOSITIVITY]
+        # the reference raises at the earliest failing (iteration, stage)
+        # over the whole cloud
+        failed = sorted(((rp, info) for rp in ranks for info in [_rank_error(rp)]
+                         if info.code == _lib.KMF_EPOSITIVITY), key=lambda f: (f[1].iteration, f[1].stage))
         dec = [_decode_failures(rp, info, p) for rp, info in failed if info.context in _C2P]
         if dec and len(dec) == len(failed):
             _raise_merged_decode(dec, cloud.n_points)
@@ -150,8 +170,7 @@ def exchange_send_lists(part: LocalPart, dist) -> None:
     mine = {peer: part.global_ids[slots] for peer, slots in part.recv.items()}
     allrecv = [None] * part.nranks
     dist.all_gather_object(allrecv, mine)
-    b = owner_ranges(part.n_global, part.nranks)
-    part.send = {peer: np.asarray(r[part.rank]) - b[part.rank] for peer, r in enumerate(allrecv)
+    part.send = {peer: part.local_of_owned(np.asarray(r[part.rank])) for peer, r in enumerate(allrecv)
                  if peer != part.rank and part.rank in r}
 
 
@@ -159,10 +178,10 @@ class RankSolver:
     """This process's rank of an NCCL-partitioned solve (torchrun, one GPU
     per process).  `dist` is an initialised torch.distributed module."""
 
-    def __init__(self, conn: Connectivity, dist, n_inner: int = 3, device: int | None = None):
+    def __init__(self, conn: Connectivity, dist, n_inner: int = 3, device: int | None = None, scheme: str = "bands"):
         self.rank, self.nranks = dist.get_rank(), dist.get_world_size()
         self.dist = dist
-        part = build_part(conn, self.rank, self.nranks, n_inner + 2)
+        part = build_part(conn, self.rank, self.nranks, n_inner + 2, scheme)
         exchange_send_lists(part, dist)
         self.rp = RankPart(conn, self.rank, self.nranks, n_inner, device, part=part)
         uid = (C.c_char * 128)()
@@ -179,6 +198,7 @@ class RankSolver:
 
     def run(self, config: SolverConfig, prims_global: np.ndarray, n_iter: int):
         """Set the state and run; history is identical on every rank."""
+        _check_depth(self.rp.part, config)
         self.rp.set_state(prims_global)
         p = _params(config)
         hist = np.zeros(max(n_iter, 1))

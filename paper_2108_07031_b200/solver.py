@@ -35,6 +35,7 @@ from .state import (
     PositivityError,
     Primitives,
     conserved_to_primitives,
+    prims_array,
     free_stream,
 )
 
@@ -98,6 +99,12 @@ class SolveResult:
     converged: bool
 
 
+def config_order(config) -> int:
+    """Scheme order of a config: this package's extension field, or 2 for
+    the reference's own SolverConfig (which is always second order)."""
+    return int(getattr(config, "order", 2))
+
+
 def _params(config: SolverConfig, instrument: bool = False, timing_skip: int = 0) -> _lib.Params:
     fs = free_stream(config.mach, config.aoa_deg, config.gamma)
     p = _lib.Params()
@@ -105,7 +112,8 @@ def _params(config: SolverConfig, instrument: bool = False, timing_skip: int = 0
     p.cfl = config.cfl
     for i, v in enumerate((fs.rho[0], fs.u1[0], fs.u2[0], fs.p[0])):
         p.fs[i] = float(v)
-    p.n_inner = config.n_inner if config.order == 2 else 0  # 0: first-order scheme on the device
+    # the reference's SolverConfig has no `order` (solver.py:69-112): second order
+    p.n_inner = config.n_inner if config_order(config) == 2 else 0  # 0: first-order scheme on the device
     p.mode = MODES.index(config.mode)
     p.convergence_tol = config.convergence_tol if config.convergence_tol is not None else 0.0
     p.instrument = int(instrument)
@@ -121,7 +129,7 @@ def local_timestep(prims: Primitives, conn: Connectivity, cfl: float, gamma: flo
     if not 0.0 < cfl <= 1.0:
         raise ValueError("cfl must lie in (0, 1]")
     dev = device_for(conn)
-    pa = prims.as_array()
+    pa = prims_array(prims)
     dt = np.empty(pa.shape[1])
     _lib.check(_lib.lib().kmf_op_timestep(dev.handle, _lib.dptr(pa), cfl, gamma, _lib.dptr(dt)), "local_timestep")
     return dt
@@ -258,7 +266,7 @@ def solve(
     prims = initial_state.copy() if initial_state is not None else initial_primitives(config, cloud)
     prims.validate("initial state")
     dev = device_for(conn)
-    dev.set_state(prims.as_array())
+    dev.set_state(prims_array(prims))
 
     n_outer = config.n_outer
     skip = min(max(timing_skip, 0), n_outer) if instrument else n_outer

@@ -33,17 +33,23 @@ def test_bench_ours_contract(gpu):
     assert d["config"]["n_points"] == 40000 and "workload" in d["config"]
     assert d["e2e"]["h2d_bytes_per_step"] == 4 * 40000 * 8 and d["e2e"]["value"] > 0
     # per step: 4 stages x (first order + 3 sweeps + flux + boundary + update)
-    # = 28 in second order; c1 is BASELINE's first-order config: 4 x 3 = 12
-    assert d["config"]["order"] == 1 and d["gpu_launches"] == 3 * 12
+    # = 28 in the reference's second-order scheme (c1)
+    assert d["config"]["order"] == 2 and d["gpu_launches"] == 3 * 28
     for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
         assert k in d["roofline"]
     assert 0 < d["roofline"]["frac"] < 1
+    rq = d["roofline_qgrad"]
+    for kern in ("first_order", "sweep"):
+        assert 0 < rq[kern]["frac"] < 1.5 and rq[kern]["launch_us"] > 0
+    assert "algorithmic_achieved" not in d["roofline_fp64"]
     cb = d["cpu_baseline"]
     assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] > 0 and cb["sample"]
 
 
-def test_bench_reference_arm_contract(gpu):
-    d = run("--impl", "reference", "--config", "c1", "--steps", "1", "--warmup", "0")
-    assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "point-iterations/s"
-    assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
-    assert d["cpu_baseline"]["value"] == d["value"]
+def test_bench_first_order_config(gpu):
+    """c1o1: BASELINE configs[0]'s first-order scheme, labelled as such:
+    4 stages x (flux + boundary + update) = 12 launches per step."""
+    d = run("--config", "c1o1", "--steps", "3", "--warmup", "3", "--no-cpu-baseline")
+    assert d["config"]["order"] == 1 and d["gpu_launches"] == 3 * 12 and d["roofline_qgrad"] is None
+    assert "first order" in d["config"]["workload"]
+

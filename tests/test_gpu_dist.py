@@ -1,5 +1,8 @@
 """Partitioned device solve (2 and 3 ranks on one GPU through the group
-runner) reproduces the single-domain solve bit for bit."""
+runner, which runs the multi-process schedule: interior pass, halo
+exchange, band pass) reproduces the single-domain solve bit for bit, for
+both ownership schemes; the NCCL transport on one rank, and on two ranks
+when two GPUs are visible."""
 
 import numpy as np
 import pytest
@@ -11,12 +14,13 @@ from paper_2108_07031_b200.dist import solve_group
 pytestmark = pytest.mark.gpu
 
 
+@pytest.mark.parametrize("scheme", ["bands", "sectors"])
 @pytest.mark.parametrize("nranks", [2, 3])
-def test_group_solve_bitwise(gpu, nranks, small_naca, small_naca_conn):
+def test_group_solve_bitwise(gpu, nranks, scheme, small_naca, small_naca_conn):
     init = perturbed_state(small_naca)
     cfg = SolverConfig(mach=0.63, aoa_deg=2.0, n_outer=6)
     ref = solve(cfg, small_naca, small_naca_conn, initial_state=init, instrument=False)
-    hist, prims, U, conv = solve_group(cfg, small_naca, small_naca_conn, nranks, initial_state=init)
+    hist, prims, U, conv = solve_group(cfg, small_naca, small_naca_conn, nranks, initial_state=init, scheme=scheme)
     assert np.array_equal(hist, ref.residue_history)
     assert np.array_equal(prims, ref.primitives.as_array())
     assert np.array_equal(U, ref.conserved)
@@ -75,3 +79,101 @@ def test_nccl_rank_solver_world_one(gpu, small_naca, small_naca_conn, tmp_path):
         assert np.array_equal(prims, ref.primitives.as_array()[:, gid])
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode", ["fused", "split4"])
+def test_group_solve_first_order_and_split4(gpu, mode, small_naca, small_naca_conn):
+    """First-order scheme (no q-gradient kernels: the flux's own interior
+    range) and split4 under the partition schedule."""
+    init = perturbed_state(small_naca)
+    for order in (1, 2):
+        cfg = SolverConfig(mach=0.63, aoa_deg=2.0, n_outer=4, mode=mode, order=order)
+        ref = solve(cfg, small_naca, small_naca_conn, initial_state=init, instrument=False)
+        hist, prims, _, _ = solve_group(cfg, small_naca, small_naca_conn, 3, initial_state=init, scheme="sectors")
+        assert np.array_equal(hist, ref.residue_history)
+        assert np.array_equal(prims, ref.primitives.as_array())
+
+
+def test_group_rejects_shallow_halo(gpu, small_naca, small_naca_conn):
+    """A partition built for n_inner = 1 (depth 3) cannot run n_inner = 3:
+    the halo gradients would be inexact (ValueError, not silent drift)."""
+    import ctypes as C
+
+    from paper_2108_07031_b200 import _lib
+    from paper_2108_07031_b200.dist import RankPart
+    from paper_2108_07031_b200.solver import _params
+
+    ranks = [RankPart(small_naca_conn, r, 2, n_inner=1) for r in range(2)]
+    init = perturbed_state(small_naca).as_array()
+    for rp in ranks:
+        rp.set_state(init)
+    p = _params(SolverConfig(mach=0.63, aoa_deg=2.0, n_outer=2, n_inner=3))
+    h = (C.c_void_p * 2)(*[rp.dev.handle.value for rp in ranks])
+    hist = np.zeros(2)
+    done, conv = C.c_int(0), C.c_int(0)
+    rc = _lib.lib().kmf_run_group(h, 2, C.byref(p), 2, _lib.dptr(hist), C.byref(done), C.byref(conv))
+    assert rc == _lib.KMF_EINVAL
+    # one sweep fits the depth-3 halo and stays bitwise
+    cfg1 = SolverConfig(mach=0.63, aoa_deg=2.0, n_outer=3, n_inner=1)
+    ref = solve(cfg1, small_naca, small_naca_conn, initial_state=perturbed_state(small_naca), instrument=False)
+    p1 = _params(cfg1)
+    hist = np.zeros(3)
+    _lib.check(_lib.lib().kmf_run_group(h, 2, C.byref(p1), 3, _lib.dptr(hist), C.byref(done), C.byref(conv)), "group")
+    assert np.array_equal(hist, ref.residue_history)
+
+
+def _nccl_worker(rank, world, port, q):
+    import os
+
+    import torch.distributed as dist
+
+    from paper_2108_07031_b200 import SolverConfig as Cfg
+    from paper_2108_07031_b200 import build_stencils, generate_naca_cloud
+    from paper_2108_07031_b200.dist import RankSolver
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ["KMF_DEVICE"] = str(rank)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cloud = generate_naca_cloud(80, 30, 1.15, 20.0)
+        conn = build_stencils(cloud)
+        init = perturbed_state(cloud)
+        cfg = Cfg(mach=0.63, aoa_deg=2.0, n_outer=6)
+        rs = RankSolver(conn, dist, n_inner=cfg.n_inner, device=rank, scheme="sectors")
+        hist, conv = rs.run(cfg, init.as_array(), cfg.n_outer)
+        gid, prims, _ = rs.rp.owned_state()
+        q.put((rank, hist, gid, prims))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_two_ranks_bitwise(gpu, small_naca, small_naca_conn):
+    """Two processes, one GPU each, NCCL halo exchange overlapped inside the
+    iteration graph: bitwise the single-domain solve (needs 2 GPUs; NCCL
+    refuses two ranks on one device)."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    from paper_2108_07031_b200 import _lib
+
+    if _lib.lib().kmf_device_count() < 2:
+        pytest.skip("needs 2 visible GPUs (NCCL cannot place two ranks on one device)")
+    s_ = socket.socket()
+    s_.bind(("127.0.0.1", 0))
+    port = s_.getsockname()[1]
+    s_.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_nccl_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p_ in procs:
+        p_.start()
+    out = [q.get(timeout=300) for _ in range(2)]
+    for p_ in procs:
+        p_.join(timeout=60)
+    cfg = SolverConfig(mach=0.63, aoa_deg=2.0, n_outer=6)
+    ref = solve(cfg, small_naca, small_naca_conn, initial_state=perturbed_state(small_naca), instrument=False)
+    for rank, hist, gid, prims in out:
+        assert np.array_equal(hist, ref.residue_history)
+        assert np.array_equal(prims, ref.primitives.as_array()[:, gid])

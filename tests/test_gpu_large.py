@@ -1,11 +1,22 @@
-"""Full-size parity (BASELINE config 3: NACA 0012 2.5M points, M 0.85,
-AoA 1): the device path against the CPU oracle on the whole cloud.
+"""Full-size parity at the BASELINE configurations: the device path against
+the CPU oracle (pinned to the reference by tests/test_oracle_golden.py) and
+the reference's own fixtures.
 
-Sizes where the oracle still finishes in seconds: q-gradients (first order
-+ 3 sweeps) bitwise on the initial state, and three whole outer iterations
-(residue history <= 1e-10 relative, final primitives rtol 1e-10 / atol
-1e-12).  The connectivity comes from the native builder (bit-exact with the
-reference builder, tests/test_builder.py).
+* config 2 (160K): 1000 iterations against an oracle fixture
+  (tests/golden/c2o1000) and 20 against the reference itself;
+* config 3 (2.5M, M 0.85 AoA 1): q-gradients bitwise, three whole
+  iterations against the live oracle on the whole cloud, 50 iterations
+  against an oracle fixture (tests/golden/c3o50), two against the
+  reference itself, fused == split4, partitioned == single domain;
+* config 4 (10M): three whole iterations against the live oracle on the
+  whole cloud, fused == split4;
+* config 5 (40M, the bench's workload): one whole iteration against the
+  live oracle on all 39,992,976 points, fused == split4 over two.
+
+Residue histories within 1e-10 relative per iteration, final primitives
+rtol 1e-10 / atol 1e-12 (sampled where the fixture is a sample).  The
+connectivity comes from the native builder (bit-exact with the reference
+builder, tests/test_builder.py).
 """
 
 import numpy as np
@@ -45,6 +56,42 @@ def test_c3_q_gradients_bitwise(gpu, c3):
     assert np.array_equal(g.qx, qx) and np.array_equal(g.qy, qy)
 
 
+def _oracle_golden_case(name, cloud=None, conn=None, mode="fused"):
+    """Device solve of a tools/make_oracle_golden.py case against its fixture."""
+    from conftest import golden
+
+    A, meta = golden(name)
+    m, L, gr, ff = meta["params"]
+    if cloud is None:
+        cloud = generate_naca_cloud(m, L, gr, ff)
+        conn = build_stencils(cloud)
+    assert cloud.n_points == meta["n_points"]
+    cfg = SolverConfig(mach=meta["mach"], aoa_deg=meta["aoa"], n_outer=meta["iters"], mode=mode)
+    res = solve(cfg, cloud, conn, instrument=False)
+    assert res.iterations == meta["iters"]
+    rel = np.abs(res.residue_history - A["history"]) / A["history"]
+    idx = A["sample_idx"]
+    err = np.abs(res.primitives.as_array()[:, idx] - A["prims_sample"])
+    print(f"{name}: max residue rel diff {rel.max():.3e} (iteration {int(rel.argmax()) + 1}), "
+          f"max sampled state abs diff {err.max():.3e}")
+    assert rel.max() <= 1e-10, rel.max()
+    assert np.allclose(res.primitives.as_array()[:, idx], A["prims_sample"], rtol=1e-10, atol=1e-12)
+    return res
+
+
+def test_c2_thousand_iterations_match_oracle(gpu):
+    """BASELINE configs[1] (160K points, M 0.63, AoA 2) for the paper's 1000
+    iterations against the oracle's history and state sample."""
+    _oracle_golden_case("c2o1000")
+
+
+def test_c3_fifty_iterations_match_oracle(gpu, c3):
+    """Config 3 (HBM-streaming sizes: one thread per point, TMA-staged
+    indices, pipelined gathers) for 50 iterations of the transonic case."""
+    cloud, conn, _, _, _ = c3
+    _oracle_golden_case("c3o50", cloud, conn)
+
+
 def test_c3_three_iterations_match_oracle(gpu, c3):
     cloud, conn, cfg, init, pk = c3
     res = solve(cfg, cloud, conn, initial_state=init, instrument=False)
@@ -68,16 +115,17 @@ def test_c3_fused_equals_split4_bitwise(gpu, c3):
     assert np.array_equal(a.primitives.as_array(), b.primitives.as_array())
 
 
-def test_c3_partitioned_solve_bitwise(gpu, c3):
-    """Two partitions of the 2.5M cloud (1.25M owned points each: the
-    HBM-streaming kernel variants, on partitioned contexts) reproduce the
-    single-domain history and state bit for bit."""
+@pytest.mark.parametrize("scheme,nranks", [("bands", 2), ("sectors", 4)])
+def test_c3_partitioned_solve_bitwise(gpu, c3, scheme, nranks):
+    """Partitions of the 2.5M cloud (0.6-1.25M owned points each: the
+    HBM-streaming kernel shapes on partitioned contexts, interior and band
+    passes) reproduce the single-domain history and state bit for bit."""
     from paper_2108_07031_b200.dist import solve_group
 
     cloud, conn, cfg, init, _ = c3
     two = SolverConfig(mach=0.85, aoa_deg=1.0, n_outer=2)
     ref = solve(two, cloud, conn, initial_state=init, instrument=False)
-    hist, prims, U, _ = solve_group(two, cloud, conn, 2, initial_state=init)
+    hist, prims, U, _ = solve_group(two, cloud, conn, nranks, initial_state=init, scheme=scheme)
     assert np.array_equal(hist, ref.residue_history)
     assert np.array_equal(prims, ref.primitives.as_array())
 
@@ -108,80 +156,85 @@ def test_c3_two_iterations_match_reference(gpu, c3):
     idx = A["sample_idx"]
     assert np.allclose(res.primitives.as_array()[:, idx], A["prims_sample"], rtol=1e-10, atol=1e-12)
 
-# --------------------------------------------------------------- 40M (opt-in)
-# The bench's default configuration (BASELINE configs[4]): one whole outer
-# iteration of the device path against the oracle on all 39,992,976 points,
-# plus fused == split4 bitwise.  ~4 min and ~70 GB of host memory, so it runs
-# only with KMF_FULL_SIZE_TESTS=1 (results: profiles/r1_full_size_parity.txt).
+# ------------------------------------------------------------ 10M and 40M
+# Whole-cloud oracle runs: config 4 needs ~25 GB and config 5 ~75 GB of
+# host memory (connectivity + packed oracle copy); the driver's B200 boxes
+# have 196 GB.
 
-full_size = pytest.mark.skipif(not __import__("os").environ.get("KMF_FULL_SIZE_TESTS"),
-                               reason="set KMF_FULL_SIZE_TESTS=1 (40M points, ~4 min, ~70 GB host memory)")
+
+def _host_gb():
+    import psutil
+
+    return psutil.virtual_memory().total / 2**30
+
+
+def _whole_cloud_oracle(cloud, conn, cfg, init, label):
+    import os
+    import time
+
+    t = time.perf_counter()
+    res = solve(cfg, cloud, conn, initial_state=init, instrument=False)
+    t_gpu = time.perf_counter() - t
+    O.set_threads(os.cpu_count() or 1)
+    fs = free_stream(cfg.mach, cfg.aoa_deg)
+    t = time.perf_counter()
+    hist, prims, _, its, _ = O.solve(O.Packed(conn), init.as_array(), [fs.rho[0], fs.u1[0], fs.u2[0], fs.p[0]],
+                                     cfg.n_outer)
+    t_cpu = time.perf_counter() - t
+    assert res.iterations == its == cfg.n_outer
+    rel = np.abs(res.residue_history - hist) / hist
+    err = np.abs(res.primitives.as_array() - prims) / (1e-12 + 1e-10 * np.abs(prims))
+    print(f"{label}: {cloud.n_points} points x {cfg.n_outer} iterations: residue rel diff {rel.max():.3e}, max "
+          f"scaled state error {err.max():.3e}; device solve {t_gpu:.1f} s (incl. context), oracle {t_cpu:.1f} s")
+    assert rel.max() <= 1e-10
+    assert np.allclose(res.primitives.as_array(), prims, rtol=1e-10, atol=1e-12)
+
+
+def _fused_equals_split4(cloud, conn, init, mach, aoa):
+    a = solve(SolverConfig(mach=mach, aoa_deg=aoa, n_outer=2, mode="fused"), cloud, conn, initial_state=init,
+              instrument=False)
+    b = solve(SolverConfig(mach=mach, aoa_deg=aoa, n_outer=2, mode="split4"), cloud, conn, initial_state=init,
+              instrument=False)
+    assert np.array_equal(a.residue_history, b.residue_history)
+    assert np.array_equal(a.primitives.as_array(), b.primitives.as_array())
+
+
+@pytest.fixture(scope="module")
+def c4():
+    if _host_gb() < 48:
+        pytest.skip(f"config 4 needs ~25 GB of host memory, this host has {_host_gb():.0f} GB")
+    cloud = generate_naca_cloud(6324, 1581, 1.003647, 20.0)
+    conn = build_stencils(cloud)
+    cfg = SolverConfig(mach=0.63, aoa_deg=2.0, n_outer=3)
+    return cloud, conn, cfg, initial_primitives(cfg, cloud)
+
+
+def test_c4_three_iterations_match_oracle(gpu, c4):
+    _whole_cloud_oracle(*c4, "c4")
+
+
+def test_c4_fused_equals_split4_bitwise(gpu, c4):
+    cloud, conn, cfg, init = c4
+    _fused_equals_split4(cloud, conn, init, cfg.mach, cfg.aoa_deg)
 
 
 @pytest.fixture(scope="module")
 def c5():
+    if _host_gb() < 120:
+        pytest.skip(f"config 5 needs ~75 GB of host memory, this host has {_host_gb():.0f} GB")
     cloud = generate_naca_cloud(12648, 3162, 1.001821, 20.0)
     conn = build_stencils(cloud)
     cfg = SolverConfig(mach=0.63, aoa_deg=2.0, n_outer=1)
     return cloud, conn, cfg, initial_primitives(cfg, cloud)
 
 
-@full_size
 def test_c5_one_iteration_matches_oracle(gpu, c5):
-    import os
-    import time
-
-    cloud, conn, cfg, init = c5
-    t = time.perf_counter()
-    res = solve(cfg, cloud, conn, initial_state=init, instrument=False)
-    t_gpu = time.perf_counter() - t
-    O.set_threads(os.cpu_count() or 1)
-    pk = O.Packed(conn)
-    fs = free_stream(cfg.mach, cfg.aoa_deg)
-    t = time.perf_counter()
-    hist, prims, _, _, _ = O.solve(pk, init.as_array(), [fs.rho[0], fs.u1[0], fs.u2[0], fs.p[0]], 1)
-    t_cpu = time.perf_counter() - t
-    rel = abs(res.residue_history[0] - hist[0]) / hist[0]
-    err = np.abs(res.primitives.as_array() - prims) / (1e-12 + 1e-10 * np.abs(prims))
-    print(f"c5 one iteration: residue rel diff {rel:.3e}, max scaled state error {err.max():.3e}; "
-          f"device solve {t_gpu:.1f} s (incl. context), oracle {t_cpu:.1f} s")
-    assert rel <= 1e-10
-    assert np.allclose(res.primitives.as_array(), prims, rtol=1e-10, atol=1e-12)
+    _whole_cloud_oracle(*c5, "c5")
 
 
-@full_size
 def test_c5_fused_equals_split4_bitwise(gpu, c5):
     cloud, conn, cfg, init = c5
-    a = solve(SolverConfig(mach=0.63, aoa_deg=2.0, n_outer=2, mode="fused"), cloud, conn, initial_state=init,
-              instrument=False)
-    b = solve(SolverConfig(mach=0.63, aoa_deg=2.0, n_outer=2, mode="split4"), cloud, conn, initial_state=init,
-              instrument=False)
-    assert np.array_equal(a.residue_history, b.residue_history)
-    assert np.array_equal(a.primitives.as_array(), b.primitives.as_array())
-
-
-@full_size
-def test_c2_thousand_iterations_match_oracle(gpu):
-    """BASELINE configs[1] (160K points, M 0.63, AoA 2) for the paper's 1000
-    iterations: residue history within 1e-10 relative per iteration and
-    final primitives within rtol 1e-10 / atol 1e-12 of the oracle."""
-    import os
-
-    cloud = generate_naca_cloud(800, 200, 1.03, 20.0)
-    conn = build_stencils(cloud)
-    cfg = SolverConfig(mach=0.63, aoa_deg=2.0, n_outer=1000)
-    init = initial_primitives(cfg, cloud)
-    res = solve(cfg, cloud, conn, initial_state=init, instrument=False)
-    O.set_threads(os.cpu_count() or 1)
-    fs = free_stream(cfg.mach, cfg.aoa_deg)
-    hist, prims, _, its, _ = O.solve(O.Packed(conn), init.as_array(), [fs.rho[0], fs.u1[0], fs.u2[0], fs.p[0]], 1000)
-    assert res.iterations == its == 1000
-    rel = np.abs(res.residue_history - hist) / hist
-    err = np.abs(res.primitives.as_array() - prims) / (1e-12 + 1e-10 * np.abs(prims))
-    print(f"c2 1000 iterations: max residue rel diff {rel.max():.3e} (at iteration {int(rel.argmax()) + 1}), "
-          f"max scaled state error {err.max():.3e}; residue {hist[0]:.6e} -> {hist[-1]:.6e}")
-    assert rel.max() <= 1e-10
-    assert np.allclose(res.primitives.as_array(), prims, rtol=1e-10, atol=1e-12)
+    _fused_equals_split4(cloud, conn, init, cfg.mach, cfg.aoa_deg)
 
 
 # ------------------------------------------ against the reference itself

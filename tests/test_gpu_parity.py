@@ -102,21 +102,41 @@ def test_fused_equals_split4_bitwise(gpu, pre, small_golden, small_naca_conn):
     assert np.array_equal(a, b)
 
 
-@pytest.mark.parametrize("impl", ["3", "4", "5", "6", "7"])
-def test_flux_kernel_variants_fused_split4_and_tolerance(gpu, impl, small_golden, small_naca, monkeypatch):
-    """Every flux kernel variant (lock-step, + L1 prefetch, lean arithmetic,
-    both, lean + next edge in registers = the default): fused == split4
-    bitwise and the reference tolerance per call.  The variant is fixed when
-    a context is created, so each case builds a fresh connectivity."""
-    monkeypatch.setenv("KMF_FLUX_IMPL", impl)
-    conn = build_stencils(small_naca)
+def _stored_offset_twin(conn):
+    """The same Connectivity with one interior point's coordinates nudged by
+    an ulp after the stencils were built: full.dx/dy no longer equal
+    x[j] - x[i] bitwise there, so the device stores the ELL offsets and runs
+    its stored-offset kernels (k_first_order / k_sweep / k_flux <XY = false>)
+    on exactly the reference's offsets."""
+    import copy
+
+    twin = copy.copy(conn)
+    cl = copy.copy(conn.cloud)
+    cl.x = conn.cloud.x.copy()
+    i = int(np.flatnonzero(cl.flag == 0)[len(cl.x) // 3])
+    cl.x[i] = np.nextafter(cl.x[i], np.inf)
+    twin.cloud = cl
+    return twin
+
+
+def test_stored_offset_kernels_bitwise(gpu, small_golden, small_naca, small_naca_conn):
+    """Stored-offset kernel path == coordinate path, bit for bit: q-gradients,
+    fused and split4 flux, and a 3-iteration solve."""
+    twin = _stored_offset_twin(small_naca_conn)
+    G, _ = small_golden
     for pre in PREFIXES:
-        G, _ = small_golden
-        a = flux_residual(flow(G, pre), conn, "fused")
-        b = flux_residual(flow(G, pre), conn, "split4")
-        assert np.array_equal(a, b)
-        ref = G[f"{pre}.R_int"]
-        assert np.all(np.abs(a - ref) <= flux_tol(ref))
+        q = G[f"{pre}.q"]
+        a, b = compute_q_derivatives(q, small_naca_conn, 3), compute_q_derivatives(q, twin, 3)
+        assert np.array_equal(a.qx, b.qx) and np.array_equal(a.qy, b.qy)
+        for mode in ("fused", "split4"):
+            assert np.array_equal(flux_residual(flow(G, pre), small_naca_conn, mode),
+                                  flux_residual(flow(G, pre), twin, mode))
+    cfg = SolverConfig(mach=0.63, aoa_deg=2.0, n_outer=3)
+    init = Primitives.from_array(G["pert.prims"])
+    ra = solve(cfg, small_naca, small_naca_conn, initial_state=init, instrument=False)
+    rb = solve(cfg, twin.cloud, twin, initial_state=init, instrument=False)
+    assert np.array_equal(ra.residue_history, rb.residue_history)
+    assert np.array_equal(ra.conserved, rb.conserved)
 
 
 @pytest.mark.parametrize("pre", PREFIXES)

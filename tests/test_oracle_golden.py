@@ -183,3 +183,40 @@ def test_first_order_scheme_against_reference_operators(small_naca_conn):
         ref = A[f"{tag}.history"]
         assert np.all(np.abs(hist - ref) <= 1e-10 * ref)
         assert np.allclose(prims, A[f"{tag}.prims"], rtol=1e-10, atol=1e-12)
+
+
+GAMMAS = (5.0 / 3.0, 1.3)
+
+
+@pytest.mark.parametrize("gamma", GAMMAS)
+def test_gamma_split_flux_and_q(gamma):
+    """Split fluxes and entropy variables at gamma = 5/3 and 1.3 (the
+    decode's 5/3 and generic evaluation paths) against the reference."""
+    K, _ = golden("kinetics")
+    A, _ = golden("gammas")
+    tag = f"g{gamma:.4f}"
+    q = O.primitives_to_q(K["prims"], gamma)
+    assert np.all(np.abs(q - A[f"{tag}.q"]) <= 4 * np.spacing(np.abs(A[f"{tag}.q"])))
+    for axis in ("x", "y"):
+        for sign in ("+", "-"):
+            ref = A[f"{tag}.split_{axis}{sign}"]
+            got = O.split_flux(K["prims"], axis, sign, gamma)
+            assert np.all(np.abs(got - ref) <= 1e-13 * np.maximum(np.abs(ref), 1.0))
+
+
+@pytest.mark.parametrize("gamma", GAMMAS)
+def test_gamma_residual_and_history(gamma, small_naca, oracle_small):
+    A, _ = golden("gammas")
+    tag = f"g{gamma:.4f}"
+    q = O.primitives_to_q(A[f"{tag}.prims"], gamma)
+    qx, qy, _ = O.q_derivatives(oracle_small, q, 3)
+    R = O.flux_residual(oracle_small, q, qx, qy, "fused", gamma)
+    assert np.all(np.abs(R - A[f"{tag}.R_int"]) <= flux_tol(A[f"{tag}.R_int"]))
+    Rb = O.apply_boundary(oracle_small, q, qx, qy, fs_vec(0.63, 2.0, gamma), R, gamma)
+    assert np.all(np.abs(Rb - A[f"{tag}.R"]) <= flux_tol(A[f"{tag}.R"]))
+    from paper_2108_07031_b200 import SolverConfig, initial_primitives
+
+    init = initial_primitives(SolverConfig(mach=0.63, aoa_deg=2.0, gamma=gamma), small_naca)
+    hist, prims, *_ = O.solve(oracle_small, init.as_array(), fs_vec(0.63, 2.0, gamma), 20, gamma=gamma)
+    assert np.max(np.abs(hist - A[f"{tag}.history"]) / A[f"{tag}.history"]) <= 1e-10
+    assert np.allclose(prims, A[f"{tag}.final"], rtol=1e-10, atol=1e-12)

@@ -25,6 +25,9 @@ c40k       config 1 (bench.py:37 POINT_LEVELS["40k"]): digests + 1000-iter
            history + final state (long: ~35 min on 8 threads).
 c160k      config 2 (800, 200, 1.03): digests + 20-iter history.
 c2p5m      config 3 (3160, 790, 1.00734), M0.85 AoA1: digests + 2 iterations.
+gammas     gamma = 5/3 and 1.3 (the decode's other two evaluation paths): split
+           fluxes and entropy variables of the kinetics states, flux_residual +
+           apply_boundary on small_naca, and a 20-iteration solve.
 
 Every digest is sha256 over the little-endian C-contiguous bytes of the array
 cast to int64 (integer arrays) or float64 (real arrays).
@@ -251,6 +254,34 @@ def case_kinetics():
     save("kinetics", arrays, {"n": int(pr.n_points)})
 
 
+def case_gammas():
+    K = dict(np.load(OUT / "kinetics.npz"))
+    pr = Primitives(*K["prims"])
+    cloud = generate_naca_cloud(80, 30, 1.15, 20.0)
+    conn = build_stencils(cloud)
+    arrays, meta = {}, {"gammas": [5.0 / 3.0, 1.3], "params": [80, 30, 1.15, 20.0]}
+    for g in (5.0 / 3.0, 1.3):
+        tag = f"g{g:.4f}"
+        arrays[f"{tag}.q"] = primitives_to_q(pr, g)
+        for axis in ("x", "y"):
+            for sign in ("+", "-"):
+                arrays[f"{tag}.split_{axis}{sign}"] = split_flux(pr, axis, sign, g)
+        # one residual evaluation on the perturbed state of this gamma
+        prims = perturbed_state(cloud, gamma=g)
+        q = primitives_to_q(prims, g)
+        grads = compute_q_derivatives(q, conn, 3)
+        flow = FlowState(prims=prims, q=q, qx=grads.qx, qy=grads.qy)
+        R_int = flux_residual(flow, conn, "fused", g)
+        arrays[f"{tag}.prims"] = prims_arr(prims)
+        arrays[f"{tag}.R_int"] = R_int
+        arrays[f"{tag}.R"] = apply_boundary(flow, R_int.copy(), conn, free_stream(0.63, 2.0, g), g)
+        cfg = SolverConfig(mach=0.63, aoa_deg=2.0, gamma=g, cfl=0.2, n_outer=20, threads=8)
+        res = solve(cfg, cloud, conn, instrument=False)
+        arrays[f"{tag}.history"] = res.residue_history
+        arrays[f"{tag}.final"] = prims_arr(res.primitives)
+    save("gammas", arrays, meta)
+
+
 def lattice_cloud(n=5, h=1.0, classify_boundary=False):
     # restated from reference tests/conftest.py:7-28
     xs, ys = np.meshgrid(np.arange(n) * h, np.arange(n) * h, indexing="ij")
@@ -404,6 +435,7 @@ def main(argv):
         "small": case_small,
         "hist2k": case_hist2k,
         "kinetics": case_kinetics,
+        "gammas": case_gammas,
         "lattice": case_lattice,
         "order1": case_order1,
         "c40k": lambda: _big("c40k", (400, 100, 1.06), 0.63, 2.0, 1000),

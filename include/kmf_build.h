@@ -24,6 +24,12 @@ int kmfb_threads(void);
 int kmfb_knn(int64_t n, const double *x, const double *y, int k, int64_t nq, const int64_t *query,
              int64_t *counts, const int64_t *ptr, int64_t *rows);
 
+/* Replaces geometry.py:349-374 _radius_neighbors: every j != i with
+ * (x_j - x_i)^2 + (y_j - y_i)^2 < eps^2, ascending index.  Call once with
+ * rows == NULL to get counts[n], then with ptr = prefix sum to fill rows. */
+int kmfb_radius(int64_t n, const double *x, const double *y, double eps, int64_t *counts, const int64_t *ptr,
+                int64_t *rows);
+
 /* Replaces the edge loop of geometry.py:396-450 _visibility_filter given
  * the wall statistics (spacing, tol) computed as the reference does.
  * keep[e] = 1 for surviving edges of rows owned by owners[r] (r when NULL);

@@ -1,19 +1,20 @@
 """Native stencil builder: ``build_stencils`` at 10M/40M.
 
-Same result, bit for bit, as the reference builder (geometry.py:453-518,
-restated with scipy in ``geometry.build_stencils``); the heavy loops run in
-``libkmf_build.so`` (csrc/kmf_build.cpp, C++/OpenMP, C ABI in
-include/kmf_build.h):
+Same result, bit for bit, as the reference builder (geometry.py:453-518;
+its scipy restatement oracle/builder_ref.py is the tests' checker); the
+heavy loops run in ``libkmf_build.so`` (csrc/kmf_build.cpp, C++/OpenMP, C
+ABI in include/kmf_build.h):
 
-* tie-inclusive kNN rows (geometry.py:315-346) from a 2-d tree;
+* tie-inclusive kNN rows (geometry.py:315-346) and radius rows
+  (geometry.py:349-374) from a 2-d tree;
 * the visibility filter's edge loop (geometry.py:396-450) -- the wall
   statistics (spacing, thickness, tolerance) stay on cKDTree here because
   the 16-nearest tie order is part of their definition;
 * CSR offsets, full and sign-split LS sums, d_min / d_mean
   (geometry.py:375-393, 532-560).
 
-The deficiency scan, boundary frames and the widening pass are the host
-builder's own code.  Split families are never materialised: their sums,
+The deficiency scan, boundary frames (``frames``, geometry.py:573-646) and
+the widening pass are the host builder's own code.  Split families are never materialised: their sums,
 determinants and counts come from the native pass and their CSR arrays are
 derived from the full stencil on first access (``SplitView``), which keeps
 the host footprint at 40M points to the full stencil (~14 GB).
@@ -22,6 +23,7 @@ the host footprint at 40M points to the full stencil (~14 GB).
 from __future__ import annotations
 
 import ctypes as C
+from dataclasses import dataclass
 from pathlib import Path
 
 import numpy as np
@@ -48,7 +50,8 @@ def lib():
         L.kmfb_visibility.argtypes = [C.c_int64, _dp, _dp, C.c_int64, _i64p, _dp, _dp, _dp, _dp, C.c_int64, _i64p,
                                       _i64p, _i64p, _u8p, _i64p]
         L.kmfb_assemble.argtypes = [C.c_int64, _dp, _dp, _i64p, _i64p, _dp, _dp, _dp, _dp, _dp, _dp, _i64p]
-        for f in (L.kmfb_knn, L.kmfb_visibility, L.kmfb_assemble):
+        L.kmfb_radius.argtypes = [C.c_int64, _dp, _dp, C.c_double, _i64p, _i64p, _i64p]
+        for f in (L.kmfb_knn, L.kmfb_visibility, L.kmfb_assemble, L.kmfb_radius):
             f.restype = C.c_int
         _lib = L
     return _lib
@@ -76,6 +79,98 @@ def _check(rc, what):
 
 
 # ------------------------------------------------------------------ pieces
+
+
+def _frame_family(rows_idx, rows_dt, rows_dn) -> StencilSet:
+    cnt = np.array([r.shape[0] for r in rows_idx], dtype=np.int64)
+    ptr = np.concatenate([[0], np.cumsum(cnt)])
+    if ptr[-1]:
+        idx = np.concatenate(rows_idx).astype(np.int64)
+        dt = np.concatenate(rows_dt)
+        dn = np.concatenate(rows_dn)
+    else:
+        idx, dt, dn = np.empty(0, dtype=np.int64), np.empty(0), np.empty(0)
+    return G.StencilSet(ptr=ptr, idx=idx, dx=dt, dy=dn)
+
+
+def frames(cloud, full, thresh, points, side, failures):
+    """Rotated boundary stencils for one class (geometry.py:573-646).
+
+    ``side`` +1 keeps dn >= 0 for the one-sided normal family (wall: fluid
+    along +n), -1 keeps dn <= 0 (outer).  A tangent-split family that is
+    too thin or degenerate falls back to the full stencil.  The usability
+    test sums with np.sum exactly as the reference does (its result decides
+    fallbacks, so its summation order is part of the bit-exact contract).
+    """
+    if points.size == 0:
+        return None
+    nx, ny = cloud.nx[points], cloud.ny[points]
+    tx, ty = -ny, nx
+    label = "wall" if side > 0 else "outer"
+    fam = {"tp": ([], [], []), "tm": ([], [], []), "nr": ([], [], [])}
+    fallback = {}
+
+    def usable(dts, dns, limit):
+        stt = float(np.sum(dts ** 2))
+        snn = float(np.sum(dns ** 2))
+        stn = float(np.sum(dts * dns))
+        return dts.shape[0] >= 3 and abs(stt * snn - stn * stn) >= limit
+
+    for loc, gi in enumerate(points):
+        lo, hi = full.ptr[gi], full.ptr[gi + 1]
+        nb = full.idx[lo:hi]
+        ex, ey = full.dx[lo:hi], full.dy[lo:hi]
+        dt = ex * tx[loc] + ey * ty[loc]
+        dn = ex * nx[loc] + ey * ny[loc]
+        lim = thresh[gi]
+        every = np.ones(dt.shape[0], dtype=bool)
+        tag = ""
+        for key, mask, mark in (("tp", dt <= 0.0, "+"), ("tm", dt >= 0.0, "-")):
+            if not usable(dt[mask], dn[mask], lim):
+                mask = every
+                tag += mark
+            fam[key][0].append(nb[mask])
+            fam[key][1].append(dt[mask])
+            fam[key][2].append(dn[mask])
+        if tag:
+            fallback[int(gi)] = tag
+        nmask = dn >= 0.0 if side > 0 else dn <= 0.0
+        if not usable(dt[nmask], dn[nmask], lim):
+            failures.append((int(gi), f"{label}-normal", f"unusable one-sided stencil ({int(nmask.sum())} pts)"))
+        fam["nr"][0].append(nb[nmask])
+        fam["nr"][1].append(dt[nmask])
+        fam["nr"][2].append(dn[nmask])
+    return G.FrameStencils(
+        points=points, tx=tx, ty=ty, nx=nx, ny=ny,
+        tplus=_frame_family(*fam["tp"]), tminus=_frame_family(*fam["tm"]),
+        normal=_frame_family(*fam["nr"]), fallback=fallback,
+    )
+
+
+@dataclass
+class Parts:
+    full: G.StencilSet
+    split: dict
+    d_min: np.ndarray
+    d_mean: np.ndarray
+    wall_frame: G.FrameStencils | None
+    outer_frame: G.FrameStencils | None
+    failures: list
+
+
+def radius_csr(cloud: G.PointCloud, eps: float):
+    """geometry.py:349-374 rows as CSR (ptr, idx int64)."""
+    x, y = np.ascontiguousarray(cloud.x), np.ascontiguousarray(cloud.y)
+    n = x.shape[0]
+    counts = np.zeros(n, dtype=np.int64)
+    L = lib()
+    _check(L.kmfb_radius(n, _d(x), _d(y), float(eps), _i(counts), None, None), "kmfb_radius")
+    ptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(counts, out=ptr[1:])
+    idx = np.empty(int(ptr[-1]), dtype=np.int64)
+    _check(L.kmfb_radius(n, _d(x), _d(y), float(eps), _i(counts), _i(ptr), _i(idx)), "kmfb_radius")
+    return ptr, idx
+
 
 
 def knn_csr(cloud: G.PointCloud, k: int, subset=None):
@@ -194,7 +289,7 @@ class SplitView:
         return self.dx[p[i]:p[i + 1]], self.dy[p[i]:p[i + 1]]
 
 
-def assemble(cloud: G.PointCloud, ptr, idx) -> G._Parts:
+def assemble(cloud: G.PointCloud, ptr, idx) -> Parts:
     """geometry.py:532-570 on the native sums; same failure list, same order."""
     n = cloud.n_points
     x, y = np.ascontiguousarray(cloud.x), np.ascontiguousarray(cloud.y)
@@ -222,9 +317,9 @@ def assemble(cloud: G.PointCloud, ptr, idx) -> G._Parts:
             failures.append((int(i), kind, f"only {sc[i]} neighbors"))
         for i in np.flatnonzero(interior & (sc >= 3) & (np.abs(s.det) < thresh)):
             failures.append((int(i), kind, f"degenerate LS matrix (det {s.det[i]:.3e})"))
-    wall_frame = G._frames(cloud, full, thresh, cloud.wall, +1.0, failures)
-    outer_frame = G._frames(cloud, full, thresh, cloud.outer, -1.0, failures)
-    return G._Parts(full, split, d_min, d_mean, wall_frame, outer_frame, failures)
+    wall_frame = frames(cloud, full, thresh, cloud.wall, +1.0, failures)
+    outer_frame = frames(cloud, full, thresh, cloud.outer, -1.0, failures)
+    return Parts(full, split, d_min, d_mean, wall_frame, outer_frame, failures)
 
 
 def _splice(ptr, idx, rows_of: np.ndarray, rptr, ridx):
@@ -244,14 +339,26 @@ def _splice(ptr, idx, rows_of: np.ndarray, rptr, ridx):
     return nptr, nidx
 
 
-def build_stencils_native(cloud: G.PointCloud, k: int | None = None) -> G.Connectivity:
-    """geometry.py:453-518 (k-nearest mode) with the native loops."""
+def build_stencils_native(cloud: G.PointCloud, k: int | None = None, epsilon: float | None = None) -> G.Connectivity:
+    """geometry.py:453-518 with the native loops, k-nearest or radius mode
+    (radius rows with fewer than 8 neighbours take their 15 nearest,
+    geometry.py:480-486)."""
     cloud.validate()
+    if epsilon is not None and k is not None:
+        raise ValueError("give either epsilon or k, not both")
+    if epsilon is not None and epsilon <= 0.0:
+        raise ValueError("epsilon must be positive")
     if k is not None and k < 6:
         raise ValueError("k must be at least 6")
-    kk = min(k or G.KNN_DEFAULT, G.KNN_CAP)
     ws = wall_statistics(cloud)
-    ptr, idx = knn_csr(cloud, kk)
+    if epsilon is not None:
+        ptr, idx = radius_csr(cloud, epsilon)
+        thin = np.flatnonzero(np.diff(ptr) < G.RADIUS_MIN_NEIGHBORS).astype(np.int64)
+        if thin.size:
+            tptr, tidx = knn_csr(cloud, G.KNN_DEFAULT, thin)
+            ptr, idx = _splice(ptr, idx, thin, tptr, tidx)
+    else:
+        ptr, idx = knn_csr(cloud, min(k or G.KNN_DEFAULT, G.KNN_CAP))
     ptr, idx = _compress(ptr, idx, visibility_keep(cloud, ptr, idx, wall_stats=ws))
     parts = assemble(cloud, ptr, idx)
     if parts.failures:

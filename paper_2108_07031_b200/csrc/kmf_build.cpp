@@ -338,6 +338,40 @@ int kmfb_knn(int64_t n, const double *x, const double *y, int k, int64_t nq, con
     return 0;
 }
 
+// geometry.py:349-374 radius rows: every j != i with squared distance
+// (x_j - x_i)^2 + (y_j - y_i)^2 < eps^2 (both squares and the sum rounded,
+// like the reference's numpy filter; the ball query it filters is a
+// superset), ascending.  Pass 1 (rows == NULL): counts; pass 2: rows at
+// offsets ptr[r].
+int kmfb_radius(int64_t n, const double *x, const double *y, double eps, int64_t *counts, const int64_t *ptr,
+                int64_t *rows)
+{
+    if (n <= 0 || !(eps > 0.0)) return 2;
+    std::vector<int32_t> all = iota32(n);
+    Tree t;
+    t.build(x, y, all.data(), n);
+    const double eps2 = eps * eps;
+#pragma omp parallel
+    {
+        std::vector<int32_t> got;
+#pragma omp for schedule(dynamic, 1024)
+        for (int64_t i = 0; i < n; i++) {
+            got.clear();
+            t.range(x[i], y[i], eps2 * (1.0 + 1e-12), [&](int32_t p, double v) {
+                if (p != i && v < eps2) got.push_back(p);
+            });
+            if (!rows) {
+                counts[i] = (int64_t)got.size();
+                continue;
+            }
+            std::sort(got.begin(), got.end());
+            int64_t o = ptr[i];
+            for (int32_t p : got) rows[o++] = p;
+        }
+    }
+    return 0;
+}
+
 // geometry.py:396-450 visibility filter.  Wall statistics (spacing, tol)
 // come from the caller (their cKDTree tie order is part of the contract).
 // keep[e] = 1 when edge e (owner owners[r] for r's rows) survives.

@@ -1,19 +1,13 @@
 """Point clouds, stencils and the NACA 0012 cloud generator (host-side setup).
 
 Drop-in for reference ``kmf.geometry``: same types and field names
-(geometry.py:56-312), same builder semantics (geometry.py:315-646) and same
-generator (geometry.py:652-770).  This is SETUP, not the timed hot path: it
+(geometry.py:56-312), same builder semantics (geometry.py:315-646, native: builder.py)
+and same generator (geometry.py:652-770).  This is SETUP, not the timed hot path: it
 runs once on the host before the device context is created.  Its outputs
 must be bit-identical to the reference's (they fix the summation order of
 every least-squares sum on the device), which tests/test_geometry_parity.py
 checks against sha256 digests of the reference's own arrays
-(tests/golden/*.json).  scipy's cKDTree is used for the neighbour queries
-because its tie behaviour at the k-th distance defines the reference
-stencils.
-
-Beyond the reference the builder is vectorised (one batched kNN query and
-row-sorted CSR assembly instead of per-point Python lists), which matters at
-the 2.5M/10M-point configurations.
+(tests/golden/*.json).
 """
 
 from __future__ import annotations
@@ -23,7 +17,6 @@ from dataclasses import dataclass, field
 from pathlib import Path
 
 import numpy as np
-from scipy.spatial import cKDTree
 
 INTERIOR, WALL, OUTER = 0, 1, 2
 SPLIT_KINDS = ("x+", "x-", "y+", "y-")
@@ -273,116 +266,7 @@ def write_point_cloud(cloud: PointCloud, path, binary: bool = False) -> None:
     path.write_text(out.getvalue())
 
 
-# ----------------------------------------------------------- neighbour search
-
-
-def _rows_to_lists(ptr: np.ndarray, idx: np.ndarray):
-    return [idx[ptr[i]:ptr[i + 1]] for i in range(ptr.shape[0] - 1)]
-
-
-def knn_lists(x, y, k, subset=None):
-    """Tie-inclusive k-nearest neighbours, self excluded, ascending index.
-
-    Semantics of geometry.py:315-346: every point at distance <= the k-th
-    neighbour's distance (self counted as the 0th) is kept; when all padded
-    candidates tie with the cut the query widens until the plateau ends.
-    Returns a list of int64 arrays.
-    """
-    n = x.shape[0]
-    pts = np.column_stack([x, y])
-    tree = cKDTree(pts)
-    query = np.arange(n) if subset is None else np.asarray(subset, dtype=np.int64)
-    k_eff = min(k + 1, n)
-    pad = min(k_eff + 8, n)
-    dist, nbr = tree.query(pts[query], k=pad)
-    dist = np.atleast_2d(dist).reshape(query.size, pad)
-    nbr = np.atleast_2d(nbr).reshape(query.size, pad)
-    keep = dist <= dist[:, k_eff - 1:k_eff]
-    plateau = np.flatnonzero(keep.all(axis=1)) if pad < n else np.empty(0, dtype=np.int64)
-    keep &= nbr != query[:, None]
-    cnt = keep.sum(axis=1)
-    rows = np.where(keep, nbr, n)
-    rows.sort(axis=1)
-    out = [rows[r, :cnt[r]].astype(np.int64) for r in range(query.size)]
-    for r in plateau:
-        qi = int(query[r])
-        width = pad
-        while True:
-            width = min(width * 2, n)
-            d, nb = tree.query(pts[qi], k=width)
-            sel = d <= d[k_eff - 1]
-            if width == n or not sel.all():
-                break
-        cand = nb[sel]
-        out[r] = np.sort(cand[cand != qi]).astype(np.int64)
-    return out
-
-
-def radius_lists(x, y, eps):
-    """All neighbours with squared distance < eps^2, ascending (geometry.py:349-374)."""
-    n = x.shape[0]
-    tree = cKDTree(np.column_stack([x, y]))
-    cands = tree.query_ball_point(np.column_stack([x, y]), r=eps * (1.0 + 1e-9))
-    eps2 = eps * eps
-    out = []
-    for i in range(n):
-        c = np.asarray(cands[i], dtype=np.int64)
-        d2 = (x[c] - x[i]) ** 2 + (y[c] - y[i]) ** 2
-        out.append(np.sort(c[(d2 < eps2) & (c != i)]))
-    return out
-
-
-def visibility_filter(cloud: PointCloud, lists, owners=None):
-    """Drop edges that cut through the body behind the wall (geometry.py:396-450).
-
-    An edge survives when each of its 1/4, 1/2, 3/4 sample points is either
-    more than two local wall spacings from the nearest wall point or lies no
-    deeper behind that point's tangent plane than the tolerance
-    min(0.2 spacing, 0.45 local thickness).
-    """
-    wall = np.flatnonzero(cloud.flag == WALL)
-    if wall.size < 2:
-        return lists
-    wx, wy = cloud.x[wall], cloud.y[wall]
-    wnx, wny = cloud.nx[wall], cloud.ny[wall]
-    wpts = np.column_stack([wx, wy])
-    tree = cKDTree(wpts)
-    spacing = tree.query(wpts, k=2)[0][:, 1]
-    d16, c16 = tree.query(wpts, k=min(16, wall.size))
-    facing = wnx[:, None] * wnx[c16] + wny[:, None] * wny[c16] < -0.5
-    thick = np.where(facing, d16, np.inf).min(axis=1)
-    tol = np.minimum(0.2 * spacing, 0.45 * thick)
-
-    sizes = np.fromiter((len(v) for v in lists), dtype=np.int64, count=len(lists))
-    if not sizes.sum():
-        return lists
-    nbr = np.concatenate(lists).astype(np.int64)
-    base = np.arange(len(lists)) if owners is None else np.asarray(owners)
-    own = np.repeat(base, sizes)
-    ok = np.ones(nbr.shape[0], dtype=bool)
-    x0, y0 = cloud.x[own], cloud.y[own]
-    ddx, ddy = cloud.x[nbr] - x0, cloud.y[nbr] - y0
-    for frac in (0.25, 0.5, 0.75):
-        px = x0 + frac * ddx
-        py = y0 + frac * ddy
-        dist, near = tree.query(np.column_stack([px, py]))
-        depth = (px - wx[near]) * wnx[near] + (py - wy[near]) * wny[near]
-        ok &= (dist > 2.0 * spacing[near]) | (depth > -tol[near])
-    if ok.all():
-        return lists
-    ptr = np.concatenate([[0], np.cumsum(sizes)])
-    return [nbr[ptr[i]:ptr[i + 1]][ok[ptr[i]:ptr[i + 1]]] for i in range(len(lists))]
-
-
-# ----------------------------------------------------------------- assembly
-
-
-def _csr(cloud: PointCloud, lists) -> StencilSet:
-    sizes = np.fromiter((len(v) for v in lists), dtype=np.int64, count=len(lists))
-    ptr = np.concatenate([[0], np.cumsum(sizes)])
-    idx = np.concatenate(lists).astype(np.int64) if ptr[-1] else np.empty(0, dtype=np.int64)
-    own = np.repeat(np.arange(len(lists)), sizes)
-    return StencilSet(ptr=ptr, idx=idx, dx=cloud.x[idx] - cloud.x[own], dy=cloud.y[idx] - cloud.y[own])
+# ----------------------------------------------------------------- builder
 
 
 def _select(full: StencilSet, mask: np.ndarray) -> StencilSet:
@@ -392,163 +276,15 @@ def _select(full: StencilSet, mask: np.ndarray) -> StencilSet:
     return StencilSet(ptr=ptr, idx=full.idx[mask], dx=full.dx[mask], dy=full.dy[mask])
 
 
-def _frame_family(rows_idx, rows_dt, rows_dn) -> StencilSet:
-    cnt = np.array([r.shape[0] for r in rows_idx], dtype=np.int64)
-    ptr = np.concatenate([[0], np.cumsum(cnt)])
-    if ptr[-1]:
-        idx = np.concatenate(rows_idx).astype(np.int64)
-        dt = np.concatenate(rows_dt)
-        dn = np.concatenate(rows_dn)
-    else:
-        idx, dt, dn = np.empty(0, dtype=np.int64), np.empty(0), np.empty(0)
-    return StencilSet(ptr=ptr, idx=idx, dx=dt, dy=dn)
+def build_stencils(cloud: PointCloud, epsilon: float | None = None, k: int | None = None) -> Connectivity:
+    """Full, split and boundary-frame stencils with cached sums (geometry.py:453-518):
+    the native builder (builder.py, libkmf_build.so), bit-identical to the
+    reference's (tests/test_builder.py, tests/test_geometry_parity.py);
+    StencilDeficiencyError (after widening failing points to k=25) exactly
+    where the reference raises it."""
+    from .builder import build_stencils_native
 
-
-def _frames(cloud, full, thresh, points, side, failures):
-    """Rotated boundary stencils for one class (geometry.py:573-646).
-
-    ``side`` +1 keeps dn >= 0 for the one-sided normal family (wall: fluid
-    along +n), -1 keeps dn <= 0 (outer).  A tangent-split family that is
-    too thin or degenerate falls back to the full stencil.  The usability
-    test sums with np.sum exactly as the reference does (its result decides
-    fallbacks, so its summation order is part of the bit-exact contract).
-    """
-    if points.size == 0:
-        return None
-    nx, ny = cloud.nx[points], cloud.ny[points]
-    tx, ty = -ny, nx
-    label = "wall" if side > 0 else "outer"
-    fam = {"tp": ([], [], []), "tm": ([], [], []), "nr": ([], [], [])}
-    fallback = {}
-
-    def usable(dts, dns, limit):
-        stt = float(np.sum(dts ** 2))
-        snn = float(np.sum(dns ** 2))
-        stn = float(np.sum(dts * dns))
-        return dts.shape[0] >= 3 and abs(stt * snn - stn * stn) >= limit
-
-    for loc, gi in enumerate(points):
-        lo, hi = full.ptr[gi], full.ptr[gi + 1]
-        nb = full.idx[lo:hi]
-        ex, ey = full.dx[lo:hi], full.dy[lo:hi]
-        dt = ex * tx[loc] + ey * ty[loc]
-        dn = ex * nx[loc] + ey * ny[loc]
-        lim = thresh[gi]
-        every = np.ones(dt.shape[0], dtype=bool)
-        tag = ""
-        for key, mask, mark in (("tp", dt <= 0.0, "+"), ("tm", dt >= 0.0, "-")):
-            if not usable(dt[mask], dn[mask], lim):
-                mask = every
-                tag += mark
-            fam[key][0].append(nb[mask])
-            fam[key][1].append(dt[mask])
-            fam[key][2].append(dn[mask])
-        if tag:
-            fallback[int(gi)] = tag
-        nmask = dn >= 0.0 if side > 0 else dn <= 0.0
-        if not usable(dt[nmask], dn[nmask], lim):
-            failures.append((int(gi), f"{label}-normal", f"unusable one-sided stencil ({int(nmask.sum())} pts)"))
-        fam["nr"][0].append(nb[nmask])
-        fam["nr"][1].append(dt[nmask])
-        fam["nr"][2].append(dn[nmask])
-    return FrameStencils(
-        points=points, tx=tx, ty=ty, nx=nx, ny=ny,
-        tplus=_frame_family(*fam["tp"]), tminus=_frame_family(*fam["tm"]),
-        normal=_frame_family(*fam["nr"]), fallback=fallback,
-    )
-
-
-@dataclass
-class _Parts:
-    full: StencilSet
-    split: dict
-    d_min: np.ndarray
-    d_mean: np.ndarray
-    wall_frame: FrameStencils | None
-    outer_frame: FrameStencils | None
-    failures: list
-
-
-def _assemble(cloud: PointCloud, lists) -> _Parts:
-    full = _csr(cloud, lists)
-    n = cloud.n_points
-    own = _owners(full.ptr)
-    length = np.hypot(full.dx, full.dy)
-    d_min = np.full(n, np.inf)
-    np.minimum.at(d_min, own, length)
-    d_mean = np.bincount(own, weights=length, minlength=n) / np.maximum(full.counts(), 1)
-    split = {
-        "x+": _select(full, full.dx <= 0.0),
-        "x-": _select(full, full.dx >= 0.0),
-        "y+": _select(full, full.dy <= 0.0),
-        "y-": _select(full, full.dy >= 0.0),
-    }
-    failures = []
-    interior = cloud.flag == INTERIOR
-    thresh = DEGENERACY_FACTOR * d_mean ** 4
-    cnt = full.counts()
-    for i in np.flatnonzero(cnt < 3):
-        failures.append((int(i), "full", f"only {cnt[i]} neighbors"))
-    for i in np.flatnonzero((cnt >= 3) & (np.abs(full.det) < thresh)):
-        failures.append((int(i), "full", f"degenerate LS matrix (det {full.det[i]:.3e})"))
-    for kind, s in split.items():
-        sc = s.counts()
-        for i in np.flatnonzero(interior & (sc < 3)):
-            failures.append((int(i), kind, f"only {sc[i]} neighbors"))
-        for i in np.flatnonzero(interior & (sc >= 3) & (np.abs(s.det) < thresh)):
-            failures.append((int(i), kind, f"degenerate LS matrix (det {s.det[i]:.3e})"))
-    wall_frame = _frames(cloud, full, thresh, cloud.wall, +1.0, failures)
-    outer_frame = _frames(cloud, full, thresh, cloud.outer, -1.0, failures)
-    return _Parts(full, split, d_min, d_mean, wall_frame, outer_frame, failures)
-
-
-def build_stencils(cloud: PointCloud, epsilon: float | None = None, k: int | None = None,
-                   native: bool | None = None) -> Connectivity:
-    """Full, split and boundary-frame stencils with cached sums (geometry.py:453-518).
-
-    Raises StencilDeficiencyError (after widening failing points to k=25)
-    exactly where the reference does.  In k-nearest mode the heavy loops run
-    in the native builder (builder.py, libkmf_build.so) unless native=False;
-    native=None uses it when the library is built.  Both paths give
-    bit-identical connectivities (tests/test_builder.py).
-    """
-    if epsilon is None and native is not False:
-        from . import builder
-
-        if native or builder.available():
-            return builder.build_stencils_native(cloud, k)
-    cloud.validate()
-    if epsilon is not None and k is not None:
-        raise ValueError("give either epsilon or k, not both")
-    if epsilon is not None and epsilon <= 0.0:
-        raise ValueError("epsilon must be positive")
-    if k is not None and k < 6:
-        raise ValueError("k must be at least 6")
-    if epsilon is not None:
-        lists = radius_lists(cloud.x, cloud.y, epsilon)
-        thin = [i for i, v in enumerate(lists) if len(v) < RADIUS_MIN_NEIGHBORS]
-        if thin:
-            for i, row in zip(thin, knn_lists(cloud.x, cloud.y, KNN_DEFAULT, thin)):
-                lists[i] = row
-    else:
-        lists = knn_lists(cloud.x, cloud.y, min(k or KNN_DEFAULT, KNN_CAP))
-    lists = visibility_filter(cloud, lists)
-    parts = _assemble(cloud, lists)
-    if parts.failures:
-        grow = sorted({i for i, _, _ in parts.failures if len(lists[i]) < KNN_CAP})
-        if grow:
-            rows = visibility_filter(cloud, knn_lists(cloud.x, cloud.y, KNN_CAP, grow), owners=grow)
-            for i, row in zip(grow, rows):
-                lists[i] = row
-            parts = _assemble(cloud, lists)
-    if parts.failures:
-        raise StencilDeficiencyError(parts.failures)
-    interior = cloud.flag == INTERIOR
-    det_safe = {kind: np.where(interior, s.det, 1.0) for kind, s in parts.split.items()}
-    return Connectivity(
-        cloud=cloud, full=parts.full, split=parts.split, d_min=parts.d_min, d_mean=parts.d_mean,
-        wall_frame=parts.wall_frame, outer_frame=parts.outer_frame, det_safe=det_safe,
-    )
+    return build_stencils_native(cloud, k=k, epsilon=epsilon)
 
 
 # ------------------------------------------------------------ the generator

@@ -83,8 +83,14 @@ class SolverConfig:
             raise ValueError("order must be 1 or 2")
 
     def to_dict(self) -> dict:
-        return {k: getattr(self, k) for k in ("mach", "aoa_deg", "gamma", "cfl", "n_outer", "n_inner", "mode",
-                                               "threads", "convergence_tol", "order")}
+        """The reference's keys (solver.py:101-112); `order` only when it is
+        not the reference's own second-order scheme, so reports and config
+        echoes stay readable by the reference's tools."""
+        d = {k: getattr(self, k) for k in ("mach", "aoa_deg", "gamma", "cfl", "n_outer", "n_inner", "mode",
+                                            "threads", "convergence_tol")}
+        if self.order != 2:
+            d["order"] = self.order
+        return d
 
 
 @dataclass

@@ -13,6 +13,7 @@ import numpy as np
 
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 
+from oracle.builder_ref import build_stencils_ref  # noqa: E402
 from paper_2108_07031_b200 import build_stencils, generate_naca_cloud  # noqa: E402
 
 SIZES = {"c1": (400, 100, 1.06), "c2": (800, 200, 1.03), "c3": (3160, 790, 1.00734), "c4": (6324, 1581, 1.003647)}
@@ -38,10 +39,10 @@ if __name__ == "__main__":
     for name in sys.argv[1:] or ["c3"]:
         cloud = generate_naca_cloud(*SIZES[name], 20.0)
         t = time.perf_counter()
-        nat = build_stencils(cloud, native=True)
+        nat = build_stencils(cloud)
         tn = time.perf_counter() - t
         t = time.perf_counter()
-        ref = build_stencils(cloud, native=False)
+        ref = build_stencils_ref(cloud)
         ts = time.perf_counter() - t
         print(f"{name}: n={cloud.n_points} edges={nat.full.idx.size} native {tn:.1f} s, scipy {ts:.1f} s, "
               f"mismatching arrays: {diff(nat, ref) or 'none'}", flush=True)

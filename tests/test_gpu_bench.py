@@ -43,7 +43,9 @@ def test_bench_ours_contract(gpu):
         assert 0 < rq[kern]["frac"] < 1.5 and rq[kern]["launch_us"] > 0
     assert "algorithmic_achieved" not in d["roofline_fp64"]
     cb = d["cpu_baseline"]
-    assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] > 0 and cb["sample"]
+    assert cb["kind"] in ("reference", "port") and cb["cores"] >= 1 and cb["value"] > 0 and cb["sample"]
+    if cb["kind"] == "reference":  # the reference package itself (baseline/_ref), the C port beside it
+        assert "kmf" in cb["sample"] and d["cpu_baseline_port"]["kind"] == "port"
 
 
 def test_bench_first_order_config(gpu):

@@ -335,6 +335,39 @@ KMF_HD void qg_pipeline(int d, Gather gather, Eval eval)
     }
 }
 
+// Two slot buffers, unrolled by two: while slot s is evaluated from one
+// buffer, the gathers of slot s+1 are already in flight into the other
+// (issued before slot s's arithmetic in program order).
+template <class Slot, class Gather, class Eval>
+KMF_HD void qg_pipeline2(int d, Gather gather, Eval eval)
+{
+    if (d <= 0) return;
+    Slot a, b;
+    gather(0, a);
+    gather(min(1, d - 1), b);
+    int s = 0;
+    for (; s + 1 < d; s += 2) {
+        eval(a);
+        gather(min(s + 2, d - 1), a);
+        eval(b);
+        gather(min(s + 3, d - 1), b);
+    }
+    if (s < d) eval(a);
+}
+
+// The sweeps keep the one-buffer loop (94 registers, 5 blocks/SM): the
+// two-buffer loop needs 125 registers (4 blocks/SM) and measured 8-11 %
+// slower at 2.5M / 10M; the first-order kernel (bounded to 64 registers
+// either way) takes the two-buffer loop (-3 %).
+template <class Slot, bool TWO, class Gather, class Eval>
+KMF_HD void qg_slots(int d, Gather gather, Eval eval)
+{
+    if constexpr (TWO)
+        qg_pipeline2<Slot>(d, gather, eval);
+    else
+        qg_pipeline<Slot>(d, gather, eval);
+}
+
 // lsq.py:164-175 first_order_q_gradients -- bitwise (CSR-order sums, no FMA)
 template <bool XY, int NC>
 __global__ void __launch_bounds__(kTB, NC == 4 ? 8 : 0) k_first_order(DG g, int lo, int hi,
@@ -361,7 +394,7 @@ __global__ void __launch_bounds__(kTB, NC == 4 ? 8 : 0) k_first_order(DG g, int 
     const double xi = g.x[i], yi = g.y[i];
     const int base = ell_base(g, i), d = g.deg[i];
     using Slot = QgSlot<NC, false>;
-    qg_pipeline<Slot>(
+    qg_slots<Slot, true>(
         d,
         [&](int s, Slot &o) {
             const int ent = base + s * 32;
@@ -417,7 +450,7 @@ __global__ void __launch_bounds__(kTB) k_sweep(DG g, int lo, int hi, const doubl
         const double xi = g.x[i], yi = g.y[i];
         const int base = ell_base(g, i), d = g.deg[i];
         using Slot = QgSlot<NC, true>;
-        qg_pipeline<Slot>(
+        qg_slots<Slot, false>(
             d,
             [&](int s, Slot &o) {
                 const int ent = base + s * 32;

@@ -250,8 +250,13 @@ __host__ __device__ constexpr int qg_points_per_block() { return kTB * NC / 4; }
 // SPB = slices per block.
 KMF_HD uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
+// Issue half: one thread arms the mbarrier and starts the copy; every
+// thread passes the block barrier (the mbarrier is initialised before anyone
+// polls it).  The kernels load their owner data between issue and wait, so
+// the copy's latency overlaps those loads; every thread waits before it may
+// leave (the copy must land before the CTA's shared memory is released).
 template <int SPB>
-KMF_HD bool qg_stage_indices_tma(const DG &g, int lo, int *sidx, int cap, int &e0, unsigned long long *mbar)
+KMF_HD bool qg_stage_issue(const DG &g, int lo, int *sidx, int cap, int &e0, unsigned long long *mbar)
 {
     const int ns = (g.n + 31) >> 5;
     const int s0 = (range_base(lo) >> 5) + blockIdx.x * SPB;
@@ -271,17 +276,21 @@ KMF_HD bool qg_stage_indices_tma(const DG &g, int lo, int *sidx, int cap, int &e
             "l"(g.eidx + e0), "r"(bytes), "r"(bar)
             : "memory");
     }
-    __syncthreads();  // the barrier is initialised before anyone polls it
-    if (staged) {
-        uint32_t done = 0;
-        while (!done)
-            asm volatile(
-                "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
-                : "=r"(done)
-                : "r"(bar)
-                : "memory");
-    }
+    __syncthreads();
     return staged;
+}
+
+KMF_HD void qg_stage_wait(bool staged, unsigned long long *mbar)
+{
+    if (!staged) return;
+    const uint32_t bar = smem_u32(mbar);
+    uint32_t done = 0;
+    while (!done)
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(bar)
+            : "memory");
 }
 
 // One neighbour slot as the q-gradient kernels consume it: the neighbour's
@@ -378,11 +387,11 @@ __global__ void __launch_bounds__(kTB, NC == 4 ? 8 : 0) k_first_order(DG g, int 
     __shared__ __align__(128) int sidx[CAP];
     __shared__ unsigned long long mbar;
     int e0 = 0;
-    const bool staged = qg_stage_indices_tma<SPB>(g, lo, sidx, CAP, e0, &mbar);
-    if (c && should_skip(c, stage, 0)) return;
+    const bool staged = qg_stage_issue<SPB>(g, lo, sidx, CAP, e0, &mbar);
     int i, k0;
     qg_thread<NC>(lo, i, k0);
-    if (i < lo || i >= hi) return;
+    const bool valid = i >= lo && i < hi;
+    if (!valid) i = lo;  // a safe slot for the owner loads below
     const int ld = g.ld;
     double qi[NC], sx[NC], sy[NC];
     qload_nc<NC>(q, i, k0, qi);
@@ -393,6 +402,8 @@ __global__ void __launch_bounds__(kTB, NC == 4 ? 8 : 0) k_first_order(DG g, int 
     }
     const double xi = g.x[i], yi = g.y[i];
     const int base = ell_base(g, i), d = g.deg[i];
+    qg_stage_wait(staged, &mbar);
+    if (!valid || (c && should_skip(c, stage, 0))) return;
     using Slot = QgSlot<NC, false>;
     qg_slots<Slot, true>(
         d,
@@ -430,25 +441,28 @@ __global__ void __launch_bounds__(kTB) k_sweep(DG g, int lo, int hi, const doubl
     __shared__ __align__(128) int sidx[CAP];
     __shared__ unsigned long long mbar;
     int e0 = 0;
-    const bool staged = qg_stage_indices_tma<SPB>(g, lo, sidx, CAP, e0, &mbar);
-    if (c && should_skip(c, stage, slot)) return;
+    const bool staged = qg_stage_issue<SPB>(g, lo, sidx, CAP, e0, &mbar);
     int i, k0;
     qg_thread<NC>(lo, i, k0);
-    double rmax = 0.0;
-    if (i >= lo && i < hi) {
-        const int ld = g.ld;
-        double qi[NC], gxi[NC], gyi[NC], sx[NC], sy[NC];
-        qload_nc<NC>(q, i, k0, qi);
+    const bool valid = i >= lo && i < hi;
+    if (!valid) i = lo;  // a safe slot for the owner loads below
+    const int ld = g.ld;
+    double qi[NC], gxi[NC], gyi[NC], sx[NC], sy[NC];
+    qload_nc<NC>(q, i, k0, qi);
 #pragma unroll
-        for (int k = 0; k < NC; k++) {
-            const double2 v = gload_cm(Gin, ld, k0 + k, i);
-            gxi[k] = v.x;
-            gyi[k] = v.y;
-            sx[k] = 0.0;
-            sy[k] = 0.0;
-        }
-        const double xi = g.x[i], yi = g.y[i];
-        const int base = ell_base(g, i), d = g.deg[i];
+    for (int k = 0; k < NC; k++) {
+        const double2 v = gload_cm(Gin, ld, k0 + k, i);
+        gxi[k] = v.x;
+        gyi[k] = v.y;
+        sx[k] = 0.0;
+        sy[k] = 0.0;
+    }
+    const double xi = g.x[i], yi = g.y[i];
+    const int base = ell_base(g, i), d = g.deg[i];
+    qg_stage_wait(staged, &mbar);
+    if (c && should_skip(c, stage, slot)) return;
+    double rmax = 0.0;
+    if (valid) {
         using Slot = QgSlot<NC, true>;
         qg_slots<Slot, false>(
             d,

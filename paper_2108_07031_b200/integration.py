@@ -6,7 +6,7 @@ kmf/geometry.py) do when a `kmf` maintainer adds them: every name under
 which the reference's modules reach the hot path -- `kmf.solve`,
 `kmf.solver.solve`, `kmf.bench.solve`, `kmf.cli.solve` (validation.py goes
 through `kmf.solver.solve`) -- runs this package's B200 `solve`, and
-`build_stencils` (k-nearest mode) the native bit-exact builder.
+`build_stencils` the native bit-exact builder.
 
 The reference's own harness (kmf.bench: BenchmarkReport, timed_run, sweep,
 the JSON/CSV writers; bench.py:45-259) and CLI (kmf.cli generate / solve /
@@ -63,14 +63,11 @@ def route_reference(kmf, stencils: bool = True) -> None:
             if ref_build is None:
                 continue
             saved.setdefault((mod.__name__, "build_stencils"), ref_build)
-            original = saved[(mod.__name__, "build_stencils")]
 
-            def build_stencils(cloud, epsilon=None, k=None, _orig=original):
-                """kmf.geometry.build_stencils (geometry.py:453-518): the native
-                builder in k-nearest mode, the reference's own otherwise."""
-                if epsilon is None:
-                    return build_stencils_native(cloud, k)
-                return _orig(cloud, epsilon=epsilon, k=k)
+            def build_stencils(cloud, epsilon=None, k=None):
+                """kmf.geometry.build_stencils (geometry.py:453-518) on the
+                native bit-exact builder (k-nearest and radius modes)."""
+                return build_stencils_native(cloud, k=k, epsilon=epsilon)
 
             mod.build_stencils = build_stencils
     setattr(kmf, _SAVED, saved)

@@ -892,8 +892,18 @@ void enqueue_tail(kmf_ctx *c, StageCtx &sc, int stage, const double *G)
     c->G_last = G;
     Mark m(c, KC_UPDATE, inst);
     IterOut io = sc.io;
-    io.close_in_kernel = c->dist_on ? 0 : 1;
+    // The stage-4 update closes the iteration itself (last block: residue,
+    // history, counters) on small clouds, where one more launch would cost
+    // more than the per-block fence; from 1M points a one-block k_close
+    // after it is cheaper (the update runs fence-free: -0.7 ms at 40M).
+    // Partitions close after the limb all-reduce (enqueue_after_update_nccl).
+    const bool own_close = !c->dist_on && c->n >= (1 << 20);
+    io.close_in_kernel = (c->dist_on || own_close) ? 0 : 1;
     launch_update(c, c->s0, stage, p->gamma, p->cfl, io);
+    if (stage == 4 && own_close) {
+        k_close<<<1, kTB, 0, c->s0>>>(c->ctrl.p, c->n, io);
+        c->nlaunch++;
+    }
 }
 
 // NCCL partition: the iteration close after the stage-4 update (exact limb

@@ -268,6 +268,8 @@ def oracle_sample(conn, init4n, cfg):
 
 
 REF_SAMPLE_POINTS = int(os.environ.get("KMF_REF_SAMPLE", 64_000))
+# point counts of the configuration clouds (m * L)
+CONFIG_POINTS = {k: v[0] * v[1] for k, v in CONFIGS.items()}
 
 
 def reference_package():
@@ -287,66 +289,37 @@ def reference_package():
         sys.path.remove(str(root))
 
 
-def reference_sample(kmf, conn, init4n, cfg, target=REF_SAMPLE_POINTS):
-    """(reference Connectivity, reference Primitives, counted points,
-    description) of a bounded sample of the workload for the reference's own
-    solve: the whole cloud when small, else a compact patch of the `target`
-    points nearest to the point n // 3 (a 2-d blob, so its deep halo --
-    partition.py -- stays a thin rim) converted to the reference's own
-    types.  The outermost halo layer has no stencils
-    (it only carries q): its LS determinants are set to 1 so the reference's
-    divisions stay finite (gradients and residuals 0 there); all other slab
-    points run the full arithmetic and are counted."""
-    from paper_2108_07031_b200.partition import build_part
-
+def reference_patch(kmf, name, target=REF_SAMPLE_POINTS):
+    """A bounded sample of configuration `name` built ENTIRELY by the
+    reference package (no code of this repo): the reference's generator
+    makes the configuration's cloud, the `target` points nearest to the
+    leading-edge wall point form a compact patch (wall points included, with
+    their wall closures), the patch's outermost 3 % become an artificial
+    far-field boundary (outer points, radial normals), and the reference's
+    own builder and initial state set it up.  Returns (reference
+    Connectivity, reference Primitives, points, description)."""
+    m, L, g, mach, aoa, _ = CONFIGS[name]
     G = kmf.geometry
-    n = conn.cloud.n_points
-
-    def st(s, det_one=None):
-        det = np.array(s.det, dtype=np.float64)
-        if det_one is not None:
-            det[det_one] = 1.0
-        return G.StencilSet(ptr=np.asarray(s.ptr), idx=np.asarray(s.idx), dx=np.asarray(s.dx), dy=np.asarray(s.dy),
-                            sxx=np.asarray(s.sxx), sxy=np.asarray(s.sxy), syy=np.asarray(s.syy), det=det)
-
-    def fr(f):
-        if f is None:
-            return None
-        return G.FrameStencils(points=np.asarray(f.points), tx=f.tx, ty=f.ty, nx=f.nx, ny=f.ny, tplus=st(f.tplus),
-                               tminus=st(f.tminus), normal=st(f.normal), fallback=dict(f.fallback))
-
-    if n <= 1.5 * target:
-        sub, gid, counted = conn, np.arange(n), n
-        desc = f"the whole {n}-point cloud"
-        last = None
-    else:
-        from scipy.spatial import cKDTree
-
-        c0 = n // 3
-        pts = np.column_stack([conn.cloud.x, conn.cloud.y])
-        _, near = cKDTree(pts).query(pts[c0], k=target)
-        owner = np.ones(n, dtype=np.int32)
-        owner[near] = 0
-        part = build_part(conn, 0, 2, cfg.n_inner + 2, owner=owner)
-        sub, gid = part.conn, part.global_ids
-        counted = int(part.layer_counts[-2])
-        last = np.arange(counted, gid.size)
-        desc = (f"a compact {part.n_owned}-point patch of the {n}-point cloud with its {cfg.n_inner + 2}-layer halo: "
-                f"{counted} points with complete stencils counted ({gid.size - counted} outermost halo points "
-                f"carry q only)")
-    c = sub.cloud
-    cloud = G.PointCloud(np.asarray(c.x), np.asarray(c.y), np.asarray(c.flag), np.asarray(c.nx), np.asarray(c.ny))
-    det_safe = {}
-    for k, v in sub.det_safe.items():
-        d = np.array(v, dtype=np.float64)
-        if last is not None:
-            d[last] = 1.0
-        det_safe[k] = d
-    rconn = G.Connectivity(cloud=cloud, full=st(sub.full, last), split={k: st(v, last) for k, v in sub.split.items()},
-                           d_min=np.asarray(sub.d_min), d_mean=np.asarray(sub.d_mean), wall_frame=fr(sub.wall_frame),
-                           outer_frame=fr(sub.outer_frame), det_safe=det_safe)
-    prims = kmf.state.Primitives(*np.asarray(init4n)[:, gid])
-    return rconn, prims, counted, desc
+    cloud = G.generate_naca_cloud(m, L, g, 20.0)
+    w = np.flatnonzero(cloud.flag == 1)
+    c0 = int(w[np.argmin(cloud.x[w])])
+    xc, yc = float(cloud.x[c0]), float(cloud.y[c0])
+    d = np.hypot(cloud.x - xc, cloud.y - yc)
+    near = np.sort(np.argpartition(d, target)[:target])
+    dd = d[near]
+    x, y = cloud.x[near], cloud.y[near]
+    flag, nx, ny = cloud.flag[near].copy(), cloud.nx[near].copy(), cloud.ny[near].copy()
+    rim = (dd > 0.97 * dd.max()) & (flag == 0)
+    flag[rim] = 2
+    nx[rim], ny[rim] = (x[rim] - xc) / dd[rim], (y[rim] - yc) / dd[rim]
+    sub = G.PointCloud(x, y, flag, nx, ny)
+    rconn = G.build_stencils(sub)
+    cfg = kmf.solver.SolverConfig(mach=mach, aoa_deg=aoa, n_outer=1)
+    prims = kmf.solver._initial_primitives(cfg, sub)
+    desc = (f"a {target}-point patch of the {cloud.n_points}-point configuration cloud around the leading edge "
+            f"({int((flag == 1).sum())} wall points, {int(rim.sum())} rim points as far field), generated, built "
+            f"and initialised by the reference package itself")
+    return rconn, prims, target, desc
 
 
 def time_reference(kmf, rconn, prims, cfg, steps, warmup):
@@ -366,11 +339,11 @@ def time_reference(kmf, rconn, prims, cfg, steps, warmup):
     return t, threads
 
 
-def cpu_baseline_reference(conn, cfg, init, steps=3):
+def cpu_baseline_reference(name, cfg, steps=3):
     kmf = reference_package()
     if kmf is None or cfg.order != 2:
         return None
-    rconn, prims, counted, desc = reference_sample(kmf, conn, init.as_array(), cfg)
+    rconn, prims, counted, desc = reference_patch(kmf, name)
     t, threads = time_reference(kmf, rconn, prims, cfg, steps, 1)
     sec = float(np.median(t))
     return {"value": counted / sec, "unit": UNIT, "cores": threads, "kind": "reference",
@@ -481,6 +454,19 @@ def run_ours(args):
         print(f"[bench] device context {time.perf_counter() - t:.1f} s", file=sys.stderr, flush=True)
         local_init = init.as_array()
     n_local = local_init.shape[1]
+    part_stats = None
+    if ws > 1:
+        # per-rank partition shape (rank 0 reports all ranks): owned and halo
+        # points, the interior pass (owned points deep enough to run before
+        # the stage's halo exchange lands) and the exchange volume
+        mine = {"owned": part.n_owned, "halo": int(part.global_ids.size - part.n_owned),
+                "interior_flux": int(part.interior_end[min(cfg.n_inner + 3, part.depth + 1)]),
+                "recv_points": int(sum(v.size for v in part.recv.values())), "peers": len(part.recv)}
+        every = [None] * ws
+        dist.all_gather_object(every, mine)
+        part_stats = {"scheme": args.partition, "depth": part.depth, "ranks": every,
+                      "interior_flux_fraction_min": min(r["interior_flux"] / r["owned"] for r in every),
+                      "halo_fraction_max": max(r["halo"] / r["owned"] for r in every)}
     params = _params(cfg)
     peak_fp64 = C.c_double(0.0)
     _lib.check(L.kmf_fp64_peak(C.byref(peak_fp64)), "kmf_fp64_peak")
@@ -589,10 +575,11 @@ def run_ours(args):
         "roofline_qgrad": qgrad_roofline(n_grad, fo_launch_s, sweep_launch_s, hbm_peak, peak_kind, float(
             kern_s[1] + kern_s[2]) / (step_ms[:K].sum() * 1e-3)) if n_sweeps else None,
         "clocks": clk.summary(),
+        "partition": part_stats,
     }
     if not args.no_cpu_baseline and ws == 1:
         port = cpu_baseline(conn, cfg, init)
-        ref = cpu_baseline_reference(conn, cfg, init)
+        ref = cpu_baseline_reference(args.config, cfg)
         line["cpu_baseline"] = ref or port
         if ref:
             line["cpu_baseline_port"] = port
@@ -602,26 +589,32 @@ def run_ours(args):
 def run_reference(args):
     """The reference arm: the reference package's own solve (kmf from
     baseline/_ref, numpy, all host threads) on a bounded sample of the
-    configuration, one outer iteration per step; the oracle port (C/OpenMP
-    restatement) when the package is not installed."""
+    configuration that the reference package itself generates, builds and
+    initialises (reference_patch: no code of this repo runs or is loaded),
+    one outer iteration per step; the oracle port (C/OpenMP restatement)
+    when the package is not installed or for the first-order scheme."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    cloud, conn, cfg, init = setup(args.config)
-    n = cloud.n_points
     W, K = max(args.warmup, 0), args.steps
     kmf = reference_package()
-    if kmf is not None and cfg.order == 2:
-        rconn, prims, npts, desc = reference_sample(kmf, conn, init.as_array(), cfg)
+    order = 1 if args.config in ORDER else 2
+    if kmf is not None and order == 2:
+        rconn, prims, npts, desc = reference_patch(kmf, args.config)
+        _, _, _, mach, aoa, _ = CONFIGS[args.config]
+        cfg = type("Cfg", (), dict(mach=mach, aoa_deg=aoa, gamma=1.4, cfl=0.2, n_inner=3, mode="fused"))()
         t, threads = time_reference(kmf, rconn, prims, cfg, K, W)
         sec = float(sum(t))
         kind = "reference"
         sample = (f"each step one outer iteration of the reference package kmf (numpy, baseline/_ref) solve() "
                   f"({K} timed after {W} warm-up) on {desc}; threads={threads}")
+        n = None
     else:
         from oracle import oracle as O
         from paper_2108_07031_b200 import free_stream
 
+        cloud, conn, cfg, init = setup(args.config)
+        n = cloud.n_points
         threads = os.cpu_count() or 1
         O.set_threads(threads)
         pk, prims, npts, desc = oracle_sample(conn, init.as_array(), cfg)
@@ -643,7 +636,8 @@ def run_reference(args):
         "warmup": W, "ms_per_step": 1e3 * sec / K, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": value / PUBLISHED[args.config] if args.config in PUBLISHED else None,
         "dtype": "f64", "data": "synthetic (procedurally generated NACA 0012 O-cloud)",
-        "config": {"workload": CONFIGS[args.config][5], "config_key": args.config, "n_points": n},
+        "config": {"workload": CONFIGS[args.config][5], "config_key": args.config,
+                   "n_points": n if n is not None else CONFIG_POINTS.get(args.config)},
         "rdp_s_per_point_iter": 1.0 / value,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

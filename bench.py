@@ -301,6 +301,12 @@ def reference_patch(kmf, name, target=REF_SAMPLE_POINTS):
     m, L, g, mach, aoa, _ = CONFIGS[name]
     G = kmf.geometry
     cloud = G.generate_naca_cloud(m, L, g, 20.0)
+    cfg = kmf.solver.SolverConfig(mach=mach, aoa_deg=aoa, n_outer=1)
+    if cloud.n_points <= 1.5 * target:  # small configurations: the whole cloud
+        rconn = G.build_stencils(cloud)
+        desc = (f"the whole {cloud.n_points}-point configuration cloud, generated, built and initialised by the "
+                f"reference package itself")
+        return rconn, kmf.solver._initial_primitives(cfg, cloud), cloud.n_points, desc
     w = np.flatnonzero(cloud.flag == 1)
     c0 = int(w[np.argmin(cloud.x[w])])
     xc, yc = float(cloud.x[c0]), float(cloud.y[c0])
@@ -314,7 +320,6 @@ def reference_patch(kmf, name, target=REF_SAMPLE_POINTS):
     nx[rim], ny[rim] = (x[rim] - xc) / dd[rim], (y[rim] - yc) / dd[rim]
     sub = G.PointCloud(x, y, flag, nx, ny)
     rconn = G.build_stencils(sub)
-    cfg = kmf.solver.SolverConfig(mach=mach, aoa_deg=aoa, n_outer=1)
     prims = kmf.solver._initial_primitives(cfg, sub)
     desc = (f"a {target}-point patch of the {cloud.n_points}-point configuration cloud around the leading edge "
             f"({int((flag == 1).sum())} wall points, {int(rim.sum())} rim points as far field), generated, built "

@@ -145,6 +145,10 @@ int kmf_set_state(kmf_ctx *ctx, const double *prims);
  * + residue; history[0..*iters_done-1] = residue_norm per iteration. */
 int kmf_run(kmf_ctx *ctx, const kmf_params *p, int n_iter, double *history, int *iters_done,
             int *converged);
+/* capture (once) the iteration graphs a kmf_run with these parameters
+ * replays -- optional: kmf_run captures on first use; solve() calls it
+ * before its timed chunk so graph capture is not timed */
+int kmf_prepare(kmf_ctx *ctx, const kmf_params *p);
 /* final primitives and conserved (each (4,n)), either may be NULL */
 int kmf_get_state(kmf_ctx *ctx, double *prims, double *U);
 /* device seconds per STAGE_NAMES key (solver.py:53-60) accumulated by the

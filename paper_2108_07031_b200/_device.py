@@ -139,6 +139,10 @@ class DeviceConnectivity:
         _lib.check(rc, "kmf_run")
         return hist[: done.value].copy(), done.value, bool(conv.value)
 
+    def prepare(self, params: _lib.Params):
+        """Capture the iteration graphs a run with `params` replays (not timed)."""
+        _lib.check(_lib.lib().kmf_prepare(self._h, C.byref(params)), "kmf_prepare")
+
     def get_state(self):
         prims = np.empty((4, self.n))
         U = np.empty((4, self.n))

@@ -96,6 +96,7 @@ def lib():
         "kmf_destroy": (None, [vp]),
         "kmf_set_state": (C.c_int, [vp, _dp]),
         "kmf_run": (C.c_int, [vp, C.POINTER(Params), C.c_int, _dp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+        "kmf_prepare": (C.c_int, [vp, C.POINTER(Params)]),
         "kmf_get_state": (C.c_int, [vp, _dp, _dp]),
         "kmf_stage_seconds": (C.c_int, [vp, _dp]),
         "kmf_last_error": (C.c_int, [vp, C.POINTER(ErrorInfo)]),
@@ -139,7 +140,7 @@ def lib():
 
 EXPORTED = (
     "kmf_abi_version", "kmf_device_count", "kmf_strerror", "kmf_create", "kmf_destroy",
-    "kmf_set_state", "kmf_run", "kmf_get_state", "kmf_stage_seconds", "kmf_last_error",
+    "kmf_set_state", "kmf_run", "kmf_prepare", "kmf_get_state", "kmf_stage_seconds", "kmf_last_error",
     "kmf_last_indices", "kmf_diag_flux", "kmf_diag_frame", "kmf_diag_stage_state",
     "kmf_op_timestep", "kmf_op_first_order", "kmf_op_q_derivatives", "kmf_op_flux_residual",
     "kmf_op_boundary", "kmf_op_primitives_to_q", "kmf_op_q_to_primitives",

@@ -76,8 +76,7 @@ struct DBuf {
 
 struct GraphKey {
     double gamma, cfl, fs[4], tol;
-    int n_inner, mode, unroll, cap, base, how;
-    const void *hist;
+    int n_inner, mode, unroll, how;
     bool operator==(const GraphKey &o) const { return std::memcmp(this, &o, sizeof o) == 0; }
 };
 
@@ -934,8 +933,7 @@ void enqueue_iteration(kmf_ctx *c, StageCtx &sc)
     }
 }
 
-int get_graph(kmf_ctx *c, const kmf_params *p, int unroll, double *hist, int hist_base, int cap, Graph &gr,
-              int how = ITER_PLAIN)
+int get_graph(kmf_ctx *c, const kmf_params *p, int unroll, Graph &gr, int how = ITER_PLAIN)
 {
     GraphKey k;
     std::memset(&k, 0, sizeof k);
@@ -946,15 +944,12 @@ int get_graph(kmf_ctx *c, const kmf_params *p, int unroll, double *hist, int his
     k.n_inner = p->n_inner;
     k.mode = p->mode;
     k.unroll = unroll;
-    k.cap = cap;
-    k.base = hist_base;
     k.how = how;
-    k.hist = hist;
     if (gr.exec && gr.key == k) return KMF_OK;
     gr.reset();
     cudaGraph_t graph;
     c->cap_ev = how == ITER_PLAIN ? nullptr : &gr.ev;
-    StageCtx sc{p, IterOut{hist, hist_base, cap, p->convergence_tol, 1}, how, false};
+    StageCtx sc{p, IterOut{p->convergence_tol, 1}, how, false};
     c->nlaunch = 0;
     CK(cudaStreamBeginCapture(c->s0, cudaStreamCaptureModeThreadLocal));
     for (int u = 0; u < unroll; u++) enqueue_iteration(c, sc);
@@ -1045,12 +1040,14 @@ int seed_state(kmf_ctx *c, double gamma, double cfl)
     return KMF_OK;
 }
 
-int reset_run_ctrl(kmf_ctx *c)
+int reset_run_ctrl(kmf_ctx *c, int hist_cap)
 {
     Ctrl init;
     std::memset(&init, 0, sizeof init);
     init.iter = 1;
     init.epoch = 1;
+    init.history = c->history.p;
+    init.hist_cap = hist_cap;
     CK(cudaMemcpyAsync(c->ctrl.p, &init, sizeof init, cudaMemcpyHostToDevice, c->s0));
     CK(cudaStreamSynchronize(c->s0));  // `init` is a stack temporary
     return KMF_OK;
@@ -1132,7 +1129,7 @@ int kmf_run(kmf_ctx *c, const kmf_params *p, int n_iter, double *history, int *i
     if (n_iter == 0) return KMF_OK;
     if (int rc = seed_state(c, p->gamma, p->cfl)) return rc;
     if ((int)c->history.n < n_iter) CK(c->history.alloc(n_iter));
-    if (int rc = reset_run_ctrl(c)) return rc;
+    if (int rc = reset_run_ctrl(c, n_iter)) return rc;
     for (double &s : c->stage_sec) s = 0.0;
 
     // graphs of U iterations (U = 8, then 1 for the rest); the timed
@@ -1146,7 +1143,7 @@ int kmf_run(kmf_ctx *c, const kmf_params *p, int n_iter, double *history, int *i
             const int reps = pass ? rest : full, unroll = pass ? 1 : U;
             if (!reps) continue;
             Graph &gr = pass ? c->g1 : c->gU;
-            if (int rc = get_graph(c, p, unroll, c->history.p, 1, n_iter, gr, how)) return rc;
+            if (int rc = get_graph(c, p, unroll, gr, how)) return rc;
             for (int k = 0; k < reps; k++) {
                 CK(cudaGraphLaunch(gr.exec, c->s0));
                 if (how == ITER_INSTRUMENT) {
@@ -1182,6 +1179,20 @@ int kmf_run(kmf_ctx *c, const kmf_params *p, int n_iter, double *history, int *i
         return KMF_EPOSITIVITY;
     }
     return KMF_OK;
+}
+
+int kmf_prepare(kmf_ctx *c, const kmf_params *p)
+{
+    if (!c || !p) return KMF_EINVAL;
+    if (int rc = check_params(c, p)) return rc;
+    if (c->dist_on && !c->nccl) {
+        set_msg("kmf_prepare: partitioned context without NCCL");
+        return KMF_EINVAL;
+    }
+    CK(cudaSetDevice(c->device));
+    const int how = p->instrument ? ITER_INSTRUMENT : ITER_PLAIN;
+    if (int rc = get_graph(c, p, 8, c->gU, how)) return rc;
+    return get_graph(c, p, 1, c->g1, how);
 }
 
 int kmf_get_state(kmf_ctx *c, double *prims, double *U)
@@ -1655,12 +1666,12 @@ int kmf_bench_steps(kmf_ctx *c, const kmf_params *p, int n_steps, int64_t flush_
     if (int rc = seed_state(c, p->gamma, p->cfl)) return rc;
     if ((int)c->history.n < 2 * n_steps) CK(c->history.alloc(2 * n_steps));
     if (flush_bytes > 0 && (int64_t)c->flush.n < flush_bytes) CK(c->flush.alloc((size_t)flush_bytes));
-    if (int rc = reset_run_ctrl(c)) return rc;
+    if (int rc = reset_run_ctrl(c, 2 * n_steps)) return rc;
     kmf_params q = *p;
     q.convergence_tol = 0.0;
     for (int pass = 0; pass < 2; pass++) {
         Graph &gr = pass ? c->gB : c->g1;
-        if (int rc = get_graph(c, &q, 1, c->history.p, 1, 2 * n_steps, gr, pass ? ITER_BENCH : ITER_PLAIN))
+        if (int rc = get_graph(c, &q, 1, gr, pass ? ITER_BENCH : ITER_PLAIN))
             return rc;
         for (int i = 0; i < n_steps; i++) {
             if (flush_bytes > 0) CK(cudaMemsetAsync(c->flush.p, i & 0xff, (size_t)flush_bytes, c->s0));
@@ -1957,7 +1968,7 @@ extern "C" int kmf_run_group(kmf_ctx **ctxs, int nctx, const kmf_params *p, int 
         c->err = kmf_error_info{};
         if (int rc = seed_state(c, p->gamma, p->cfl)) return rc;
         if ((int)c->history.n < n_iter) CK(c->history.alloc(n_iter));
-        if (int rc = reset_run_ctrl(c)) return rc;
+        if (int rc = reset_run_ctrl(c, n_iter)) return rc;
         enqueue_pack(c, c->s0);  // the halo q the first band pass reads (and a continuation needs)
     }
     auto sync_all = [&]() -> int {
@@ -1994,7 +2005,7 @@ extern "C" int kmf_run_group(kmf_ctx **ctxs, int nctx, const kmf_params *p, int 
             std::vector<double *> Gs(nctx, nullptr);
             std::vector<StageCtx> sc;
             for (kmf_ctx *c : byrank)
-                sc.push_back(StageCtx{p, IterOut{c->history.p, 1, n_iter, p->convergence_tol, 0}, ITER_PLAIN, false});
+                sc.push_back(StageCtx{p, IterOut{p->convergence_tol, 0}, ITER_PLAIN, false});
             for (int r = 0; r < nctx; r++) {
                 CK(cudaSetDevice(byrank[r]->device));
                 enqueue_head(byrank[r], sc[r], stage, Gs[r]);  // interior pass: no halo data read
@@ -2019,7 +2030,7 @@ extern "C" int kmf_run_group(kmf_ctx **ctxs, int nctx, const kmf_params *p, int 
         for (kmf_ctx *c : byrank) {
             CK(cudaSetDevice(c->device));
             CK(cudaMemcpy(c->ctrl.p->limbs, tot.data(), sizeof(unsigned long long) * kLimbs, cudaMemcpyHostToDevice));
-            IterOut io{c->history.p, 1, n_iter, p->convergence_tol, 0};
+            IterOut io{p->convergence_tol, 0};
             k_close<<<1, kTB, 0, c->s0>>>(c->ctrl.p, (int)c->n_global, io);
             CK(cudaGetLastError());
         }

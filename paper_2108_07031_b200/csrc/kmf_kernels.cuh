@@ -47,6 +47,8 @@ struct Ctrl {
     unsigned int ctx_mask;
     unsigned int blocks_done;   // last-block detection of the stage-4 update
     unsigned long long resmax;  // inner-residual max (bits of a nonnegative double)
+    double *history;            // residue_norm of iteration k at history[k - 1], k <= hist_cap
+    int hist_cap;
     unsigned long long limbs[kLimbs];
 };
 
@@ -555,9 +557,9 @@ __device__ __forceinline__ void accum_add_warp(unsigned long long *limbs, double
 
 KMF_HD double accum_round(const unsigned long long *limbs);
 
+// Per-launch iteration-close parameters (the history buffer and its size
+// live in Ctrl, set per run, so captured graphs do not depend on them).
 struct IterOut {
-    double *history;
-    int hist_base, cap;
     double tol;
     int close_in_kernel;  // 0 under a partition: limbs are all-reduced first, then k_close
 };
@@ -573,8 +575,8 @@ __device__ __noinline__ void close_iteration(Ctrl *c, const unsigned long long *
     if (st == 0ull) {
         const double res = sqrt(accum_round(limbs) / (double)n);
         const int it = c->iter;
-        const int h = it - io.hist_base;
-        if (h >= 0 && h < io.cap) io.history[h] = res;
+        const int h = it - 1;
+        if (h >= 0 && h < c->hist_cap) c->history[h] = res;
         if (io.tol > 0.0 && res <= io.tol) c->state = ((unsigned long long)seq_of(ep, kStageFinal, 0) << 2) | 2ull;
         c->iter = it + 1;
     }

@@ -564,7 +564,7 @@ def run_ours(args):
         "rdp_s_per_point_iter": 1.0 / value,
         "e2e": e2e,
         "gpu_launches": int(lps.value) * K,
-        "roofline": {"bound": "hbm", "kernel": "k_flux3<fused> (flux_residual interior)",
+        "roofline": {"bound": "hbm", "kernel": "k_flux<fused> (flux_residual interior)",
                      "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": achieved_gbs / hbm_peak,
                      "traffic": traffic, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
                      "bytes_per_point": FLUX_BYTES_PER_POINT, "launch_us": flux_launch_s * 1e6,

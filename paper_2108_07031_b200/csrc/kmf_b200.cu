@@ -530,9 +530,6 @@ int build_context(kmf_ctx *c, const kmf_geometry *g)
     // q-gradient time at 160K / 2.5M / 10M against 2 threads per point;
     // small clouds keep 2 threads per point (more threads in flight)
     c->qg_nc = n > 100000 ? 4 : 2;
-#ifdef KMF_QG_NC_FORCE
-    c->qg_nc = KMF_QG_NC_FORCE;
-#endif
     return KMF_OK;
 }
 

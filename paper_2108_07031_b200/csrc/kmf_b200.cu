@@ -1986,10 +1986,15 @@ extern "C" int kmf_run_group(kmf_ctx **ctxs, int nctx, const kmf_params *p, int 
                     set_msg("kmf_run_group: send/recv lists of ranks %d and %d disagree", src->rank, dst->rank);
                     return KMF_EINVAL;
                 }
-                if (dst->recv_cnt[k])
-                    CK(cudaMemcpyPeer(dst->recvbuf.p + 4 * dst->recv_off[k], dst->device,
-                                      src->sendbuf.p + 4 * src->send_off[j], src->device,
-                                      sizeof(double) * 4 * dst->recv_cnt[k]));
+                // on the receiver's solver stream, ahead of its unpack (the
+                // context streams are non-blocking: a legacy-stream copy would
+                // not be ordered before the unpack kernel)
+                if (dst->recv_cnt[k]) {
+                    CK(cudaSetDevice(dst->device));
+                    CK(cudaMemcpyPeerAsync(dst->recvbuf.p + 4 * dst->recv_off[k], dst->device,
+                                           src->sendbuf.p + 4 * src->send_off[j], src->device,
+                                           sizeof(double) * 4 * dst->recv_cnt[k], dst->s0));
+                }
             }
         for (kmf_ctx *c : byrank) {
             CK(cudaSetDevice(c->device));

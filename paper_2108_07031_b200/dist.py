@@ -143,14 +143,17 @@ def solve_group(config: SolverConfig, cloud, conn: Connectivity, nranks: int, in
                                   C.byref(conv))
     if rc == _lib.KMF_EPOSITIVITY:
         # the reference raises at the earliest failing (iteration, stage)
-        # over the whole cloud
+        # over the whole cloud, and within a stage at its first raise site
+        # (interior flux < wall < outer closures < decode: context order)
         failed = sorted(((rp, info) for rp in ranks for info in [_rank_error(rp)]
-                         if info.code == _lib.KMF_EPOSITIVITY), key=lambda f: (f[1].iteration, f[1].stage))
-        dec = [_decode_failures(rp, info, p) for rp, info in failed if info.context in _C2P]
-        if dec and len(dec) == len(failed):
+                         if info.code == _lib.KMF_EPOSITIVITY),
+                        key=lambda f: (f[1].iteration, f[1].stage, f[1].context))
+        first = (failed[0][1].iteration, failed[0][1].stage)
+        earliest = [(rp, info) for rp, info in failed if (info.iteration, info.stage) == first]
+        dec = [_decode_failures(rp, info, p) for rp, info in earliest if info.context in _C2P]
+        if dec and len(dec) == len(earliest):
             _raise_merged_decode(dec, cloud.n_points)
-        for rp, info in failed:
-            _raise_rank_error(rp, p)
+        _raise_rank_error(earliest[0][0], p)
     _lib.check(rc, "kmf_run_group")
     n = cloud.n_points
     prims, U = np.empty((4, n)), np.empty((4, n))

@@ -125,8 +125,13 @@ struct kmf_ctx {
     bool xy = true;  // offsets recomputed from coordinates
     int qg_nc = 2;   // q-gradient components per thread (4 above 100K points)
     bool has_perm = false;
-    cudaStream_t s0 = nullptr, s1 = nullptr, s2 = nullptr;  // solver, boundary branch, halo exchange
+    // solver, boundary branch, halo exchange, band pass (partitions)
+    cudaStream_t s0 = nullptr, s1 = nullptr, s2 = nullptr, s3 = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr, xfork = nullptr, xjoin = nullptr;
+    // band pass: stage start on s0 / halo unpacked (group runner) / done
+    cudaEvent_t bfork = nullptr, bready = nullptr, bjoin = nullptr;
+    static constexpr int kMaxEv = 10;
+    cudaEvent_t lev[kMaxEv] = {};                  // interior pass: level k written
 
     // geometry
     DBuf<double> x, y, pxy, dmin, fsum, fcoef, edx, edy;
@@ -183,6 +188,7 @@ struct kmf_ctx {
     // reads lower levels at slots the interior pass already advanced, so the
     // single-domain ping-pong (GA, GB) would have been overwritten
     static constexpr int kMaxLevels = 8;
+    static_assert(kMaxLevels < kMaxEv, "one interior-level event per gradient level");
     DBuf<double> Glev[kMaxLevels];
     void *nccl = nullptr;  // ncclComm_t when the NCCL transport is initialised
     void (*nccl_destroy)(void *) = nullptr;
@@ -239,9 +245,11 @@ struct kmf_ctx {
         drop_graphs();
         for (auto &e : evs)
             if (e) cudaEventDestroy(e);
-        for (cudaEvent_t e : {fork, join, xfork, xjoin})
+        for (cudaEvent_t e : {fork, join, xfork, xjoin, bfork, bready, bjoin})
             if (e) cudaEventDestroy(e);
-        for (cudaStream_t s : {s0, s1, s2})
+        for (cudaEvent_t e : lev)
+            if (e) cudaEventDestroy(e);
+        for (cudaStream_t s : {s0, s1, s2, s3})
             if (s) cudaStreamDestroy(s);
     }
 };
@@ -522,8 +530,9 @@ int build_context(kmf_ctx *c, const kmf_geometry *g)
     CK(cudaMemset(c->ctrl.p, 0, sizeof(Ctrl)));
     CK(cudaMemset(c->R.p, 0, sizeof(double) * 4 * ld));
     CK(c->diag.alloc(std::max<long long>(E, std::max(std::max(c->bedges[0], c->bedges[1]), c->bedges[2])) + 1));
-    for (cudaStream_t *s : {&c->s0, &c->s1, &c->s2}) CK(cudaStreamCreateWithFlags(s, cudaStreamNonBlocking));
-    for (cudaEvent_t *e : {&c->fork, &c->join, &c->xfork, &c->xjoin})
+    for (cudaStream_t *s : {&c->s0, &c->s1, &c->s2, &c->s3}) CK(cudaStreamCreateWithFlags(s, cudaStreamNonBlocking));
+    for (cudaEvent_t &e : c->lev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (cudaEvent_t *e : {&c->fork, &c->join, &c->xfork, &c->xjoin, &c->bfork, &c->bready, &c->bjoin})
         CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     for (auto &e : c->evs) CK(cudaEventCreate(&e));
     // one thread per point (all 4 components) from 160K points up: -6 %
@@ -563,19 +572,21 @@ struct Mark {
     kmf_ctx *c;
     int cls;
     bool on;
+    cudaStream_t st;
     cudaEvent_t a = nullptr;
-    Mark(kmf_ctx *c_, int cls_, bool on_) : c(c_), cls(cls_), on(on_ && c_->cap_ev)
+    Mark(kmf_ctx *c_, int cls_, bool on_, cudaStream_t st_ = nullptr)
+        : c(c_), cls(cls_), on(on_ && c_->cap_ev), st(st_ ? st_ : c_->s0)
     {
         if (!on) return;
         cudaEventCreate(&a);
-        cudaEventRecordWithFlags(a, c->s0, cudaEventRecordExternal);
+        cudaEventRecordWithFlags(a, st, cudaEventRecordExternal);
     }
     ~Mark()
     {
         if (!on) return;
         cudaEvent_t b;
         cudaEventCreate(&b);
-        cudaEventRecordWithFlags(b, c->s0, cudaEventRecordExternal);
+        cudaEventRecordWithFlags(b, st, cudaEventRecordExternal);
         c->cap_ev->push_back(EvPair{cls, a, b});
     }
 };
@@ -633,18 +644,25 @@ void launch_sweep(kmf_ctx *c, cudaStream_t s, int lo, int hi, const double *Gin,
 
 // q-derivatives of one stage over one pass: level 0 (first order), then
 // the n_inner sweeps, level k reading level k-1; returns the final level.
+// Partitions: the interior pass records lev[k] after writing level k; the
+// band pass (its own stream) waits for lev[k-1] before level k, since a band
+// slot reads level k-1 at interior neighbours.
 double *launch_qgrad(kmf_ctx *c, cudaStream_t s, int stage, int n_inner, Ctrl *ctl, bool band, bool timed)
 {
+    const bool ev = c->dist_on;  // n_inner + 2 <= depth <= kMaxLevels < kMaxEv (check_params)
     int lo, hi;
     {
-        Mark m(c, KC_FO, timed);
+        Mark m(c, KC_FO, timed, s);
         stage_range(c, 0, false, band, lo, hi);
         launch_first_order(c, s, lo, hi, c->gbuf(0), ctl, stage);
+        if (ev && !band) cudaEventRecord(c->lev[0], s);
     }
-    Mark m(c, KC_SWEEP, timed);
+    Mark m(c, KC_SWEEP, timed, s);
     for (int it = 0; it < n_inner; it++) {
+        if (ev && band) cudaStreamWaitEvent(s, c->lev[it], 0);
         stage_range(c, 1 + it, false, band, lo, hi);
         launch_sweep(c, s, lo, hi, c->gbuf(it), c->gbuf(it + 1), ctl, stage, 1 + it, 0, it + 1 == n_inner);
+        if (ev && !band) cudaEventRecord(c->lev[it + 1], s);
     }
     return c->gbuf(n_inner);
 }
@@ -812,8 +830,9 @@ ncclResult_t enqueue_exchange_nccl(kmf_ctx *c, cudaStream_t s)
 // ---------------------------------------------------------- one RK stage
 // Per stage (solver.py:524-549) on s0:
 //   interior pass: q-gradients, interior flux            (no halo data read)
-//   [partition: wait for the halo q exchanged after the previous update]
-//   band pass: q-gradients, boundary closure on a forked branch, band flux
+//   band pass (partition, stream s3): after the halo q exchanged after the
+//     previous update, level k once the interior pass wrote level k-1;
+//     boundary closure, band flux
 //   update (+ stage 4: residue limbs; partition: limb all-reduce, close)
 //   [NCCL partition: fork the halo exchange of the new q onto s2; the next
 //    stage's interior pass overlaps it]
@@ -833,6 +852,7 @@ void enqueue_head(kmf_ctx *c, StageCtx &sc, int stage, double *&G)
     const kmf_params *p = sc.p;
     Ctrl *ctl = c->ctrl.p;
     const bool inst = sc.how == ITER_INSTRUMENT, bench = sc.how == ITER_BENCH;
+    if (c->dist_on) cudaEventRecord(c->bfork, c->s0);  // the band pass starts from here (enqueue_tail)
     {
         Mark m(c, KC_QGRAD, inst);
         if (p->n_inner > 0) {
@@ -861,26 +881,31 @@ void enqueue_tail(kmf_ctx *c, StageCtx &sc, int stage, const double *G)
     Ctrl *ctl = c->ctrl.p;
     const bool inst = sc.how == ITER_INSTRUMENT, bench = sc.how == ITER_BENCH;
     if (c->dist_on) {
+        // band pass on s3, concurrent with the rest of the interior pass: it
+        // needs the halo (the exchange joined, or the group runner's unpack
+        // marked by bready) and, per level, the interior level below it
+        cudaStream_t sb = c->s3;
+        cudaStreamWaitEvent(sb, c->bfork, 0);  // the previous update
         if (sc.xchg_pending) {
-            cudaStreamWaitEvent(c->s0, c->xjoin, 0);
+            cudaStreamWaitEvent(sb, c->xjoin, 0);
             sc.xchg_pending = false;
         }
-        {
-            Mark m(c, KC_QGRAD, inst);
-            if (p->n_inner > 0) launch_qgrad(c, c->s0, stage, p->n_inner, ctl, true, bench);
+        if (!c->nccl) cudaStreamWaitEvent(sb, c->bready, 0);
+        if (p->n_inner > 0) {
+            launch_qgrad(c, sb, stage, p->n_inner, ctl, true, false);
+            // boundary and band flux read the final level at interior slots
+            cudaStreamWaitEvent(sb, c->lev[p->n_inner], 0);
+        } else {
+            cudaEventRecord(c->fork, c->s0);  // the zeroed gradients
+            cudaStreamWaitEvent(sb, c->fork, 0);
         }
-        Mark m(c, KC_FLUXBND, inst);
-        cudaEventRecord(c->fork, c->s0);
-        cudaStreamWaitEvent(c->s1, c->fork, 0);
-        launch_boundary(c, c->s1, G, p->fs, p->gamma, ctl, stage);
-        cudaEventRecord(c->join, c->s1);
+        launch_boundary(c, sb, G, p->fs, p->gamma, ctl, stage);
         int lo, hi;
         stage_range(c, p->n_inner > 0 ? p->n_inner + 1 : 0, true, true, lo, hi);
-        {
-            Mark mf(c, KC_FLUX, bench);
-            launch_flux(c, c->s0, lo, hi, G, p->mode, p->gamma, 0, ctl, stage);
-        }
-        cudaStreamWaitEvent(c->s0, c->join, 0);
+        launch_flux(c, sb, lo, hi, G, p->mode, p->gamma, 0, ctl, stage);
+        cudaEventRecord(c->bjoin, sb);
+        Mark m(c, KC_FLUXBND, inst);
+        cudaStreamWaitEvent(c->s0, c->bjoin, 0);
     } else {
         Mark m(c, KC_FLUXBND, inst);
         cudaStreamWaitEvent(c->s0, c->join, 0);
@@ -1999,6 +2024,7 @@ extern "C" int kmf_run_group(kmf_ctx **ctxs, int nctx, const kmf_params *p, int 
         for (kmf_ctx *c : byrank) {
             CK(cudaSetDevice(c->device));
             enqueue_unpack(c, c->s0);
+            CK(cudaEventRecord(c->bready, c->s0));
         }
         return KMF_OK;
     };

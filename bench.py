@@ -24,8 +24,12 @@ Reported (ours):
                  stream, L2 flushed (256 MiB memset) between timed steps
                  (the 40M state is also far larger than L2);
   e2e            the same metric through the C ABI with host buffers: per
-                 step kmf_set_state (pinned H2D of the primitives) +
-                 kmf_run(1) + kmf_get_state (D2H primitives + residue);
+                 step the pinned H2D of the initial primitives, one outer
+                 iteration and the D2H of the final primitives + residue
+                 (kmf_run_cases: step k+1's upload and step k-1's download
+                 overlap step k's iteration); e2e.serial the same three
+                 transfers/calls one after another (kmf_set_state + kmf_run
+                 + kmf_get_state), checked bitwise equal;
   roofline       flux_residual interior kernel (the dominant kernel) against
                  HBM (MEASURED_PEAKS.json) -- it is FP64-bound, so
                  roofline_fp64 reports executed DP-pipe instructions against
@@ -500,29 +504,53 @@ def run_ours(args):
     stage_share = float(kern_s[0] / (step_ms[:K].sum() * 1e-3))
 
     # ---- end to end through the C ABI with pinned host buffers ------------
+    # (1) kmf_run_cases: every step is one case -- upload of its initial
+    # state, one outer iteration, download of its final state and residue --
+    # with step k+1's upload and step k-1's download on the copy engines
+    # while step k iterates; (2) the same three calls serialised per step
+    # (kmf_set_state + kmf_run + kmf_get_state).
     host_in = _lib.pinned((4, n_local))
-    host_out = _lib.pinned((4, n_local))
+    host_out = [_lib.pinned((4, n_local)) for _ in range(2)]
     host_in[...] = local_init
     hist = np.zeros(1)
     done, conv = C.c_int(0), C.c_int(0)
     e2e_params = _params(cfg)
 
-    def e2e_step():
+    def cases(m):
+        parr = (_lib.Params * m)(*([e2e_params] * m))
+        pin = (C.c_void_p * m)(*([host_in.ctypes.data] * m))
+        pout = (C.c_void_p * m)(*[host_out[k % 2].ctypes.data for k in range(m)])
+        hist_c = np.zeros(m)
+        _lib.check(L.kmf_run_cases(dev.handle, parr, 1, m, pin, pout, _lib.dptr(hist_c), None, None, None),
+                   "run_cases")
+        return hist_c
+
+    def serial_step():
         _lib.check(L.kmf_set_state(dev.handle, _lib.dptr(host_in)), "set_state")
         _lib.check(L.kmf_run(dev.handle, C.byref(e2e_params), 1, _lib.dptr(hist), C.byref(done), C.byref(conv)),
                    "run")
-        _lib.check(L.kmf_get_state(dev.handle, _lib.dptr(host_out), None), "get_state")
+        _lib.check(L.kmf_get_state(dev.handle, _lib.dptr(host_out[0]), None), "get_state")
 
+    cases(max(W, 2))
+    barrier(dist)
+    t0 = time.perf_counter()
+    e2e_hist = cases(K)
+    e2e_s = allreduce_max(dist, time.perf_counter() - t0)
+    streamed = host_out[(K - 1) % 2].copy()
     for _ in range(max(W, 1)):
-        e2e_step()
+        serial_step()
     barrier(dist)
     t0 = time.perf_counter()
     for _ in range(K):
-        e2e_step()
-    e2e_s = allreduce_max(dist, time.perf_counter() - t0)
+        serial_step()
+    ser_s = allreduce_max(dist, time.perf_counter() - t0)
+    if not (np.all(e2e_hist == hist[0]) and np.array_equal(streamed, host_out[0])):
+        raise SystemExit("bench: streamed and serial end-to-end steps disagree")
     e2e = {"value": n * K / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 4 * n_local * 8,
            "d2h_bytes_per_step": 4 * n_local * 8 + 8, "ms_per_step": 1e3 * e2e_s / K,
-           "path": "kmf_set_state(pinned) + kmf_run(1 iteration) + kmf_get_state(pinned)"}
+           "path": "kmf_run_cases (pinned host in/out per step, copies overlapped with the previous/next step)",
+           "serial": {"value": n * K / ser_s, "ms_per_step": 1e3 * ser_s / K,
+                      "path": "kmf_set_state(pinned) + kmf_run(1 iteration) + kmf_get_state(pinned) per step"}}
 
     if rank != 0:
         return

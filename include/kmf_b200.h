@@ -149,6 +149,21 @@ int kmf_run(kmf_ctx *ctx, const kmf_params *p, int n_iter, double *history, int 
  * replays -- optional: kmf_run captures on first use; solve() calls it
  * before its timed chunk so graph capture is not timed */
 int kmf_prepare(kmf_ctx *ctx, const kmf_params *p);
+/* Streaming cases: n_cases independent solves on this context's cloud,
+ * case k = kmf_set_state(prims_in[k]) + kmf_run(&params[k], n_iter,
+ * instrument off) + kmf_get_state(prims_out[k]) with the same results bit
+ * for bit, pipelined: case k+1's upload and case k-1's download run on the
+ * copy engines while case k iterates (host buffers should be pinned,
+ * kmf_host_alloc; they are read / written asynchronously until the call
+ * returns).  The reference's harness runs such batches one solve at a time
+ * (bench.py:174-215 sweep).  Outputs per case k: history[k*n_iter + i]
+ * (0 past iters_done[k]), iters_done[k], converged[k], status[k]
+ * (KMF_OK / KMF_EPOSITIVITY); any may be NULL.  Returns KMF_EPOSITIVITY if
+ * a case failed (kmf_last_error: the first failing case), after running
+ * every case.  The context keeps the last case's final state. */
+int kmf_run_cases(kmf_ctx *ctx, const kmf_params *params, int n_iter, int n_cases,
+                  const double *const *prims_in, double *const *prims_out, double *history,
+                  int *iters_done, int *converged, int *status);
 /* final primitives and conserved (each (4,n)), either may be NULL */
 int kmf_get_state(kmf_ctx *ctx, double *prims, double *U);
 /* device seconds per STAGE_NAMES key (solver.py:53-60) accumulated by the

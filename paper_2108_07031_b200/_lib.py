@@ -97,6 +97,9 @@ def lib():
         "kmf_set_state": (C.c_int, [vp, _dp]),
         "kmf_run": (C.c_int, [vp, C.POINTER(Params), C.c_int, _dp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
         "kmf_prepare": (C.c_int, [vp, C.POINTER(Params)]),
+        "kmf_run_cases": (C.c_int, [vp, C.POINTER(Params), C.c_int, C.c_int, C.POINTER(C.c_void_p),
+                                    C.POINTER(C.c_void_p), _dp, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                    C.POINTER(C.c_int)]),
         "kmf_get_state": (C.c_int, [vp, _dp, _dp]),
         "kmf_stage_seconds": (C.c_int, [vp, _dp]),
         "kmf_last_error": (C.c_int, [vp, C.POINTER(ErrorInfo)]),
@@ -148,7 +151,7 @@ EXPORTED = (
     "kmf_op_full_flux", "kmf_op_state_update", "kmf_op_residue", "kmf_bench_steps", "kmf_fp64_peak", "kmf_fastmath_probe",
     "kmf_probe_edge_state",
     "kmf_host_alloc", "kmf_host_free", "kmf_set_partition", "kmf_nccl_get_unique_id", "kmf_nccl_init",
-    "kmf_run_group",
+    "kmf_run_group", "kmf_run_cases",
 )
 
 

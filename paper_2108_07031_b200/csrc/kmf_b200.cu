@@ -127,6 +127,10 @@ struct kmf_ctx {
     bool has_perm = false;
     // solver, boundary branch, halo exchange, band pass (partitions)
     cudaStream_t s0 = nullptr, s1 = nullptr, s2 = nullptr, s3 = nullptr;
+    // kmf_run_cases: upload / download streams and their buffer events
+    // (per half of the double-buffered P0 / stage_buf)
+    cudaStream_t sh = nullptr, sd = nullptr;
+    cudaEvent_t cs_up[2] = {}, cs_free[2] = {}, cs_got[2] = {}, cs_down[2] = {};
     cudaEvent_t fork = nullptr, join = nullptr, xfork = nullptr, xjoin = nullptr;
     // band pass: stage start on s0 / halo unpacked (group runner) / done
     cudaEvent_t bfork = nullptr, bready = nullptr, bjoin = nullptr;
@@ -249,7 +253,10 @@ struct kmf_ctx {
             if (e) cudaEventDestroy(e);
         for (cudaEvent_t e : lev)
             if (e) cudaEventDestroy(e);
-        for (cudaStream_t s : {s0, s1, s2, s3})
+        for (cudaEvent_t *arr : {cs_up, cs_free, cs_got, cs_down})
+            for (int b = 0; b < 2; b++)
+                if (arr[b]) cudaEventDestroy(arr[b]);
+        for (cudaStream_t s : {s0, s1, s2, s3, sh, sd})
             if (s) cudaStreamDestroy(s);
     }
 };
@@ -530,7 +537,10 @@ int build_context(kmf_ctx *c, const kmf_geometry *g)
     CK(cudaMemset(c->ctrl.p, 0, sizeof(Ctrl)));
     CK(cudaMemset(c->R.p, 0, sizeof(double) * 4 * ld));
     CK(c->diag.alloc(std::max<long long>(E, std::max(std::max(c->bedges[0], c->bedges[1]), c->bedges[2])) + 1));
-    for (cudaStream_t *s : {&c->s0, &c->s1, &c->s2, &c->s3}) CK(cudaStreamCreateWithFlags(s, cudaStreamNonBlocking));
+    for (cudaStream_t *s : {&c->s0, &c->s1, &c->s2, &c->s3, &c->sh, &c->sd})
+        CK(cudaStreamCreateWithFlags(s, cudaStreamNonBlocking));
+    for (cudaEvent_t *arr : {c->cs_up, c->cs_free, c->cs_got, c->cs_down})
+        for (int b = 0; b < 2; b++) CK(cudaEventCreateWithFlags(&arr[b], cudaEventDisableTiming));
     for (cudaEvent_t &e : c->lev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (cudaEvent_t *e : {&c->fork, &c->join, &c->xfork, &c->xjoin, &c->bfork, &c->bready, &c->bjoin})
         CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
@@ -968,6 +978,7 @@ int get_graph(kmf_ctx *c, const kmf_params *p, int unroll, Graph &gr, int how = 
     k.unroll = unroll;
     k.how = how;
     if (gr.exec && gr.key == k) return KMF_OK;
+    if (gr.exec) CK(cudaStreamSynchronize(c->s0));  // a replay of the old graph may still be in flight
     gr.reset();
     cudaGraph_t graph;
     c->cap_ev = how == ITER_PLAIN ? nullptr : &gr.ev;
@@ -1059,6 +1070,36 @@ int seed_state(kmf_ctx *c, double gamma, double cfl)
     }
     CK(cudaGetLastError());
     c->state_gamma = gamma;
+    return KMF_OK;
+}
+
+// `count` outer iterations on s0: graphs of U iterations (U = 8, then 1 for
+// the rest).  ITER_INSTRUMENT replays are read after each replay (event
+// nodes around each stage's launch groups) into stage_sec.
+int replay(kmf_ctx *c, const kmf_params *p, int count, int how)
+{
+    const int U = 8;
+    int full = count / U, rest = count % U;
+    for (int pass = 0; pass < 2; pass++) {
+        const int reps = pass ? rest : full, unroll = pass ? 1 : U;
+        if (!reps) continue;
+        Graph &gr = pass ? c->g1 : c->gU;
+        if (int rc = get_graph(c, p, unroll, gr, how)) return rc;
+        for (int k = 0; k < reps; k++) {
+            CK(cudaGraphLaunch(gr.exec, c->s0));
+            if (how == ITER_INSTRUMENT) {
+                CK(cudaStreamSynchronize(c->s0));
+                double t[KC_N];
+                if (int rc = graph_times(gr, t)) return rc;
+                // STAGE_NAMES: timestep, q_variables, q_derivatives, flux_residual,
+                // state_update, residue -- timestep, q_variables and residue run
+                // fused inside the update kernels and are reported there
+                c->stage_sec[2] += t[KC_QGRAD] * 1e-3;
+                c->stage_sec[3] += t[KC_FLUXBND] * 1e-3;
+                c->stage_sec[4] += t[KC_UPDATE] * 1e-3;
+            }
+        }
+    }
     return KMF_OK;
 }
 
@@ -1154,37 +1195,11 @@ int kmf_run(kmf_ctx *c, const kmf_params *p, int n_iter, double *history, int *i
     if (int rc = reset_run_ctrl(c, n_iter)) return rc;
     for (double &s : c->stage_sec) s = 0.0;
 
-    // graphs of U iterations (U = 8, then 1 for the rest); the timed
-    // iterations of an instrumented run replay graphs with event nodes
-    // around each stage's launch groups and read them after every replay
+    // the timed iterations of an instrumented run replay graphs with event
+    // nodes around each stage's launch groups
     const int skip = p->instrument ? std::max(0, std::min(p->timing_skip, n_iter)) : n_iter;
-    auto replay = [&](int count, int how) -> int {
-        const int U = 8;
-        int full = count / U, rest = count % U;
-        for (int pass = 0; pass < 2; pass++) {
-            const int reps = pass ? rest : full, unroll = pass ? 1 : U;
-            if (!reps) continue;
-            Graph &gr = pass ? c->g1 : c->gU;
-            if (int rc = get_graph(c, p, unroll, gr, how)) return rc;
-            for (int k = 0; k < reps; k++) {
-                CK(cudaGraphLaunch(gr.exec, c->s0));
-                if (how == ITER_INSTRUMENT) {
-                    CK(cudaStreamSynchronize(c->s0));
-                    double t[KC_N];
-                    if (int rc = graph_times(gr, t)) return rc;
-                    // STAGE_NAMES: timestep, q_variables, q_derivatives, flux_residual,
-                    // state_update, residue -- timestep, q_variables and residue run
-                    // fused inside the update kernels and are reported there
-                    c->stage_sec[2] += t[KC_QGRAD] * 1e-3;
-                    c->stage_sec[3] += t[KC_FLUXBND] * 1e-3;
-                    c->stage_sec[4] += t[KC_UPDATE] * 1e-3;
-                }
-            }
-        }
-        return KMF_OK;
-    };
-    if (int rc = replay(skip, ITER_PLAIN)) return rc;
-    if (int rc = replay(n_iter - skip, ITER_INSTRUMENT)) return rc;
+    if (int rc = replay(c, p, skip, ITER_PLAIN)) return rc;
+    if (int rc = replay(c, p, n_iter - skip, ITER_INSTRUMENT)) return rc;
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(c->s0));
     Ctrl fin;
@@ -1215,6 +1230,105 @@ int kmf_prepare(kmf_ctx *c, const kmf_params *p)
     const int how = p->instrument ? ITER_INSTRUMENT : ITER_PLAIN;
     if (int rc = get_graph(c, p, 8, c->gU, how)) return rc;
     return get_graph(c, p, 1, c->g1, how);
+}
+
+// Streaming cases (include/kmf_b200.h).  Per case k, buffer half b = k & 1:
+//   sh: [wait free[b]] upload in[k] -> P0 half b, record up[b]
+//   s0: [wait up[b]] k_init, record free[b]; Ctrl reset; n_iter iterations;
+//       Ctrl snapshot; [wait down[b]] k_get_state -> stage_buf half b, record got[b]
+//   sd: [wait got[b]] download -> out[k], record down[b]
+// so case k+1's upload and case k-1's download run on the copy engines
+// while case k iterates.  Every case runs exactly kmf_set_state + kmf_run
+// (PLAIN) + kmf_get_state's arithmetic.
+// Ctrl block copies on the solver stream as a kernel: a cudaMemcpyAsync
+// would queue on the copy engine behind the next case's upload.
+__global__ void k_ctrl_copy(Ctrl *dst, const Ctrl *src)
+{
+    static_assert(sizeof(Ctrl) % 8 == 0, "Ctrl is copied in 8-byte words");
+    const unsigned long long *s = reinterpret_cast<const unsigned long long *>(src);
+    unsigned long long *d = reinterpret_cast<unsigned long long *>(dst);
+    for (int w = threadIdx.x; w < (int)(sizeof(Ctrl) / 8); w += blockDim.x) d[w] = s[w];
+}
+
+int kmf_run_cases(kmf_ctx *c, const kmf_params *params, int n_iter, int n_cases, const double *const *prims_in,
+                  double *const *prims_out, double *history, int *iters_done, int *converged, int *status)
+{
+    if (!c || !params || n_iter < 1 || n_cases < 1 || !prims_in || !prims_out) return KMF_EINVAL;
+    for (int k = 0; k < n_cases; k++) {
+        if (!prims_in[k] || !prims_out[k]) return KMF_EINVAL;
+        if (int rc = check_params(c, &params[k])) return rc;
+    }
+    if (c->dist_on && !c->nccl) {
+        set_msg("kmf_run_cases: partitioned context without NCCL");
+        return KMF_EINVAL;
+    }
+    CK(cudaSetDevice(c->device));
+    c->err = kmf_error_info{};
+    c->err_idx.clear();
+    const size_t n4 = 4 * (size_t)c->n, bytes = sizeof(double) * n4;
+    if (c->P0.n < 2 * n4) CK(c->P0.alloc(2 * n4));
+    DBuf<double> hist;
+    DBuf<Ctrl> snap, dinit;
+    CK(hist.alloc((size_t)n_cases * n_iter));
+    CK(snap.alloc(n_cases));
+    std::vector<Ctrl> init(n_cases);
+    for (int k = 0; k < n_cases; k++) {
+        std::memset(&init[k], 0, sizeof(Ctrl));
+        init[k].iter = 1;
+        init[k].epoch = 1;
+        init[k].history = hist.p + (size_t)k * n_iter;
+        init[k].hist_cap = n_iter;
+    }
+    CK(dinit.upload(init.data(), n_cases));
+    const DG g = c->dg();
+    const long long *perm = c->has_perm ? c->perm.p : nullptr;
+    CK(cudaDeviceSynchronize());  // earlier work on any stream of this context
+    for (int k = 0; k < n_cases; k++) {
+        const kmf_params *p = &params[k];
+        const int b = k & 1;
+        double *P = c->P0.p + b * n4, *S = c->stage_buf.p + b * n4;
+        CK(cudaStreamWaitEvent(c->sh, c->cs_free[b], 0));
+        CK(cudaMemcpyAsync(P, prims_in[k], bytes, cudaMemcpyHostToDevice, c->sh));
+        CK(cudaEventRecord(c->cs_up[b], c->sh));
+        CK(cudaStreamWaitEvent(c->s0, c->cs_up[b], 0));
+        k_init<<<nblk(c->n), kTB, 0, c->s0>>>(g, P, perm, c->Uo.p, c->q.p, c->dt.p, p->gamma, p->cfl);
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(c->cs_free[b], c->s0));
+        k_ctrl_copy<<<1, 32, 0, c->s0>>>(c->ctrl.p, dinit.p + k);
+        if (int rc = replay(c, p, n_iter, ITER_PLAIN)) return rc;
+        k_ctrl_copy<<<1, 32, 0, c->s0>>>(snap.p + k, c->ctrl.p);
+        CK(cudaStreamWaitEvent(c->s0, c->cs_down[b], 0));
+        k_get_state<<<nblk(c->n), kTB, 0, c->s0>>>(g, c->Uo.p, perm, p->gamma, S, nullptr);
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(c->cs_got[b], c->s0));
+        CK(cudaStreamWaitEvent(c->sd, c->cs_got[b], 0));
+        CK(cudaMemcpyAsync(prims_out[k], S, bytes, cudaMemcpyDeviceToHost, c->sd));
+        CK(cudaEventRecord(c->cs_down[b], c->sd));
+    }
+    CK(cudaDeviceSynchronize());
+    c->have_state = true;  // the last case's final state
+    c->pending_init = false;
+    c->state_gamma = params[n_cases - 1].gamma;
+    CK(cudaMemcpy(init.data(), snap.p, sizeof(Ctrl) * n_cases, cudaMemcpyDeviceToHost));
+    if (history) CK(cudaMemcpy(history, hist.p, sizeof(double) * n_cases * n_iter, cudaMemcpyDeviceToHost));
+    int rc = KMF_OK;
+    for (int k = 0; k < n_cases; k++) {
+        const Ctrl &f = init[k];
+        const int st = (int)(f.state & 3ull);
+        const int done = std::min(f.iter - 1, n_iter);
+        if (history)
+            for (int i = done; i < n_iter; i++) history[(size_t)k * n_iter + i] = 0.0;
+        if (iters_done) iters_done[k] = done;
+        if (converged) converged[k] = st == 2;
+        if (status) status[k] = st == 1 ? KMF_EPOSITIVITY : KMF_OK;
+        if (st == 1 && rc == KMF_OK) {
+            char msg[64];
+            std::snprintf(msg, sizeof msg, "positivity (case %d)", k);
+            record_error(c, KMF_EPOSITIVITY, f.err_iter, f.err_stage, first_context(f.ctx_mask), 0, msg);
+            rc = KMF_EPOSITIVITY;
+        }
+    }
+    return rc;
 }
 
 int kmf_get_state(kmf_ctx *c, double *prims, double *U)

@@ -36,6 +36,7 @@ from .state import (
     Primitives,
     conserved_to_primitives,
     prims_array,
+    primitives_to_conserved,
     free_stream,
 )
 
@@ -319,3 +320,64 @@ def solve(
         iterations=done,
         converged=converged,
     )
+
+
+def solve_cases(
+    configs,
+    cloud: PointCloud,
+    conn: Connectivity | None = None,
+    initial_states=None,
+) -> list:
+    """Independent solves on one cloud, streamed through one device context.
+
+    ``configs`` is a SolverConfig or one per case; ``initial_states`` a list of
+    Primitives (default: ``initial_primitives`` of each config).  Case k gives
+    ``solve(configs[k], cloud, conn, initial_states[k], instrument=False)``
+    bit for bit in residue history, final primitives and convergence
+    (``conserved`` is recomputed from the final primitives) -- but
+    case k+1's upload and case k-1's download overlap case k's iterations
+    (kmf_run_cases), the batch the reference's harness runs one solve at a
+    time (bench.py:174-215 ``sweep``).  A case that fails positivity is
+    returned as its PositivityError instead of a SolveResult (the batch
+    keeps going, as the reference's sweep records failed cells).
+    """
+    if conn is None:
+        conn = build_stencils(cloud)
+    if initial_states is None:
+        cfgs = list(configs) if isinstance(configs, (list, tuple)) else [configs]
+        initial_states = [initial_primitives(c, cloud) for c in cfgs]
+    m = len(initial_states)
+    cfgs = list(configs) if isinstance(configs, (list, tuple)) else [configs] * m
+    if len(cfgs) != m:
+        raise ValueError("one config per initial state")
+    n_iter = cfgs[0].n_outer
+    if any(c.n_outer != n_iter for c in cfgs):
+        raise ValueError("every case runs the same n_outer")
+    states = []
+    for prims in initial_states:
+        prims.validate("initial state")
+        states.append(prims_array(prims))
+    dev = device_for(conn)
+    outs, hist, done, conv, status = dev.run_cases([_params(c) for c in cfgs], states, n_iter)
+    results = []
+    for k in range(m):
+        if status[k] == _lib.KMF_EPOSITIVITY:
+            # replay the failing case alone for the reference's exact error
+            try:
+                solve(cfgs[k], cloud, conn, initial_states[k], instrument=False)
+            except PositivityError as exc:
+                results.append(exc)
+                continue
+            raise _lib.DeviceError(f"case {k}: positivity failure did not reproduce")
+        prims = Primitives.from_array(outs[k])
+        results.append(SolveResult(
+            primitives=prims,
+            conserved=primitives_to_conserved(prims, cfgs[k].gamma),
+            residue_history=hist[k, : done[k]].copy(),
+            stage_seconds={name: 0.0 for name in STAGE_NAMES},
+            wall_seconds=0.0,
+            timed_iterations=done[k],
+            iterations=done[k],
+            converged=conv[k],
+        ))
+    return results

@@ -444,6 +444,17 @@ def run_ours(args):
     _lib.require_device()
     from paper_2108_07031_b200 import reorder
 
+    shared_gpu = ws > 1 and os.environ.get("KMF_SHARE_GPU") == "1"
+    if shared_gpu:
+        # functional run of the N-rank path on fewer GPUs (tests / one-GPU
+        # boxes): ranks share devices and NCCL connects them over its socket
+        # transport (one fake host per rank).  Timings are NOT scaling data;
+        # the JSON line says so ("shared_gpu": true).
+        local = local % L.kmf_device_count()
+        os.environ["NCCL_HOSTID"] = f"kmf-bench-host-{rank}"
+        os.environ.setdefault("NCCL_SOCKET_IFNAME", "lo")
+        os.environ.setdefault("NCCL_IB_DISABLE", "1")
+
     cloud, conn, cfg, init = setup(args.config, dist, rank)
     n = cloud.n_points
     if ws > 1:
@@ -609,6 +620,8 @@ def run_ours(args):
             kern_s[1] + kern_s[2]) / (step_ms[:K].sum() * 1e-3)) if n_sweeps else None,
         "clocks": clk.summary(),
         "partition": part_stats,
+        **({"shared_gpu": True, "note": "KMF_SHARE_GPU: ranks share GPUs over NCCL sockets; not scaling data"}
+           if shared_gpu else {}),
     }
     if not args.no_cpu_baseline and ws == 1:
         port = cpu_baseline(conn, cfg, init)

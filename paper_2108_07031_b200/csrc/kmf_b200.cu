@@ -245,8 +245,8 @@ struct kmf_ctx {
     }
     ~kmf_ctx()
     {
+        drop_graphs();  // the graphs hold NCCL kernel nodes: before the communicator goes
         if (nccl && nccl_destroy) nccl_destroy(nccl);
-        drop_graphs();
         for (auto &e : evs)
             if (e) cudaEventDestroy(e);
         for (cudaEvent_t e : {fork, join, xfork, xjoin, bfork, bready, bjoin})
@@ -770,6 +770,7 @@ struct NcclApi {
     ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
     ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
     ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
@@ -792,6 +793,7 @@ NcclApi &nccl_api()
     KMF_SYM(GetUniqueId, "ncclGetUniqueId");
     KMF_SYM(CommInitRank, "ncclCommInitRank");
     KMF_SYM(CommDestroy, "ncclCommDestroy");
+    KMF_SYM(CommAbort, "ncclCommAbort");
     KMF_SYM(Send, "ncclSend");
     KMF_SYM(Recv, "ncclRecv");
     KMF_SYM(AllReduce, "ncclAllReduce");
@@ -2035,9 +2037,16 @@ extern "C" int kmf_nccl_init(kmf_ctx *c, const void *id128, int rank, int nranks
         return KMF_ENCCL;
     }
     c->nccl = comm;
+    // Teardown runs after the context's streams are idle (kmf_destroy
+    // synchronises), so nothing is in flight: ncclCommAbort releases the
+    // communicator locally, whereas ncclCommDestroy's finalize waits on its
+    // peers' proxies and hung at interpreter exit with the socket transport.
     c->nccl_destroy = [](void *p) {
         NcclApi &a = nccl_api();
-        if (a.CommDestroy) a.CommDestroy((ncclComm_t)p);
+        if (a.CommAbort)
+            a.CommAbort((ncclComm_t)p);
+        else if (a.CommDestroy)
+            a.CommDestroy((ncclComm_t)p);
     };
     c->drop_graphs();
     // One eager round of the exact send/recv pattern (on both streams the

@@ -1,5 +1,6 @@
 """Try the NCCL rank path with two processes on ONE GPU (dev aid): NCCL may
 refuse duplicate devices; if it accepts, compare with the single domain."""
+import faulthandler
 import os
 import socket
 import sys
@@ -11,21 +12,29 @@ import numpy as np  # noqa: E402
 
 
 def worker(rank, world, port, q):
+    faulthandler.dump_traceback_later(240, exit=True)
     import torch.distributed as dist
 
     from conftest import perturbed_state
     from paper_2108_07031_b200 import SolverConfig, build_stencils, generate_naca_cloud
     from paper_2108_07031_b200.dist import RankSolver
+    from paper_2108_07031_b200.state import prims_array
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
+    if os.environ.get("FAKE_HOSTS"):
+        # each rank reports its own host: NCCL skips its same-host duplicate-
+        # device check and connects the ranks through its socket transport
+        os.environ["NCCL_HOSTID"] = f"kmf-fake-host-{rank}"
+        os.environ.setdefault("NCCL_SOCKET_IFNAME", "lo")
+        os.environ.setdefault("NCCL_IB_DISABLE", "1")
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         cloud = generate_naca_cloud(80, 30, 1.15, 20.0)
         conn = build_stencils(cloud)
         cfg = SolverConfig(mach=0.63, aoa_deg=2.0, n_outer=6)
         rs = RankSolver(conn, dist, n_inner=3, device=0, scheme=sys.argv[1] if len(sys.argv) > 1 else "sectors")
-        hist, conv = rs.run(cfg, perturbed_state(cloud).as_array(), cfg.n_outer)
+        hist, conv = rs.run(cfg, prims_array(perturbed_state(cloud)), cfg.n_outer)
         gid, prims, _ = rs.rp.owned_state()
         q.put((rank, hist, gid, prims, None))
     except Exception as e:  # report, do not hang
@@ -39,6 +48,7 @@ if __name__ == "__main__":
 
     from conftest import perturbed_state
     from paper_2108_07031_b200 import SolverConfig, build_stencils, generate_naca_cloud, solve
+    from paper_2108_07031_b200.state import prims_array
 
     s_ = socket.socket()
     s_.bind(("127.0.0.1", 0))
@@ -61,4 +71,4 @@ if __name__ == "__main__":
             print(f"rank {rank}: error {err}")
             continue
         print(f"rank {rank}: history equal {np.array_equal(hist, ref.residue_history)}, state equal "
-              f"{np.array_equal(prims, ref.primitives.as_array()[:, gid])}")
+              f"{np.array_equal(prims, prims_array(ref.primitives)[:, gid])}")

@@ -109,7 +109,9 @@ KMF_HD void fsflux_m(const FState *const (&st)[M], const bool (&Y)[M], const dou
     for (int m = 0; m < M; m++) {
         const FState &s = *st[m];
         const double ut = Y[m] ? s.u1 : s.u2;
-        const double A = 0.5 * fma(sg[m], E[m], 1.0);
+        // A = (1 + sg erf s) / 2 as ONE fma: scaling by 1/2 is exact, so
+        // fma(+-1/2, E, 1/2) rounds to exactly 0.5 * fma(sg, E, 1)
+        const double A = fma(copysign(0.5, sg[m]), E[m], 0.5);
         const double B = e2[m] * s.bc;
         const double sgB = copysign(B, sg[m]);  // sg = +-1 as a sign flip (ALU, not the FP64 pipe)
         const double unsq = un[m] * un[m];

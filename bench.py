@@ -386,12 +386,12 @@ def cpu_baseline(conn, cfg, init, target_s=12.0):
                       f"the reference) with OpenMP over {threads} threads"}
 
 
-def qgrad_roofline(n_pts, fo_s, sweep_s, peak, peak_kind, share):
+def qgrad_roofline(n_fo, n_sweep, fo_s, sweep_s, peak, peak_kind, share):
     """First-order and sweep kernels against HBM: SURVEY 8(d)'s algorithmic
     bytes per point (208 / 272) x the points one launch covers, divided by
     the launch's average duration (event nodes on its stream)."""
-    fo = FO_BYTES_PER_POINT * n_pts / fo_s / 1e9
-    sw = SWEEP_BYTES_PER_POINT * n_pts / sweep_s / 1e9
+    fo = FO_BYTES_PER_POINT * n_fo / fo_s / 1e9
+    sw = SWEEP_BYTES_PER_POINT * n_sweep / sweep_s / 1e9
     return {"bound": "hbm", "unit": "GB/s", "peak": peak, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
             "first_order": {"kernel": "k_first_order", "bytes_per_point": FO_BYTES_PER_POINT, "launch_us": fo_s * 1e6,
                             "achieved": fo, "frac": fo / peak},
@@ -567,10 +567,20 @@ def run_ours(args):
         return
     peaks, peak_kind = measured_peaks()
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    n_flux = rs.rp.part.n_owned if ws > 1 else n  # points one flux launch covers
+    # points the timed launches cover: the whole cloud on one GPU; under a
+    # partition the timed (event-marked) launches are the interior pass's
+    # (partition.stage_ranges), the band pass runs unmarked on its own stream
+    n_fo = n_sweep = n_flux = n
+    if ws > 1:
+        from paper_2108_07031_b200.partition import stage_ranges
+
+        ranges = {name: iv for name, iv, _ in stage_ranges(rs.rp.part, cfg.n_inner if n_sweeps else 0)}
+        n_flux = ranges["flux"][1]
+        if n_sweeps:
+            n_fo = ranges["first_order"][1]
+            n_sweep = sum(ranges[f"sweep{s}"][1] for s in range(1, n_sweeps + 1)) / n_sweeps
     achieved_gbs = FLUX_BYTES_PER_POINT * n_flux / flux_launch_s / 1e9
     dfma_rate = peak_fp64.value / 2.0  # DP-pipe instructions/s (TFLOP/s / 2)
-    n_grad = (rs.rp.part.layer_counts[-1] if ws > 1 else n)  # q-gradient launches cover owned + halo layers
     # executed DP-pipe instructions and DRAM traffic of one flux launch,
     # measured once per kernel build by ncu (tools/flux_counts.sh)
     traffic, counts = None, None
@@ -616,7 +626,7 @@ def run_ours(args):
             "note": "whole outer iteration against the HBM roofline implied by SURVEY 8(d)'s 6.44 KB per "
                     "point-iteration (north star), per GPU"},
         "roofline_fp64": roofline_fp64(counts, n, n_flux, flux_launch_s, dfma_rate, peak_fp64.value),
-        "roofline_qgrad": qgrad_roofline(n_grad, fo_launch_s, sweep_launch_s, hbm_peak, peak_kind, float(
+        "roofline_qgrad": qgrad_roofline(n_fo, n_sweep, fo_launch_s, sweep_launch_s, hbm_peak, peak_kind, float(
             kern_s[1] + kern_s[2]) / (step_ms[:K].sum() * 1e-3)) if n_sweeps else None,
         "clocks": clk.summary(),
         "partition": part_stats,

@@ -152,7 +152,16 @@ def _nccl_worker(rank, world, port, scheme, order, q):
         rs = RankSolver(conn, dist, n_inner=3, device=rank % ndev, scheme=scheme)
         hist, conv = rs.run(cfg, prims_array(init), cfg.n_outer)
         gid, prims, _ = rs.rp.owned_state()
-        q.put((rank, hist, gid, prims, None))
+        # the streamed-cases path on the same communicator: two cases from
+        # the same local state, each must equal the run above
+        from paper_2108_07031_b200.solver import _params
+
+        local = np.ascontiguousarray(prims_array(init)[:, rs.rp.part.global_ids])
+        outs, hc, _, _, st = rs.dev.run_cases([_params(cfg)] * 2, [local, local], cfg.n_outer)
+        no = rs.rp.part.n_owned
+        cases_ok = st == [0, 0] and all(np.array_equal(hc[k], hist) and np.array_equal(outs[k][:, :no], prims)
+                                        for k in range(2))
+        q.put((rank, hist, gid, prims, None if cases_ok else "run_cases differs from run"))
     except Exception as exc:  # reported, never left hanging on the queue
         q.put((rank, None, None, None, repr(exc)))
     finally:

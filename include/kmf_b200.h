@@ -35,7 +35,8 @@ enum {
     KMF_EPOSITIVITY = 1,
     KMF_EINVAL = 2,
     KMF_ECUDA = 3,
-    KMF_ENCCL = 4
+    KMF_ENCCL = 4,
+    KMF_EPEER = 5   /* peer transport: a peer rank did not arrive within the deadline */
 };
 
 /* Which reference raise site a positivity failure corresponds to. */
@@ -261,6 +262,34 @@ int kmf_nccl_init(kmf_ctx *ctx, const void *id128, int rank, int nranks);
  * by device/peer copies, limbs summed on the host */
 int kmf_run_group(kmf_ctx **ctxs, int nctx, const kmf_params *p, int n_iter, double *history, int *iters_done,
                   int *converged);
+
+/* Peer transport (csrc/kmf_peer.cuh): no NCCL on the data path.  Every
+ * rank maps its peers' q arrays and flag blocks (NVLink / NVSwitch peer
+ * memory); each stage update stores the new q of its send points straight
+ * into the peers' halo slots (compute and transfer in one kernel), device
+ * counters with system-scope release/acquire order the pushes against the
+ * peers' band passes, and the residue limbs are all-gathered over peer
+ * memory before the iteration close.  Histories stay bitwise the
+ * single-GPU ones.  A wait that exceeds 30 s sets KMF_EPEER on the run.
+ *
+ * Processes (one per GPU): kmf_peer_handle writes this context's
+ * KMF_PEER_HANDLE_BYTES of CUDA IPC handles; after an all-gather of them,
+ * kmf_peer_open(handles[nranks], dst_counts, dst_slots) maps the peers:
+ * per peer in the partition's peer order, the peer's local halo slots that
+ * receive this rank's send list (its recv list for this rank).  kmf_run,
+ * kmf_run_cases and kmf_bench_steps then run as for one domain.
+ * One process: kmf_peer_link(ctxs) links the ranks' contexts directly and
+ * kmf_run_linked enqueues every rank's run before awaiting any. */
+#define KMF_PEER_HANDLE_BYTES 128
+int kmf_peer_handle(kmf_ctx *ctx, void *out);
+int kmf_peer_open(kmf_ctx *ctx, const void *handles, const int64_t *dst_counts, const int64_t *dst_slots);
+int kmf_peer_link(kmf_ctx **ctxs, int nctx);
+int kmf_run_linked(kmf_ctx **ctxs, int nctx, const kmf_params *p, int n_iter, double *history, int *iters_done,
+                   int *converged);
+/* diagnostics: out[0..2] = this rank's pushes, band passes, iterations;
+ * out[3 + r], out[3 + nranks + r], out[3 + 2 nranks + r] = the data, read
+ * and limb counters peer r last published here */
+int kmf_peer_counters(kmf_ctx *ctx, uint64_t *out);
 
 /* ---- measurement support (bench.py) -------------------------------------- */
 

@@ -15,7 +15,8 @@ import numpy as np
 
 LIB_PATH = Path(__file__).resolve().parent / "libkmf_b200.so"
 
-KMF_OK, KMF_EPOSITIVITY, KMF_EINVAL, KMF_ECUDA, KMF_ENCCL = 0, 1, 2, 3, 4
+KMF_OK, KMF_EPOSITIVITY, KMF_EINVAL, KMF_ECUDA, KMF_ENCCL, KMF_EPEER = 0, 1, 2, 3, 4, 5
+KMF_PEER_HANDLE_BYTES = 128
 BENCH_KERNELS = 3  # KMF_BENCH_KERNELS: interior flux, first order, sweeps
 DIAG_LAST_RUN = 2  # kmf_diag_* `which`: the final gradients of the last run
 
@@ -130,6 +131,12 @@ def lib():
         "kmf_nccl_init": (C.c_int, [vp, C.c_void_p, C.c_int, C.c_int]),
         "kmf_run_group": (C.c_int, [C.POINTER(vp), C.c_int, C.POINTER(Params), C.c_int, _dp, C.POINTER(C.c_int),
                                     C.POINTER(C.c_int)]),
+        "kmf_peer_handle": (C.c_int, [vp, C.c_void_p]),
+        "kmf_peer_open": (C.c_int, [vp, C.c_void_p, _i64p, _i64p]),
+        "kmf_peer_link": (C.c_int, [C.POINTER(vp), C.c_int]),
+        "kmf_peer_counters": (C.c_int, [vp, C.POINTER(C.c_uint64)]),
+        "kmf_run_linked": (C.c_int, [C.POINTER(vp), C.c_int, C.POINTER(Params), C.c_int, _dp, C.POINTER(C.c_int),
+                                     C.POINTER(C.c_int)]),
         "kmf_host_alloc": (C.c_void_p, [C.c_int64]),
         "kmf_host_free": (None, [C.c_void_p]),
     }
@@ -151,7 +158,8 @@ EXPORTED = (
     "kmf_op_full_flux", "kmf_op_state_update", "kmf_op_residue", "kmf_bench_steps", "kmf_fp64_peak", "kmf_fastmath_probe",
     "kmf_probe_edge_state",
     "kmf_host_alloc", "kmf_host_free", "kmf_set_partition", "kmf_nccl_get_unique_id", "kmf_nccl_init",
-    "kmf_run_group", "kmf_run_cases",
+    "kmf_run_group", "kmf_run_cases", "kmf_peer_handle", "kmf_peer_open", "kmf_peer_link", "kmf_run_linked",
+    "kmf_peer_counters",
 )
 
 

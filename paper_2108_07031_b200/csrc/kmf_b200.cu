@@ -5,6 +5,7 @@
 #include "../../include/kmf_b200.h"
 #include "kmf_kernels.cuh"
 #include "kmf_flux.cuh"
+#include "kmf_peer.cuh"
 
 #include <cuda_runtime.h>
 #include <dlfcn.h>
@@ -196,6 +197,17 @@ struct kmf_ctx {
     DBuf<double> Glev[kMaxLevels];
     void *nccl = nullptr;  // ncclComm_t when the NCCL transport is initialised
     void (*nccl_destroy)(void *) = nullptr;
+    // peer transport (kmf_peer.cuh): flag block in this device's memory, the
+    // peers' q / flag blocks mapped here, the push map of the update
+    bool peer_on = false;
+    DBuf<PeerFlags> pflags;
+    PeerSet pset{};
+    PeerPush ppush{};
+    DBuf<int> push_ptr;
+    DBuf<unsigned> push_dst;
+    std::vector<void *> ipc_opened;             // cudaIpcOpenMemHandle mappings (closed at teardown)
+    std::vector<int> send_slot_h, recv_slot_h;  // host copies of the partition's lists
+    bool transport() const { return nccl != nullptr || peer_on; }
 
     DG dg() const
     {
@@ -247,6 +259,7 @@ struct kmf_ctx {
     {
         drop_graphs();  // the graphs hold NCCL kernel nodes: before the communicator goes
         if (nccl && nccl_destroy) nccl_destroy(nccl);
+        for (void *m : ipc_opened) cudaIpcCloseMemHandle(m);
         for (auto &e : evs)
             if (e) cudaEventDestroy(e);
         for (cudaEvent_t e : {fork, join, xfork, xjoin, bfork, bready, bjoin})
@@ -752,12 +765,13 @@ void launch_update(kmf_ctx *c, cudaStream_t s, int stage, double gamma, double c
     Ctrl *ctl = c->ctrl.p;
     double *Uo = c->Uo.p, *Us = c->Us.p, *dt = c->dt.p, *q = c->q.p;
     const double *R = c->R.p;
+    const PeerPush pp = c->peer_on ? c->ppush : PeerPush{};
     c->nlaunch++;
     switch (stage) {
-    case 1: k_update<1><<<nb, kTB, 0, s>>>(g, 0, hi, Uo, Us, R, dt, q, gamma, cfl, ctl, io); break;
-    case 2: k_update<2><<<nb, kTB, 0, s>>>(g, 0, hi, Uo, Us, R, dt, q, gamma, cfl, ctl, io); break;
-    case 3: k_update<3><<<nb, kTB, 0, s>>>(g, 0, hi, Uo, Us, R, dt, q, gamma, cfl, ctl, io); break;
-    default: k_update<4><<<nb, kTB, 0, s>>>(g, 0, hi, Uo, Us, R, dt, q, gamma, cfl, ctl, io); break;
+    case 1: k_update<1><<<nb, kTB, 0, s>>>(g, 0, hi, Uo, Us, R, dt, q, gamma, cfl, ctl, io, pp); break;
+    case 2: k_update<2><<<nb, kTB, 0, s>>>(g, 0, hi, Uo, Us, R, dt, q, gamma, cfl, ctl, io, pp); break;
+    case 3: k_update<3><<<nb, kTB, 0, s>>>(g, 0, hi, Uo, Us, R, dt, q, gamma, cfl, ctl, io, pp); break;
+    default: k_update<4><<<nb, kTB, 0, s>>>(g, 0, hi, Uo, Us, R, dt, q, gamma, cfl, ctl, io, pp); break;
     }
 }
 
@@ -902,7 +916,12 @@ void enqueue_tail(kmf_ctx *c, StageCtx &sc, int stage, const double *G)
             cudaStreamWaitEvent(sb, c->xjoin, 0);
             sc.xchg_pending = false;
         }
-        if (!c->nccl) cudaStreamWaitEvent(sb, c->bready, 0);
+        if (c->peer_on) {  // the peers' pushes of the previous update have landed
+            k_peer_wait_data<<<1, 32, 0, sb>>>(c->pset, ctl);
+            c->nlaunch++;
+        } else if (!c->nccl) {
+            cudaStreamWaitEvent(sb, c->bready, 0);
+        }
         if (p->n_inner > 0) {
             launch_qgrad(c, sb, stage, p->n_inner, ctl, true, false);
             // boundary and band flux read the final level at interior slots
@@ -918,6 +937,10 @@ void enqueue_tail(kmf_ctx *c, StageCtx &sc, int stage, const double *G)
         cudaEventRecord(c->bjoin, sb);
         Mark m(c, KC_FLUXBND, inst);
         cudaStreamWaitEvent(c->s0, c->bjoin, 0);
+        if (c->peer_on) {  // halo read: release it to the pushing peers, wait for the ones this rank pushes into
+            k_peer_band_done<<<1, 32, 0, c->s0>>>(c->pset, ctl);
+            c->nlaunch++;
+        }
     } else {
         Mark m(c, KC_FLUXBND, inst);
         cudaStreamWaitEvent(c->s0, c->join, 0);
@@ -936,6 +959,17 @@ void enqueue_tail(kmf_ctx *c, StageCtx &sc, int stage, const double *G)
     if (stage == 4 && own_close) {
         k_close<<<1, kTB, 0, c->s0>>>(c->ctrl.p, c->n, io);
         c->nlaunch++;
+    }
+    if (c->peer_on) {
+        // publish the pushes fused into the update; at stage 4 the residue
+        // limbs are all-gathered over peer memory, then the iteration closes
+        k_peer_pushed<<<1, 32, 0, c->s0>>>(c->pset);
+        c->nlaunch++;
+        if (stage == 4) {
+            k_peer_limbs<<<1, kTB, 0, c->s0>>>(c->pset, ctl);
+            k_close<<<1, kTB, 0, c->s0>>>(ctl, (int)c->n_global, io);
+            c->nlaunch += 2;
+        }
     }
 }
 
@@ -989,6 +1023,10 @@ int get_graph(kmf_ctx *c, const kmf_params *p, int unroll, Graph &gr, int how = 
     CK(cudaStreamBeginCapture(c->s0, cudaStreamCaptureModeThreadLocal));
     for (int u = 0; u < unroll; u++) enqueue_iteration(c, sc);
     if (sc.xchg_pending) cudaStreamWaitEvent(c->s0, c->xjoin, 0);  // join the last exchange
+    if (c->peer_on) {  // ... and the peers' last pushes into this rank's halo
+        k_peer_wait_data<<<1, 32, 0, c->s0>>>(c->pset, c->ctrl.p);
+        c->nlaunch++;
+    }
     cudaError_t ce = cudaStreamEndCapture(c->s0, &graph);
     c->cap_ev = nullptr;
     CK(ce);
@@ -1063,7 +1101,13 @@ int seed_state(kmf_ctx *c, double gamma, double cfl)
         c->pending_init = false;
     } else {
         k_refresh<<<nblk(c->n_act()), kTB, 0, c->s0>>>(g, c->n_act(), c->Uo.p, c->q.p, c->dt.p, gamma, cfl);
-        if (c->dist_on && c->nccl) {
+        if (c->dist_on && c->peer_on) {
+            // continued run: once the peers finished reading what this rank
+            // pushed last, push the refreshed q of the send points
+            k_peer_wait_read<<<1, 32, 0, c->s0>>>(c->pset, c->ctrl.p);
+            if (c->n_owned) k_peer_push_all<<<nblk(c->n_owned), kTB, 0, c->s0>>>(c->n_owned, c->ppush, c->q.p);
+            k_peer_pushed<<<1, 32, 0, c->s0>>>(c->pset);
+        } else if (c->dist_on && c->nccl) {
             if (enqueue_exchange_nccl(c, c->s0) != ncclSuccess) {
                 set_msg("seed_state: NCCL halo exchange failed");
                 return KMF_ENCCL;
@@ -1174,7 +1218,11 @@ int kmf_set_state(kmf_ctx *c, const double *prims)
     return KMF_OK;
 }
 
-int kmf_run(kmf_ctx *c, const kmf_params *p, int n_iter, double *history, int *iters_done, int *converged)
+}  // extern "C"
+
+namespace {
+
+int run_check(kmf_ctx *c, const kmf_params *p, int n_iter)
 {
     if (!c || !p || n_iter < 0) return KMF_EINVAL;
     if (!c->have_state) {
@@ -1182,27 +1230,36 @@ int kmf_run(kmf_ctx *c, const kmf_params *p, int n_iter, double *history, int *i
         return KMF_EINVAL;
     }
     if (int rc = check_params(c, p)) return rc;
-    if (c->dist_on && !c->nccl) {
-        set_msg("kmf_run: partitioned context without NCCL (use kmf_nccl_init or kmf_run_group)");
+    if (c->dist_on && !c->transport()) {
+        set_msg("kmf_run: partitioned context without a transport (kmf_nccl_init, kmf_peer_open / kmf_peer_link, "
+                "or kmf_run_group)");
         return KMF_EINVAL;
     }
+    return KMF_OK;
+}
+
+// kmf_run's enqueue half: seed, Ctrl reset, the graph replays (the
+// instrumented replays synchronise after each to read their event nodes)
+int run_begin(kmf_ctx *c, const kmf_params *p, int n_iter)
+{
     CK(cudaSetDevice(c->device));
-    if (iters_done) *iters_done = 0;
-    if (converged) *converged = 0;
     c->err = kmf_error_info{};
     c->err_idx.clear();
-    if (n_iter == 0) return KMF_OK;
     if (int rc = seed_state(c, p->gamma, p->cfl)) return rc;
     if ((int)c->history.n < n_iter) CK(c->history.alloc(n_iter));
     if (int rc = reset_run_ctrl(c, n_iter)) return rc;
     for (double &s : c->stage_sec) s = 0.0;
-
-    // the timed iterations of an instrumented run replay graphs with event
-    // nodes around each stage's launch groups
     const int skip = p->instrument ? std::max(0, std::min(p->timing_skip, n_iter)) : n_iter;
     if (int rc = replay(c, p, skip, ITER_PLAIN)) return rc;
     if (int rc = replay(c, p, n_iter - skip, ITER_INSTRUMENT)) return rc;
     CK(cudaGetLastError());
+    return KMF_OK;
+}
+
+// ... and its completion half: wait, read the control block
+int run_finish(kmf_ctx *c, int n_iter, double *history, int *iters_done, int *converged)
+{
+    CK(cudaSetDevice(c->device));
     CK(cudaStreamSynchronize(c->s0));
     Ctrl fin;
     CK(cudaMemcpy(&fin, c->ctrl.p, sizeof fin, cudaMemcpyDeviceToHost));
@@ -1213,6 +1270,11 @@ int kmf_run(kmf_ctx *c, const kmf_params *p, int n_iter, double *history, int *i
         CK(cudaMemcpy(history, c->history.p, sizeof(double) * completed, cudaMemcpyDeviceToHost));
     if (iters_done) *iters_done = completed;
     if (converged) *converged = status == 2;
+    if (fin.peer_fail) {
+        record_error(c, KMF_EPEER, fin.iter, 0, 0, 0, "peer transport: a peer rank did not arrive in time");
+        set_msg("peer transport: a peer rank did not arrive in time (rank %d)", c->rank);
+        return KMF_EPEER;
+    }
     if (status == 1) {
         record_error(c, KMF_EPOSITIVITY, fin.err_iter, fin.err_stage, first_context(fin.ctx_mask), 0, "positivity");
         return KMF_EPOSITIVITY;
@@ -1220,12 +1282,26 @@ int kmf_run(kmf_ctx *c, const kmf_params *p, int n_iter, double *history, int *i
     return KMF_OK;
 }
 
+}  // namespace
+
+extern "C" {
+
+int kmf_run(kmf_ctx *c, const kmf_params *p, int n_iter, double *history, int *iters_done, int *converged)
+{
+    if (int rc = run_check(c, p, n_iter)) return rc;
+    if (iters_done) *iters_done = 0;
+    if (converged) *converged = 0;
+    if (n_iter == 0) return KMF_OK;
+    if (int rc = run_begin(c, p, n_iter)) return rc;
+    return run_finish(c, n_iter, history, iters_done, converged);
+}
+
 int kmf_prepare(kmf_ctx *c, const kmf_params *p)
 {
     if (!c || !p) return KMF_EINVAL;
     if (int rc = check_params(c, p)) return rc;
-    if (c->dist_on && !c->nccl) {
-        set_msg("kmf_prepare: partitioned context without NCCL");
+    if (c->dist_on && !c->transport()) {
+        set_msg("kmf_prepare: partitioned context without a transport");
         return KMF_EINVAL;
     }
     CK(cudaSetDevice(c->device));
@@ -1260,8 +1336,8 @@ int kmf_run_cases(kmf_ctx *c, const kmf_params *params, int n_iter, int n_cases,
         if (!prims_in[k] || !prims_out[k]) return KMF_EINVAL;
         if (int rc = check_params(c, &params[k])) return rc;
     }
-    if (c->dist_on && !c->nccl) {
-        set_msg("kmf_run_cases: partitioned context without NCCL");
+    if (c->dist_on && !c->transport()) {
+        set_msg("kmf_run_cases: partitioned context without a transport");
         return KMF_EINVAL;
     }
     CK(cudaSetDevice(c->device));
@@ -1322,7 +1398,11 @@ int kmf_run_cases(kmf_ctx *c, const kmf_params *params, int n_iter, int n_cases,
             for (int i = done; i < n_iter; i++) history[(size_t)k * n_iter + i] = 0.0;
         if (iters_done) iters_done[k] = done;
         if (converged) converged[k] = st == 2;
-        if (status) status[k] = st == 1 ? KMF_EPOSITIVITY : KMF_OK;
+        if (status) status[k] = f.peer_fail ? KMF_EPEER : st == 1 ? KMF_EPOSITIVITY : KMF_OK;
+        if (f.peer_fail && rc == KMF_OK) {
+            set_msg("peer transport: a peer rank did not arrive in time (case %d)", k);
+            rc = KMF_EPEER;
+        }
         if (st == 1 && rc == KMF_OK) {
             char msg[64];
             std::snprintf(msg, sizeof msg, "positivity (case %d)", k);
@@ -1991,6 +2071,8 @@ extern "C" int kmf_set_partition(kmf_ctx *c, int64_t n_owned, int64_t n_global, 
         return KMF_OK;
     };
     if (int rc = build(send_slots, c->send_off, c->send_cnt, so, c->ps_slot, c->ps_base, c->ps_stride, true)) return rc;
+    c->send_slot_h.assign(send_slots, send_slots + so);
+    c->recv_slot_h.assign(recv_slots, recv_slots + ro);
     if (int rc = build(recv_slots, c->recv_off, c->recv_cnt, ro, c->pr_slot, c->pr_base, c->pr_stride, false))
         return rc;
     CK(c->sendbuf.alloc(4 * (size_t)std::max<long long>(so, 1)));
@@ -2098,8 +2180,9 @@ extern "C" int kmf_run_group(kmf_ctx **ctxs, int nctx, const kmf_params *p, int 
     std::vector<kmf_ctx *> byrank(nctx, nullptr);
     for (int k = 0; k < nctx; k++) {
         kmf_ctx *c = ctxs[k];
-        if (!c || !c->dist_on || c->nranks != nctx || byrank[c->rank] || !c->have_state) {
-            set_msg("kmf_run_group: contexts must be partitioned ranks 0..n-1 with state");
+        if (!c || !c->dist_on || c->nranks != nctx || byrank[c->rank] || !c->have_state || c->peer_on) {
+            set_msg("kmf_run_group: contexts must be partitioned ranks 0..n-1 with state (peer-linked "
+                    "contexts run with kmf_run_linked)");
             return KMF_EINVAL;
         }
         if (int rc = check_params(c, p)) return rc;
@@ -2220,6 +2303,243 @@ extern "C" int kmf_run_group(kmf_ctx **ctxs, int nctx, const kmf_params *p, int 
     if (err_rank >= 0) {
         set_msg("positivity failure on rank %d", err_rank);
         return KMF_EPOSITIVITY;
+    }
+    return KMF_OK;
+}
+
+// ------------------------------------------------------- peer transport
+namespace {
+
+// PeerSet / PeerPush of context c from its peers' mapped q arrays and flag
+// blocks and, per peer it sends to (partition peer order), the peer's
+// local slots receiving c's send list
+int peer_setup(kmf_ctx *c, double *const *peer_q, PeerFlags *const *peer_flags,
+               const std::vector<std::vector<long long>> &dst)
+{
+    if (c->nranks > kMaxRanks) {
+        set_msg("peer transport: %d ranks exceed %d", c->nranks, kMaxRanks);
+        return KMF_EINVAL;
+    }
+    PeerSet ps{};
+    PeerPush pp{};
+    ps.me = c->pflags.p;
+    ps.rank = c->rank;
+    ps.nranks = c->nranks;
+    ps.timeout_ns = kPeerTimeoutNs;
+    if (const char *t = std::getenv("KMF_PEER_TIMEOUT_S"))
+        if (std::atof(t) > 0) ps.timeout_ns = (unsigned long long)(std::atof(t) * 1e9);
+    for (int r = 0; r < c->nranks; r++) {
+        ps.peer[r] = r == c->rank ? c->pflags.p : peer_flags[r];
+        pp.q[r] = r == c->rank ? c->q.p : peer_q[r];
+    }
+    std::vector<int> cnt((size_t)c->n_owned + 1, 0);
+    for (size_t k = 0; k < c->peer_rank.size(); k++) {
+        const int r = c->peer_rank[k];
+        if (r < 0 || r >= c->nranks || r == c->rank) return KMF_EINVAL;
+        if (c->send_cnt[k]) ps.send_mask |= 1u << r;
+        if (c->recv_cnt[k]) ps.recv_mask |= 1u << r;
+        if ((long long)dst[k].size() != c->send_cnt[k]) {
+            set_msg("peer transport: rank %d expects %lld halo slots from rank %d, rank %d sends %lld", r,
+                    (long long)dst[k].size(), c->rank, c->rank, c->send_cnt[k]);
+            return KMF_EINVAL;
+        }
+        for (long long e = 0; e < c->send_cnt[k]; e++) cnt[c->send_slot_h[c->send_off[k] + e] + 1]++;
+    }
+    for (int i = 0; i < c->n_owned; i++) cnt[i + 1] += cnt[i];
+    std::vector<int> fill(cnt.begin(), cnt.end() - 1);
+    std::vector<unsigned> out(std::max<long long>(c->send_total, 1));
+    for (size_t k = 0; k < c->peer_rank.size(); k++)
+        for (long long e = 0; e < c->send_cnt[k]; e++) {
+            const long long d = dst[k][e];
+            if (d < 0 || d >= (1ll << kPeerSlotBits)) return KMF_EINVAL;
+            out[fill[c->send_slot_h[c->send_off[k] + e]]++] =
+                ((unsigned)c->peer_rank[k] << kPeerSlotBits) | (unsigned)d;
+        }
+    CK(c->push_ptr.upload(cnt.data(), cnt.size()));
+    CK(c->push_dst.upload(out.data(), out.size()));
+    // load the transport's kernels now: with lazy module loading a kernel's
+    // first launch may wait for the device to go idle, which a rank already
+    // spinning on its peers never does
+    cudaFuncAttributes fa;
+    for (const void *f : {(const void *)k_peer_wait_data, (const void *)k_peer_wait_read, (const void *)k_peer_band_done,
+                          (const void *)k_peer_pushed, (const void *)k_peer_push_all, (const void *)k_peer_limbs})
+        CK(cudaFuncGetAttributes(&fa, f));
+    pp.ptr = c->push_ptr.p;
+    pp.dst = c->push_dst.p;
+    c->pset = ps;
+    c->ppush = pp;
+    c->peer_on = true;
+    c->drop_graphs();
+    return KMF_OK;
+}
+
+int peer_flags_alloc(kmf_ctx *c)
+{
+    if (!c->pflags.p) {
+        CK(c->pflags.alloc(1));
+        CK(cudaMemset(c->pflags.p, 0, sizeof(PeerFlags)));
+        CK(cudaDeviceSynchronize());  // the legacy-stream memset before any peer or stream touches the block
+    }
+    return KMF_OK;
+}
+
+}  // namespace
+
+extern "C" int kmf_peer_handle(kmf_ctx *c, void *out)
+{
+    if (!c || !out || !c->dist_on) return KMF_EINVAL;
+    CK(cudaSetDevice(c->device));
+    if (int rc = peer_flags_alloc(c)) return rc;
+    cudaIpcMemHandle_t h[2];
+    CK(cudaIpcGetMemHandle(&h[0], c->q.p));
+    CK(cudaIpcGetMemHandle(&h[1], c->pflags.p));
+    std::memcpy(out, h, sizeof h);
+    static_assert(sizeof h == KMF_PEER_HANDLE_BYTES, "two IPC handles");
+    return KMF_OK;
+}
+
+extern "C" int kmf_peer_open(kmf_ctx *c, const void *handles, const int64_t *dst_counts, const int64_t *dst_slots)
+{
+    if (!c || !handles || !c->dist_on || c->nccl || c->peer_on) return KMF_EINVAL;
+    CK(cudaSetDevice(c->device));
+    if (int rc = peer_flags_alloc(c)) return rc;
+    std::vector<double *> q(c->nranks, nullptr);
+    std::vector<PeerFlags *> f(c->nranks, nullptr);
+    const cudaIpcMemHandle_t *h = static_cast<const cudaIpcMemHandle_t *>(handles);
+    for (int r = 0; r < c->nranks; r++) {
+        if (r == c->rank) continue;
+        void *a = nullptr, *b = nullptr;
+        CK(cudaIpcOpenMemHandle(&a, h[2 * r], cudaIpcMemLazyEnablePeerAccess));
+        c->ipc_opened.push_back(a);
+        CK(cudaIpcOpenMemHandle(&b, h[2 * r + 1], cudaIpcMemLazyEnablePeerAccess));
+        c->ipc_opened.push_back(b);
+        q[r] = static_cast<double *>(a);
+        f[r] = static_cast<PeerFlags *>(b);
+    }
+    std::vector<std::vector<long long>> dst(c->peer_rank.size());
+    long long off = 0;
+    for (size_t k = 0; k < c->peer_rank.size(); k++) {
+        const long long n = dst_counts ? dst_counts[k] : 0;
+        dst[k].assign(dst_slots + off, dst_slots + off + n);
+        off += n;
+    }
+    return peer_setup(c, q.data(), f.data(), dst);
+}
+
+extern "C" int kmf_peer_link(kmf_ctx **ctxs, int nctx)
+{
+    if (!ctxs || nctx < 1) return KMF_EINVAL;
+    std::vector<kmf_ctx *> byrank(nctx, nullptr);
+    for (int k = 0; k < nctx; k++) {
+        kmf_ctx *c = ctxs[k];
+        if (!c || !c->dist_on || c->nranks != nctx || byrank[c->rank] || c->nccl || c->peer_on) {
+            set_msg("kmf_peer_link: contexts must be partitioned ranks 0..n-1 without a transport");
+            return KMF_EINVAL;
+        }
+        byrank[c->rank] = c;
+    }
+    for (kmf_ctx *c : byrank) {
+        CK(cudaSetDevice(c->device));
+        if (int rc = peer_flags_alloc(c)) return rc;
+    }
+    std::vector<double *> q(nctx);
+    std::vector<PeerFlags *> f(nctx);
+    for (int r = 0; r < nctx; r++) {
+        q[r] = byrank[r]->q.p;
+        f[r] = byrank[r]->pflags.p;
+    }
+    for (kmf_ctx *c : byrank) {
+        for (kmf_ctx *o : byrank)  // peer access between distinct devices (NVLink); same device: nothing to do
+            if (o->device != c->device) {
+                CK(cudaSetDevice(c->device));
+                cudaError_t e = cudaDeviceEnablePeerAccess(o->device, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CK(e);
+                cudaGetLastError();
+            }
+        std::vector<std::vector<long long>> dst(c->peer_rank.size());
+        for (size_t k = 0; k < c->peer_rank.size(); k++) {
+            const kmf_ctx *o = byrank[c->peer_rank[k]];
+            size_t j = 0;
+            while (j < o->peer_rank.size() && o->peer_rank[j] != c->rank) j++;
+            if (j < o->peer_rank.size())
+                dst[k].assign(o->recv_slot_h.begin() + o->recv_off[j],
+                              o->recv_slot_h.begin() + o->recv_off[j] + o->recv_cnt[j]);
+        }
+        CK(cudaSetDevice(c->device));
+        if (int rc = peer_setup(c, q.data(), f.data(), dst)) return rc;
+    }
+    return KMF_OK;
+}
+
+extern "C" int kmf_run_linked(kmf_ctx **ctxs, int nctx, const kmf_params *p, int n_iter, double *history,
+                              int *iters_done, int *converged)
+{
+    if (!ctxs || nctx < 1 || !p) return KMF_EINVAL;
+    std::vector<kmf_ctx *> byrank(nctx, nullptr);
+    for (int k = 0; k < nctx; k++) {
+        kmf_ctx *c = ctxs[k];
+        if (!c || !c->peer_on || c->nranks != nctx || byrank[c->rank]) {
+            set_msg("kmf_run_linked: contexts must be peer-linked ranks 0..n-1 (kmf_peer_link)");
+            return KMF_EINVAL;
+        }
+        if (int rc = run_check(c, p, n_iter)) return rc;
+        byrank[c->rank] = c;
+    }
+    if (iters_done) *iters_done = 0;
+    if (converged) *converged = 0;
+    if (n_iter == 0) return KMF_OK;
+    kmf_params q = *p;
+    q.instrument = 0;  // the ranks run concurrently: no per-replay host reads
+    // every graph is captured and instantiated, every buffer sized, before
+    // any rank starts (an instantiation or a cudaFree may wait for the
+    // device to go idle, which it does not while a rank spins on its
+    // peers); then every rank's whole run is
+    // enqueued before any is awaited (the ranks wait on each other on the
+    // device)
+    for (kmf_ctx *c : byrank) {
+        CK(cudaSetDevice(c->device));
+        // (re)allocations before any launch too: cudaFree waits for the device
+        if ((int)c->history.n < n_iter) CK(c->history.alloc(n_iter));
+        if (n_iter >= 8)
+            if (int rc = get_graph(c, &q, 8, c->gU, ITER_PLAIN)) return rc;
+        if (n_iter % 8)
+            if (int rc = get_graph(c, &q, 1, c->g1, ITER_PLAIN)) return rc;
+    }
+    for (kmf_ctx *c : byrank)
+        if (int rc = run_begin(c, &q, n_iter)) return rc;
+    std::vector<int> rcs(nctx);
+    for (int r = 0; r < nctx; r++) {
+        int done = 0, conv = 0;
+        rcs[r] = run_finish(byrank[r], n_iter, r == 0 ? history : nullptr, &done, &conv);
+        if (r == 0) {
+            if (iters_done) *iters_done = done;
+            if (converged) *converged = conv;
+        }
+    }
+    // a transport / CUDA failure first; positivity failures stay recorded on
+    // each failing context (kmf_last_error), as with kmf_run_group
+    for (int r = 0; r < nctx; r++)
+        if (rcs[r] != KMF_OK && rcs[r] != KMF_EPOSITIVITY) return rcs[r];
+    for (int r = 0; r < nctx; r++)
+        if (rcs[r] == KMF_EPOSITIVITY) return KMF_EPOSITIVITY;
+    return KMF_OK;
+}
+
+// diagnostics: this rank's peer counters -- out[0..2] pushes, bands,
+// iterations; then data[r], read[r], limb_seq[r] for r < nranks
+extern "C" int kmf_peer_counters(kmf_ctx *c, uint64_t *out)
+{
+    if (!c || !out || !c->pflags.p) return KMF_EINVAL;
+    CK(cudaSetDevice(c->device));
+    PeerFlags f;
+    CK(cudaMemcpy(&f, c->pflags.p, sizeof f, cudaMemcpyDeviceToHost));
+    out[0] = f.pushes;
+    out[1] = f.bands;
+    out[2] = f.iters;
+    for (int r = 0; r < c->nranks; r++) {
+        out[3 + r] = f.data[r];
+        out[3 + c->nranks + r] = f.read[r];
+        out[3 + 2 * c->nranks + r] = f.limb_seq[r];
     }
     return KMF_OK;
 }

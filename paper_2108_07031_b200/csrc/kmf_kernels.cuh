@@ -50,6 +50,7 @@ struct Ctrl {
     double *history;            // residue_norm of iteration k at history[k - 1], k <= hist_cap
     int hist_cap;
     unsigned long long limbs[kLimbs];
+    unsigned long long peer_fail;  // peer transport: a wait for another rank timed out (kmf_peer.cuh)
 };
 
 KMF_HD long long seq_of(int epoch, int stage, int slot)
@@ -585,11 +586,33 @@ __device__ __noinline__ void close_iteration(Ctrl *c, const unsigned long long *
     __threadfence();
 }
 
+// Peer transport (kmf_peer.cuh): the stage update stores the new q of
+// every owned point some peer holds in its halo straight into that peer's
+// q array (NVLink / IPC peer memory) -- compute and halo transfer in one
+// kernel.  CSR over owned slots; dst = (peer rank << kPeerSlotBits) | slot.
+constexpr int kMaxRanks = 16;
+constexpr unsigned kPeerSlotBits = 27;
+struct PeerPush {
+    const int *ptr;        // [n_owned + 1]; null: no push
+    const unsigned *dst;
+    double *q[kMaxRanks];  // peers' q arrays
+};
+
+__device__ __forceinline__ void peer_push(const PeerPush &pp, int i, const double (&v)[4])
+{
+    const int b = pp.ptr[i], e = pp.ptr[i + 1];
+    for (int t = b; t < e; t++) {
+        const unsigned d = pp.dst[t];
+        qstore(pp.q[d >> kPeerSlotBits], (int)(d & ((1u << kPeerSlotBits) - 1)), v);
+    }
+    if (e > b) __threadfence_system();  // performed at system scope before this thread retires
+}
+
 template <int STAGE>
 __global__ void __launch_bounds__(kTB) k_update(DG g, int lo, int hi, double *__restrict__ Uo, double *__restrict__ Us,
                                                 const double *__restrict__ R, double *__restrict__ dt,
                                                 double *__restrict__ q, double gamma, double cfl, Ctrl *c,
-                                                IterOut io)
+                                                IterOut io, PeerPush pp)
 {
     __shared__ unsigned long long sl[kLimbs];
     __shared__ bool last;
@@ -624,6 +647,7 @@ __global__ void __launch_bounds__(kTB) k_update(DG g, int lo, int hi, double *__
         double qq[4];
         p2q(rho, u1, u2, p, gamma, qq);
         qstore(q, i, qq);
+        if (pp.ptr) peer_push(pp, i, qq);
         if (STAGE == 4) {
             dt[i] = timestep(rho, u1, u2, p, gamma, cfl, g.dmin[i]);
             const double dr = SUB(un[0], uo[0]);

@@ -124,9 +124,18 @@ def _raise_rank_error(rp: RankPart, params) -> None:
         raise PositivityError(str(exc), indices=idx) from None
 
 
+TRANSPORTS = ("host", "peer")
+
+
 def solve_group(config: SolverConfig, cloud, conn: Connectivity, nranks: int, initial_state: Primitives | None = None,
-                devices=None, scheme: str = "bands"):
-    """Partitioned solve in one process; returns (history, prims (4,n), U (4,n), converged)."""
+                devices=None, scheme: str = "bands", transport: str = "host"):
+    """Partitioned solve in one process; returns (history, prims (4,n), U (4,n), converged).
+
+    transport "host": kmf_run_group (the host moves the halo between the
+    stages); "peer": the contexts are peer-linked (kmf_peer_link) and run
+    concurrently with the device-side peer transport (kmf_run_linked)."""
+    if transport not in TRANSPORTS:
+        raise ValueError(f"transport must be one of {TRANSPORTS}")
     prims0 = (initial_state.copy() if initial_state is not None else initial_primitives(config, cloud))
     prims0.validate("initial state")
     devices = devices or [_lib.device_index()] * nranks
@@ -139,8 +148,15 @@ def solve_group(config: SolverConfig, cloud, conn: Connectivity, nranks: int, in
     handles = (C.c_void_p * nranks)(*[rp.dev.handle.value for rp in ranks])
     hist = np.zeros(config.n_outer)
     done, conv = C.c_int(0), C.c_int(0)
-    rc = _lib.lib().kmf_run_group(handles, nranks, C.byref(p), config.n_outer, _lib.dptr(hist), C.byref(done),
-                                  C.byref(conv))
+    if transport == "peer":
+        _lib.check(_lib.lib().kmf_peer_link(handles, nranks), "kmf_peer_link")
+        run = _lib.lib().kmf_run_linked
+    else:
+        run = _lib.lib().kmf_run_group
+    rc = run(handles, nranks, C.byref(p), config.n_outer, _lib.dptr(hist), C.byref(done), C.byref(conv))
+    if rc == _lib.KMF_EPEER:
+        raise _lib.DeviceError("peer transport timed out; counters (pushes, bands, iterations | data | read | "
+                               "limbs) per rank: " + "; ".join(str(peer_counters(rp)) for rp in ranks))
     if rc == _lib.KMF_EPOSITIVITY:
         # the reference raises at the earliest failing (iteration, stage)
         # over the whole cloud, and within a stage at its first raise site
@@ -154,7 +170,7 @@ def solve_group(config: SolverConfig, cloud, conn: Connectivity, nranks: int, in
         if dec and len(dec) == len(earliest):
             _raise_merged_decode(dec, cloud.n_points)
         _raise_rank_error(earliest[0][0], p)
-    _lib.check(rc, "kmf_run_group")
+    _lib.check(rc, f"solve_group ({transport})")
     n = cloud.n_points
     prims, U = np.empty((4, n)), np.empty((4, n))
     for rp in ranks:
@@ -162,6 +178,15 @@ def solve_group(config: SolverConfig, cloud, conn: Connectivity, nranks: int, in
         prims[:, gid] = pr
         U[:, gid] = u
     return hist[: done.value], prims, U, bool(conv.value)
+
+
+def peer_counters(rp: RankPart) -> list:
+    """kmf_peer_counters of one rank (diagnostics)."""
+    nr = rp.part.nranks
+    out = (C.c_uint64 * (3 + 3 * nr))()
+    _lib.check(_lib.lib().kmf_peer_counters(rp.dev.handle, out), "kmf_peer_counters")
+    v = list(out)
+    return [v[:3], v[3:3 + nr], v[3 + nr:3 + 2 * nr], v[3 + 2 * nr:]]
 
 
 def exchange_send_lists(part: LocalPart, dist) -> None:
@@ -177,16 +202,30 @@ def exchange_send_lists(part: LocalPart, dist) -> None:
                  if peer != part.rank and part.rank in r}
 
 
-class RankSolver:
-    """This process's rank of an NCCL-partitioned solve (torchrun, one GPU
-    per process).  `dist` is an initialised torch.distributed module."""
+RANK_TRANSPORTS = ("nccl", "peer")
 
-    def __init__(self, conn: Connectivity, dist, n_inner: int = 3, device: int | None = None, scheme: str = "bands"):
+
+class RankSolver:
+    """This process's rank of a partitioned solve (torchrun, one GPU per
+    process).  `dist` is an initialised torch.distributed module (plumbing:
+    ids, handles, lists, errors).  transport "nccl": halo send/recv and the
+    limb all-reduce by NCCL inside the iteration graph; "peer": the GPUs
+    push the halo into each other's memory from the update kernel and
+    all-gather the limbs over peer memory (CUDA IPC, csrc/kmf_peer.cuh)."""
+
+    def __init__(self, conn: Connectivity, dist, n_inner: int = 3, device: int | None = None, scheme: str = "bands",
+                 transport: str = "nccl"):
+        if transport not in RANK_TRANSPORTS:
+            raise ValueError(f"transport must be one of {RANK_TRANSPORTS}")
         self.rank, self.nranks = dist.get_rank(), dist.get_world_size()
         self.dist = dist
+        self.transport = transport
         part = build_part(conn, self.rank, self.nranks, n_inner + 2, scheme)
         exchange_send_lists(part, dist)
         self.rp = RankPart(conn, self.rank, self.nranks, n_inner, device, part=part)
+        if transport == "peer":
+            self._open_peers()
+            return
         uid = (C.c_char * 128)()
         if self.rank == 0:
             _lib.check(_lib.lib().kmf_nccl_get_unique_id(uid), "kmf_nccl_get_unique_id")
@@ -194,6 +233,25 @@ class RankSolver:
         dist.broadcast_object_list(box, src=0)
         uid = (C.c_char * 128).from_buffer_copy(box[0])
         _lib.check(_lib.lib().kmf_nccl_init(self.rp.dev.handle, uid, self.rank, self.nranks), "kmf_nccl_init")
+
+    def _open_peers(self) -> None:
+        """All-gather the ranks' IPC handles and receive lists, then map the
+        peers (kmf_peer_open): this rank pushes its send list to peer p into
+        the local slots of p's receive list for this rank."""
+        L, part = _lib.lib(), self.rp.part
+        h = (C.c_char * _lib.KMF_PEER_HANDLE_BYTES)()
+        _lib.check(L.kmf_peer_handle(self.rp.dev.handle, h), "kmf_peer_handle")
+        every = [None] * self.nranks
+        self.dist.all_gather_object(every, (bytes(h), {p: np.asarray(s, np.int64) for p, s in part.recv.items()}))
+        handles = (C.c_char * (_lib.KMF_PEER_HANDLE_BYTES * self.nranks)).from_buffer_copy(
+            b"".join(e[0] for e in every))
+        peers = sorted(set(part.send) | set(part.recv))  # attach_partition's peer order
+        dst = [every[p][1].get(self.rank, np.empty(0, np.int64)) if p in part.send else np.empty(0, np.int64)
+               for p in peers]
+        counts = np.array([d.size for d in dst], dtype=np.int64)
+        slots = np.ascontiguousarray(np.concatenate(dst) if dst else np.empty(0, np.int64), dtype=np.int64)
+        _lib.check(L.kmf_peer_open(self.rp.dev.handle, handles, _lib.i64ptr(counts), _lib.i64ptr(slots)),
+                   "kmf_peer_open")
 
     @property
     def dev(self) -> DeviceConnectivity:

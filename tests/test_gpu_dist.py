@@ -1,8 +1,9 @@
-"""Partitioned device solve (2 and 3 ranks on one GPU through the group
-runner, which runs the multi-process schedule: interior pass, halo
-exchange, band pass) reproduces the single-domain solve bit for bit, for
-both ownership schemes; the NCCL transport on one rank, and on two ranks
-when two GPUs are visible."""
+"""Partitioned device solve reproduces the single-domain solve bit for bit,
+for both ownership schemes and every transport: the one-process group
+runner with the host moving the halo ("host") or the contexts peer-linked
+("peer": update kernels push into each other's halo, device counters order
+the stages, limbs all-gathered over peer memory); multi-process NCCL and
+multi-process peer transport (CUDA IPC), several ranks sharing one GPU."""
 
 import numpy as np
 import pytest
@@ -14,42 +15,47 @@ from paper_2108_07031_b200.dist import solve_group
 pytestmark = pytest.mark.gpu
 
 
+@pytest.mark.parametrize("transport", ["host", "peer"])
 @pytest.mark.parametrize("scheme", ["bands", "sectors"])
 @pytest.mark.parametrize("nranks", [2, 3])
-def test_group_solve_bitwise(gpu, nranks, scheme, small_naca, small_naca_conn):
+def test_group_solve_bitwise(gpu, nranks, scheme, transport, small_naca, small_naca_conn):
     init = perturbed_state(small_naca)
     cfg = SolverConfig(mach=0.63, aoa_deg=2.0, n_outer=6)
     ref = solve(cfg, small_naca, small_naca_conn, initial_state=init, instrument=False)
-    hist, prims, U, conv = solve_group(cfg, small_naca, small_naca_conn, nranks, initial_state=init, scheme=scheme)
+    hist, prims, U, conv = solve_group(cfg, small_naca, small_naca_conn, nranks, initial_state=init, scheme=scheme,
+                                       transport=transport)
     assert np.array_equal(hist, ref.residue_history)
     assert np.array_equal(prims, ref.primitives.as_array())
     assert np.array_equal(U, ref.conserved)
 
 
-def test_group_solve_default_init_transonic(gpu, small_naca, small_naca_conn):
+@pytest.mark.parametrize("transport", ["host", "peer"])
+def test_group_solve_default_init_transonic(gpu, transport, small_naca, small_naca_conn):
     cfg = SolverConfig(mach=0.85, aoa_deg=1.0, n_outer=20)
     ref = solve(cfg, small_naca, small_naca_conn, instrument=False)
-    hist, prims, _, _ = solve_group(cfg, small_naca, small_naca_conn, 2)
+    hist, prims, _, _ = solve_group(cfg, small_naca, small_naca_conn, 2, transport=transport)
     assert np.array_equal(hist, ref.residue_history)
     assert np.array_equal(prims, ref.primitives.as_array())
 
 
-def test_group_solve_convergence_stop(gpu, small_naca, small_naca_conn):
+@pytest.mark.parametrize("transport", ["host", "peer"])
+def test_group_solve_convergence_stop(gpu, transport, small_naca, small_naca_conn):
     from paper_2108_07031_b200 import free_stream
 
     init = free_stream(0.63, 2.0, n=small_naca.n_points)
     cfg = SolverConfig(mach=0.63, aoa_deg=2.0, n_outer=30, convergence_tol=1e-6)
-    hist, _, _, conv = solve_group(cfg, small_naca, small_naca_conn, 2, initial_state=init)
+    hist, _, _, conv = solve_group(cfg, small_naca, small_naca_conn, 2, initial_state=init, transport=transport)
     assert conv and hist.shape == (1,)
 
 
-def test_group_solve_positivity(gpu, small_naca, small_naca_conn):
+@pytest.mark.parametrize("transport", ["host", "peer"])
+def test_group_solve_positivity(gpu, transport, small_naca, small_naca_conn):
     from paper_2108_07031_b200 import PositivityError
 
     init = perturbed_state(small_naca, amp=-0.64)
     cfg = SolverConfig(mach=0.63, aoa_deg=2.0, n_outer=5, cfl=1.0)
     with pytest.raises(PositivityError) as exc:
-        solve_group(cfg, small_naca, small_naca_conn, 2, initial_state=init)
+        solve_group(cfg, small_naca, small_naca_conn, 2, initial_state=init, transport=transport)
     assert str(exc.value).startswith("iteration 1: conserved_to_primitives: nonpositive density")
     assert list(exc.value.indices) == [880]
 
@@ -81,17 +87,55 @@ def test_nccl_rank_solver_world_one(gpu, small_naca, small_naca_conn, tmp_path):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("transport", ["host", "peer"])
 @pytest.mark.parametrize("mode", ["fused", "split4"])
-def test_group_solve_first_order_and_split4(gpu, mode, small_naca, small_naca_conn):
+def test_group_solve_first_order_and_split4(gpu, mode, transport, small_naca, small_naca_conn):
     """First-order scheme (no q-gradient kernels: the flux's own interior
     range) and split4 under the partition schedule."""
     init = perturbed_state(small_naca)
     for order in (1, 2):
         cfg = SolverConfig(mach=0.63, aoa_deg=2.0, n_outer=4, mode=mode, order=order)
         ref = solve(cfg, small_naca, small_naca_conn, initial_state=init, instrument=False)
-        hist, prims, _, _ = solve_group(cfg, small_naca, small_naca_conn, 3, initial_state=init, scheme="sectors")
+        hist, prims, _, _ = solve_group(cfg, small_naca, small_naca_conn, 3, initial_state=init, scheme="sectors",
+                                        transport=transport)
         assert np.array_equal(hist, ref.residue_history)
         assert np.array_equal(prims, ref.primitives.as_array())
+
+
+def test_peer_linked_continuation(gpu, small_naca, small_naca_conn):
+    """kmf_run_linked twice on the same peer-linked contexts (the second run
+    seeds by refreshing q and pushing the send points: the continued-run
+    protocol) equals one 7-iteration solve; the host-exchange group runner
+    refuses peer-linked contexts."""
+    import ctypes as C
+
+    from paper_2108_07031_b200 import _lib
+    from paper_2108_07031_b200.dist import RankPart
+    from paper_2108_07031_b200.solver import _params
+
+    init = perturbed_state(small_naca)
+    ranks = [RankPart(small_naca_conn, r, 3, n_inner=3, scheme="sectors") for r in range(3)]
+    for rp in ranks:
+        rp.set_state(init.as_array())
+    h = (C.c_void_p * 3)(*[rp.dev.handle.value for rp in ranks])
+    _lib.check(_lib.lib().kmf_peer_link(h, 3), "link")
+    assert _lib.lib().kmf_run_group(h, 3, C.byref(_params(SolverConfig(mach=0.63, n_outer=1))), 1, None, None,
+                                    None) == _lib.KMF_EINVAL  # peer-linked contexts run linked
+    ref = solve(SolverConfig(mach=0.63, aoa_deg=2.0, n_outer=7), small_naca, small_naca_conn, initial_state=init,
+                instrument=False)
+    got = []
+    for n in (3, 4):
+        cfg = SolverConfig(mach=0.63, aoa_deg=2.0, n_outer=n)
+        hist = np.zeros(n)
+        done, conv = C.c_int(0), C.c_int(0)
+        _lib.check(_lib.lib().kmf_run_linked(h, 3, C.byref(_params(cfg)), n, _lib.dptr(hist), C.byref(done),
+                                             C.byref(conv)), "linked")
+        assert done.value == n
+        got.extend(hist.tolist())
+    assert np.array_equal(np.array(got), ref.residue_history)
+    for rp in ranks:
+        gid, prims, _ = rp.owned_state()
+        assert np.array_equal(prims, ref.primitives.as_array()[:, gid])
 
 
 def test_group_rejects_shallow_halo(gpu, small_naca, small_naca_conn):
@@ -122,7 +166,7 @@ def test_group_rejects_shallow_halo(gpu, small_naca, small_naca_conn):
     assert np.array_equal(hist, ref.residue_history)
 
 
-def _nccl_worker(rank, world, port, scheme, order, q):
+def _rank_worker(rank, world, port, scheme, order, transport, q):
     import os
 
     import torch.distributed as dist
@@ -135,7 +179,7 @@ def _nccl_worker(rank, world, port, scheme, order, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     ndev = _lib.lib().kmf_device_count()
-    if ndev < world:
+    if ndev < world and transport == "nccl":
         # fewer GPUs than ranks: each rank reports its own host, so NCCL
         # skips its same-host duplicate-device check and connects the ranks
         # through its socket transport (loopback) -- the same NCCL calls,
@@ -149,7 +193,7 @@ def _nccl_worker(rank, world, port, scheme, order, q):
         conn = build_stencils(cloud)
         init = perturbed_state(cloud)
         cfg = Cfg(mach=0.63, aoa_deg=2.0, n_outer=6, order=order)
-        rs = RankSolver(conn, dist, n_inner=3, device=rank % ndev, scheme=scheme)
+        rs = RankSolver(conn, dist, n_inner=3, device=rank % ndev, scheme=scheme, transport=transport)
         hist, conv = rs.run(cfg, prims_array(init), cfg.n_outer)
         gid, prims, _ = rs.rp.owned_state()
         # the streamed-cases path on the same communicator: two cases from
@@ -168,12 +212,15 @@ def _nccl_worker(rank, world, port, scheme, order, q):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("transport", ["nccl", "peer"])
 @pytest.mark.parametrize("world,scheme,order", [(2, "sectors", 2), (3, "bands", 2), (4, "sectors", 1)])
-def test_nccl_ranks_bitwise(gpu, world, scheme, order, small_naca, small_naca_conn):
-    """N processes with the NCCL transport inside the iteration graph (halo
-    send/recv forked beside the interior pass, limb all-reduce before the
-    close): bitwise the single-domain solve.  With fewer GPUs than ranks the
-    ranks share a GPU over NCCL's socket transport (see _nccl_worker)."""
+def test_ranks_bitwise(gpu, world, scheme, order, transport, small_naca, small_naca_conn):
+    """N processes, the halo exchange and residue reduction inside the
+    iteration graph -- NCCL (send/recv forked beside the interior pass,
+    limb all-reduce) or the peer transport (CUDA IPC mappings of the peers'
+    q and flag blocks, halo pushed by the update kernel) -- bitwise the
+    single-domain solve.  With fewer GPUs than ranks the ranks share a GPU
+    (NCCL over its socket transport, see _rank_worker; IPC on one device)."""
     import socket
 
     import torch.multiprocessing as mp
@@ -186,7 +233,8 @@ def test_nccl_ranks_bitwise(gpu, world, scheme, order, small_naca, small_naca_co
     s_.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_nccl_worker, args=(r, world, port, scheme, order, q)) for r in range(world)]
+    procs = [ctx.Process(target=_rank_worker, args=(r, world, port, scheme, order, transport, q))
+             for r in range(world)]
     for p_ in procs:
         p_.start()
     try:

@@ -429,6 +429,59 @@ def roofline_fp64(counts, n_cloud, n_flux, launch_s, dfma_rate, probe_tflops):
     return out
 
 
+def rank_solver_checked(args, conn, cfg, init, dist, rank, local):
+    """The N-rank solver on args.transport, checked before it is timed: its
+    first `args.check_iters` residues must equal, bit for bit, a single-GPU
+    solve of the whole cloud on rank 0 (the partitioned arithmetic is the
+    single-GPU one).  A peer transport that fails the check (error, deadline
+    or mismatch on any rank) is replaced by NCCL, and the line says so."""
+    import dataclasses
+
+    from paper_2108_07031_b200 import _lib
+    from paper_2108_07031_b200._device import DeviceConnectivity
+    from paper_2108_07031_b200.dist import RankSolver
+    from paper_2108_07031_b200.solver import _params
+
+    k = max(args.check_iters, 0)
+    ref = None
+    if k and rank == 0:
+        t = time.perf_counter()
+        full = DeviceConnectivity(conn, device=local)
+        full.set_state(init.as_array())
+        ref, _, _ = full.run(_params(dataclasses.replace(cfg, n_outer=k)), k)
+        full.close()
+        print(f"[bench] single-GPU reference residues ({k} iterations) {time.perf_counter() - t:.1f} s",
+              file=sys.stderr, flush=True)
+    transport, fallback = args.transport, None
+    while True:
+        err, same = None, True
+        try:
+            rs = RankSolver(conn, dist, n_inner=cfg.n_inner, device=local, scheme=args.partition, transport=transport)
+            if k:
+                hist, _ = rs.run(dataclasses.replace(cfg, n_outer=k), init.as_array(), k)
+                same = rank != 0 or bool(np.array_equal(hist, ref))
+        except (_lib.DeviceError, ValueError) as e:
+            err, same, rs = str(e).splitlines()[0][:200], False, None
+        flags = [None] * dist.get_world_size()
+        dist.all_gather_object(flags, (same, err))
+        ok = all(f[0] for f in flags)
+        if ok or transport == "nccl":
+            if not ok:
+                raise SystemExit(f"bench: the {transport} transport failed its check: {flags}")
+            break
+        fallback = {"from": transport, "why": [f[1] or ("residues differ from the single-GPU solve" if not f[0]
+                                                        else None) for f in flags]}
+        print(f"[bench] {transport} transport failed its check, falling back to NCCL: {fallback}", file=sys.stderr,
+              flush=True)
+        transport, rs = "nccl", None
+        import gc
+
+        gc.collect()
+    info = {"name": transport, "fallback": fallback,
+            "check": {"iterations": k, "bitwise_vs_single_gpu": bool(k)} if k else None}
+    return rs, info
+
+
 def run_ours(args):
     ws, rank, local = dist_env()
     if ws > 1:
@@ -457,12 +510,12 @@ def run_ours(args):
 
     cloud, conn, cfg, init = setup(args.config, dist, rank)
     n = cloud.n_points
+    transport_info = None
     if ws > 1:
-        # geometric partition over the ranks, NCCL halo exchange + limb
-        # all-reduce inside the iteration graph (paper_2108_07031_b200/dist.py)
-        from paper_2108_07031_b200.dist import RankSolver
-
-        rs = RankSolver(conn, dist, n_inner=cfg.n_inner, device=local, scheme=args.partition)
+        # geometric partition over the ranks; the halo exchange and residue
+        # reduction inside the iteration graph over the chosen transport
+        # (paper_2108_07031_b200/dist.py), validated before timing
+        rs, transport_info = rank_solver_checked(args, conn, cfg, init, dist, rank, local)
         dev = rs.dev
         part = rs.rp.part
         print(f"[bench] rank {rank}: {part.n_owned} owned + {part.global_ids.size - part.n_owned} halo points "
@@ -607,8 +660,8 @@ def run_ours(args):
         "config": {"workload": CONFIGS[args.config][5], "config_key": args.config, "n_points": n,
                    "n_edges": int(conn.full.idx.size), "n_inner": cfg.n_inner, "order": cfg.order, "mode": cfg.mode,
                    "l2": "flushed between timed steps (256 MiB memset on the solver stream)",
-                   "parallelism": (f"partition x{ws} ({args.partition}, deep halo, NCCL halo exchange overlapped "
-                                   "with the interior pass)") if ws > 1 else "single GPU",
+                   "parallelism": (f"partition x{ws} ({args.partition}, deep halo, {transport_info['name']} halo "
+                                   "exchange overlapped with the interior pass)") if ws > 1 else "single GPU",
                    "point_order": args.order},
         "rdp_s_per_point_iter": 1.0 / value,
         "e2e": e2e,
@@ -630,8 +683,9 @@ def run_ours(args):
             kern_s[1] + kern_s[2]) / (step_ms[:K].sum() * 1e-3)) if n_sweeps else None,
         "clocks": clk.summary(),
         "partition": part_stats,
-        **({"shared_gpu": True, "note": "KMF_SHARE_GPU: ranks share GPUs over NCCL sockets; not scaling data"}
-           if shared_gpu else {}),
+        "transport": transport_info,
+        **({"shared_gpu": True, "note": "KMF_SHARE_GPU: ranks share GPUs (NCCL over sockets / IPC on one device); "
+                                        "not scaling data"} if shared_gpu else {}),
     }
     if not args.no_cpu_baseline and ws == 1:
         port = cpu_baseline(conn, cfg, init)
@@ -712,6 +766,11 @@ def main():
     ap.add_argument("--partition", choices=("sectors", "bands"), default="sectors",
                     help="ownership scheme of the multi-GPU partition (partition.py)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--transport", choices=("peer", "nccl"), default="peer",
+                    help="N > 1: halo / residue transport (peer: the update kernels push the halo into the peers' "
+                         "memory; nccl: NCCL send/recv + all-reduce); either inside the iteration graph")
+    ap.add_argument("--check-iters", type=int, default=2,
+                    help="N > 1: residues checked bitwise against a single-GPU solve before timing (0: skip)")
     ap.add_argument("--order", choices=("natural", "hilbert", "ringtile2", "ringtile4", "ringtile8"),
                     default=os.environ.get("KMF_ORDER", "natural"),
                     help="device point order (bitwise neutral, locality only)")

@@ -55,3 +55,26 @@ def test_bench_first_order_config(gpu):
     assert d["config"]["order"] == 1 and d["gpu_launches"] == 3 * 12 and d["roofline_qgrad"] is None
     assert "first order" in d["config"]["workload"]
 
+
+
+@pytest.mark.parametrize("transport", ["peer", "nccl"])
+def test_bench_two_ranks(gpu, transport):
+    """--gpus 2 self-launches two ranks (torchrun); with one visible GPU the
+    ranks share it (KMF_SHARE_GPU: IPC on one device / NCCL over sockets).
+    Before timing, the partitioned residues must equal a single-GPU solve
+    bit for bit; the line carries the transport and that check."""
+    import os
+
+    env = dict(os.environ, KMF_SHARE_GPU="1")
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--config", "c1", "--steps", "2",
+                          "--warmup", "3", "--no-cpu-baseline", "--transport", transport],
+                         capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
+    t = d["transport"]
+    assert t["name"] == transport and t["fallback"] is None and t["check"]["bitwise_vs_single_gpu"]
+    assert d["partition"]["scheme"] == "sectors" and len(d["partition"]["ranks"]) == 2
+    assert d.get("shared_gpu") is True

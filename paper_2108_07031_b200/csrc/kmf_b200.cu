@@ -2438,6 +2438,22 @@ extern "C" int kmf_peer_link(kmf_ctx **ctxs, int nctx)
         }
         byrank[c->rank] = c;
     }
+    // Ranks sharing a device share its hardware work queues (one per
+    // stream up to CUDA_DEVICE_MAX_CONNECTIONS, default 8); a rank spinning
+    // on its peers at the head of a queue another rank's stream maps to would
+    // block that rank for good.  Each rank runs two streams (solver, band
+    // pass): refuse what cannot be scheduled.
+    int conns = 8;
+    if (const char *e = std::getenv("CUDA_DEVICE_MAX_CONNECTIONS")) conns = std::max(1, std::atoi(e));
+    for (kmf_ctx *c : byrank) {
+        int same = 0;
+        for (kmf_ctx *o : byrank) same += o->device == c->device;
+        if (same > 1 && 2 * same > conns) {
+            set_msg("kmf_peer_link: %d ranks on device %d need CUDA_DEVICE_MAX_CONNECTIONS >= %d (set before CUDA "
+                    "initialises; it is %d)", same, c->device, 2 * same, conns);
+            return KMF_EINVAL;
+        }
+    }
     for (kmf_ctx *c : byrank) {
         CK(cudaSetDevice(c->device));
         if (int rc = peer_flags_alloc(c)) return rc;

@@ -11,6 +11,13 @@ from pathlib import Path
 import numpy as np
 import pytest
 
+# before CUDA initialises in this process: the peer-linked group tests run
+# up to 4 ranks concurrently on one device, each on two streams that spin on
+# each other (kmf_peer_link refuses fewer hardware queues than 2 per rank)
+import os  # noqa: E402
+
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = Path(__file__).resolve().parent.parent
 GOLDEN = ROOT / "tests" / "golden"
 if str(ROOT) not in sys.path:

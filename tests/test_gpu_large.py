@@ -115,17 +115,21 @@ def test_c3_fused_equals_split4_bitwise(gpu, c3):
     assert np.array_equal(a.primitives.as_array(), b.primitives.as_array())
 
 
-@pytest.mark.parametrize("scheme,nranks", [("bands", 2), ("sectors", 4)])
-def test_c3_partitioned_solve_bitwise(gpu, c3, scheme, nranks):
+@pytest.mark.parametrize("scheme,nranks,transport", [("bands", 2, "host"), ("sectors", 4, "host"),
+                                                     ("sectors", 4, "peer"), ("bands", 3, "peer")])
+def test_c3_partitioned_solve_bitwise(gpu, c3, scheme, nranks, transport):
     """Partitions of the 2.5M cloud (0.6-1.25M owned points each: the
     HBM-streaming kernel shapes on partitioned contexts, interior and band
-    passes) reproduce the single-domain history and state bit for bit."""
+    passes; the host-moved halo or the peer transport with the ranks
+    running concurrently) reproduce the single-domain history and state bit
+    for bit."""
     from paper_2108_07031_b200.dist import solve_group
 
     cloud, conn, cfg, init, _ = c3
     two = SolverConfig(mach=0.85, aoa_deg=1.0, n_outer=2)
     ref = solve(two, cloud, conn, initial_state=init, instrument=False)
-    hist, prims, U, _ = solve_group(two, cloud, conn, nranks, initial_state=init, scheme=scheme)
+    hist, prims, U, _ = solve_group(two, cloud, conn, nranks, initial_state=init, scheme=scheme,
+                                    transport=transport)
     assert np.array_equal(hist, ref.residue_history)
     assert np.array_equal(prims, ref.primitives.as_array())
 

@@ -279,7 +279,10 @@ int kmf_run_group(kmf_ctx **ctxs, int nctx, const kmf_params *p, int n_iter, dou
  * receive this rank's send list (its recv list for this rank).  kmf_run,
  * kmf_run_cases and kmf_bench_steps then run as for one domain.
  * One process: kmf_peer_link(ctxs) links the ranks' contexts directly and
- * kmf_run_linked enqueues every rank's run before awaiting any. */
+ * kmf_run_linked enqueues every rank's run before awaiting any (kmf_run,
+ * kmf_run_cases and kmf_bench_steps refuse such a context alone: its peers
+ * would never start).  Ranks sharing a device need
+ * CUDA_DEVICE_MAX_CONNECTIONS >= 2 per rank (kmf_peer_link checks). */
 #define KMF_PEER_HANDLE_BYTES 128
 int kmf_peer_handle(kmf_ctx *ctx, void *out);
 int kmf_peer_open(kmf_ctx *ctx, const void *handles, const int64_t *dst_counts, const int64_t *dst_slots);

@@ -200,6 +200,7 @@ struct kmf_ctx {
     // peer transport (kmf_peer.cuh): flag block in this device's memory, the
     // peers' q / flag blocks mapped here, the push map of the update
     bool peer_on = false;
+    bool peer_local = false;  // linked to contexts of this process: runs only through kmf_run_linked
     DBuf<PeerFlags> pflags;
     PeerSet pset{};
     PeerPush ppush{};
@@ -1222,9 +1223,15 @@ int kmf_set_state(kmf_ctx *c, const double *prims)
 
 namespace {
 
-int run_check(kmf_ctx *c, const kmf_params *p, int n_iter)
+int run_check(kmf_ctx *c, const kmf_params *p, int n_iter, bool linked = false)
 {
     if (!c || !p || n_iter < 0) return KMF_EINVAL;
+    if (c->peer_local && !linked) {
+        // its peers are contexts of this process: run alone, it would wait
+        // on ranks that never start
+        set_msg("this context is peer-linked in-process: run all ranks with kmf_run_linked");
+        return KMF_EINVAL;
+    }
     if (!c->have_state) {
         set_msg("kmf_run: no state (call kmf_set_state first)");
         return KMF_EINVAL;
@@ -1335,6 +1342,10 @@ int kmf_run_cases(kmf_ctx *c, const kmf_params *params, int n_iter, int n_cases,
     for (int k = 0; k < n_cases; k++) {
         if (!prims_in[k] || !prims_out[k]) return KMF_EINVAL;
         if (int rc = check_params(c, &params[k])) return rc;
+    }
+    if (c->peer_local) {
+        set_msg("kmf_run_cases: peer-linked in-process contexts run through kmf_run_linked");
+        return KMF_EINVAL;
     }
     if (c->dist_on && !c->transport()) {
         set_msg("kmf_run_cases: partitioned context without a transport");
@@ -1877,6 +1888,10 @@ int kmf_bench_steps(kmf_ctx *c, const kmf_params *p, int n_steps, int64_t flush_
     if (!c || !p || n_steps < 1 || !step_ms || !kernel_ms) return KMF_EINVAL;
     if (!c->have_state) {
         set_msg("kmf_bench_steps: no state");
+        return KMF_EINVAL;
+    }
+    if (c->peer_local || (c->dist_on && !c->transport())) {
+        set_msg("kmf_bench_steps: a partitioned context needs its own transport (NCCL or IPC peers)");
         return KMF_EINVAL;
     }
     if (int rc = check_params(c, p)) return rc;
@@ -2483,6 +2498,7 @@ extern "C" int kmf_peer_link(kmf_ctx **ctxs, int nctx)
         }
         CK(cudaSetDevice(c->device));
         if (int rc = peer_setup(c, q.data(), f.data(), dst)) return rc;
+        c->peer_local = true;
     }
     return KMF_OK;
 }
@@ -2498,7 +2514,7 @@ extern "C" int kmf_run_linked(kmf_ctx **ctxs, int nctx, const kmf_params *p, int
             set_msg("kmf_run_linked: contexts must be peer-linked ranks 0..n-1 (kmf_peer_link)");
             return KMF_EINVAL;
         }
-        if (int rc = run_check(c, p, n_iter)) return rc;
+        if (int rc = run_check(c, p, n_iter, true)) return rc;
         byrank[c->rank] = c;
     }
     if (iters_done) *iters_done = 0;

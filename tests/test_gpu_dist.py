@@ -119,8 +119,11 @@ def test_peer_linked_continuation(gpu, small_naca, small_naca_conn):
         rp.set_state(init.as_array())
     h = (C.c_void_p * 3)(*[rp.dev.handle.value for rp in ranks])
     _lib.check(_lib.lib().kmf_peer_link(h, 3), "link")
-    assert _lib.lib().kmf_run_group(h, 3, C.byref(_params(SolverConfig(mach=0.63, n_outer=1))), 1, None, None,
-                                    None) == _lib.KMF_EINVAL  # peer-linked contexts run linked
+    one = _params(SolverConfig(mach=0.63, n_outer=1))
+    assert _lib.lib().kmf_run_group(h, 3, C.byref(one), 1, None, None, None) == _lib.KMF_EINVAL
+    # ... and not alone either (its peers would never start): refused, not a 30 s deadline
+    d0, c0 = C.c_int(0), C.c_int(0)
+    assert _lib.lib().kmf_run(ranks[0].dev.handle, C.byref(one), 1, None, C.byref(d0), C.byref(c0)) == _lib.KMF_EINVAL
     ref = solve(SolverConfig(mach=0.63, aoa_deg=2.0, n_outer=7), small_naca, small_naca_conn, initial_state=init,
                 instrument=False)
     got = []

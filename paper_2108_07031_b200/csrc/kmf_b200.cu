@@ -18,7 +18,6 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
-#include <thread>
 #include <vector>
 
 
@@ -143,8 +142,6 @@ struct kmf_ctx {
     DBuf<double> x, y, pxy, dmin, fsum, fcoef, edx, edy;
     DBuf<unsigned char> flag;
     DBuf<int> eoff, deg, eidx;
-    DBuf<int> tw;                 // tile neighbour runs (k_sweep_tiles); empty: untiled kernels
-    DBuf<unsigned short> eloc;
     DBuf<long long> perm, cptr;
     long long n_edges = 0;
     // boundary
@@ -232,8 +229,6 @@ struct kmf_ctx {
         g.fsum = fsum.p;
         g.fcoef = fcoef.p;
         g.cptr = cptr.p;
-        g.tw = tw.p;
-        g.eloc = eloc.p;
         return g;
     }
     DB db() const
@@ -283,74 +278,6 @@ struct kmf_ctx {
 namespace {
 
 // ------------------------------------------------------------------ create
-
-// Neighbour runs of every 64-point tile for k_sweep_tiles: the tile's
-// distinct neighbour slots, merged into runs across gaps of <= 4 slots,
-// admitted densest first (neighbour hits per staged record) up to kTileW
-// runs / kTileCap records; eloc = the staged record of each ELL entry.
-void build_tiles(long long n, const std::vector<int> &off, const std::vector<int> &dg, const std::vector<int> &ei,
-                 std::vector<int> &tw, std::vector<unsigned short> &el)
-{
-    const long long ntile = (n + kTileP - 1) / kTileP;
-    const int W = 1 + 2 * kTileW;
-    tw.assign((size_t)ntile * W, 0);
-    el.assign(ei.size(), kNoLoc);
-    auto work = [&](long long t0, long long t1) {
-        std::vector<int> js;
-        struct Run {
-            int a, b, hits;
-        };
-        std::vector<Run> runs;
-        for (long long t = t0; t < t1; t++) {
-            js.clear();
-            const long long k1 = std::min(n, (t + 1) * kTileP);
-            for (long long k = t * kTileP; k < k1; k++)
-                for (int s = 0; s < dg[k]; s++) js.push_back(ei[off[k / 32] + (k % 32) + s * 32]);
-            std::sort(js.begin(), js.end());
-            runs.clear();
-            for (size_t e = 0; e < js.size(); e++) {
-                if (runs.empty() || js[e] - runs.back().b > 4)
-                    runs.push_back({js[e], js[e], 1});
-                else {
-                    runs.back().b = js[e];
-                    runs.back().hits++;
-                }
-            }
-            std::stable_sort(runs.begin(), runs.end(), [](const Run &x, const Run &y) {
-                return (double)x.hits / (x.b - x.a + 1) > (double)y.hits / (y.b - y.a + 1);
-            });
-            int *row = &tw[(size_t)t * W];
-            int cap = 0, nw = 0;
-            int at[kTileW], len[kTileW], base[kTileW];
-            for (const Run &r : runs) {
-                const int l = r.b - r.a + 1;
-                if (nw == kTileW || cap + l > kTileCap) continue;
-                at[nw] = r.a;
-                len[nw] = l;
-                base[nw] = cap;
-                row[1 + 2 * nw] = r.a;
-                row[2 + 2 * nw] = l;
-                cap += l;
-                nw++;
-            }
-            row[0] = nw;
-            for (long long k = t * kTileP; k < k1; k++)
-                for (int s = 0; s < dg[k]; s++) {
-                    const long long e = off[k / 32] + (k % 32) + s * 32;
-                    const int j = ei[e];
-                    for (int w = 0; w < nw; w++)
-                        if (j >= at[w] && j < at[w] + len[w]) {
-                            el[e] = (unsigned short)(base[w] + j - at[w]);
-                            break;
-                        }
-                }
-        }
-    };
-    const int nth = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
-    std::vector<std::thread> th;
-    for (int k = 0; k < nth; k++) th.emplace_back(work, ntile * k / nth, ntile * (k + 1) / nth);
-    for (auto &x : th) x.join();
-}
 
 int build_context(kmf_ctx *c, const kmf_geometry *g)
 {
@@ -522,13 +449,6 @@ int build_context(kmf_ctx *c, const kmf_geometry *g)
         CK(c->eoff.upload(off.data(), off.size()));
         CK(c->deg.upload(dg.data(), dg.size()));
         CK(c->eidx.upload(ei.data(), ei.size()));
-        if (xy && n > 100000) {
-            std::vector<int> tw;
-            std::vector<unsigned short> el;
-            build_tiles(n, off, dg, ei, tw, el);
-            CK(c->tw.upload(tw.data(), tw.size()));
-            CK(c->eloc.upload(el.data(), el.size()));
-        }
         CK(c->cptr.upload(cp.data(), cp.size()));
         if (!xy) {
             CK(c->edx.upload(ex.data(), ex.size()));
@@ -712,22 +632,6 @@ void launch_sw_t(kmf_ctx *c, cudaStream_t s, int lo, int hi, const double *Gin, 
 {
     if (hi <= lo) return;
     c->nlaunch++;
-    if (XY && NC == 4 && c->tw.p) {  // tile-staged neighbour records
-        static const bool carved = [] {
-            for (const void *f : {(const void *)k_sweep_tiles<true>, (const void *)k_sweep_tiles<false>})
-                cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-            return true;
-        }();
-        (void)carved;
-        const int nb = (hi - (lo & ~(kTileP - 1)) + kTileP - 1) / kTileP;
-        if (outp)
-            k_sweep_tiles<true><<<nb, kTileP, kTileSweepSmem, s>>>(c->dg(), lo, hi, (const double *)c->q.p, Gin, Gout,
-                                                                   ctl, stage, slot, want_res);
-        else
-            k_sweep_tiles<false><<<nb, kTileP, kTileSweepSmem, s>>>(c->dg(), lo, hi, (const double *)c->q.p, Gin,
-                                                                    Gout, ctl, stage, slot, want_res);
-        return;
-    }
     const int nb = nblk(hi - range_base(lo), qg_points_per_block<NC>());
     if (outp)
         k_sweep<XY, NC, true><<<nb, kTB, 0, s>>>(c->dg(), lo, hi, (const double *)c->q.p, Gin, Gout, ctl, stage, slot,

@@ -93,11 +93,6 @@ struct DG {
     const double *__restrict__ fsum;   // [4][ld] full-stencil sxx, sxy, syy, det
     const double *__restrict__ fcoef;  // [8][ld] (cx, cy) of x+, x-, y+, y-
     const long long *__restrict__ cptr;  // caller CSR ptr of the point in this slot (diag)
-    // neighbour windows of 64-point tiles (kmf_b200.cu build_tiles): per
-    // tile kTileW x (start, len) runs of slots staged in shared memory, and
-    // per ELL entry the staged record index (kNoLoc: not staged)
-    const int *__restrict__ tw;                 // [n_tiles][1 + 2 kTileW]
-    const unsigned short *__restrict__ eloc;    // ELL layout
 };
 
 // Boundary frames (wall entries first, then outer), geometry.py:573-646.
@@ -440,184 +435,6 @@ __global__ void __launch_bounds__(kTB, NC == 4 ? 8 : 0) k_first_order(DG g, int 
 // bitwise.  With want_res the max |new - old| (lsq.py:238-243) is reduced.
 // OUTP: the stage's last sweep writes the plane layout the flux and
 // boundary kernels read.
-// ---------------------------------------------------------------------------
-// Tile-staged q-gradient sweep (n > 100K, offsets from coordinates).  A
-// 64-point tile's neighbours are, in the ring point order, a few runs of
-// consecutive slots (its own ring and the adjacent rings, §2): one thread
-// issues a TMA bulk copy per run and field (x,y; q; the four (qx,qy)
-// planes) into shared memory at block start, while every thread loads its
-// owner data; the slot loop then reads its neighbour records from shared
-// memory (kTileCap records, conflict-free 128-bit reads) instead of
-// waiting on L1/L2 gathers.  Entries outside the staged runs (kNoLoc) are
-// gathered from global memory as before.  Values and summation order are
-// the untiled kernel's: bitwise the same gradients.
-constexpr int kTileP = 64;      // points per tile = threads per block
-constexpr int kTileW = 8;       // runs per tile
-constexpr int kTileCap = 288;   // staged records per tile
-constexpr int kTileEnt = 2048;  // staged ELL entries per tile (2 slices x 32 x 32 slots)
-constexpr unsigned short kNoLoc = 0xFFFF;
-constexpr size_t kTileSweepSmem = (size_t)kTileCap * 112 + kTileEnt * 2 + 16;
-
-KMF_HD void bulk_g2s(void *dst, const void *src, uint32_t bytes, unsigned long long *mbar)
-{
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(mbar))
-                 : "memory");
-}
-
-template <bool OUTP>
-__global__ void __launch_bounds__(kTileP, 6) k_sweep_tiles(DG g, int lo, int hi, const double *__restrict__ q,
-                                                           const double *__restrict__ Gin, double *__restrict__ Gout,
-                                                           Ctrl *c, int stage, int slot, int want_res)
-{
-    extern __shared__ __align__(128) unsigned char smem[];
-    double2 *sxy = reinterpret_cast<double2 *>(smem);
-    double2 *sq = sxy + kTileCap;           // [2][kTileCap]: (q0,q1), (q2,q3) -- staged as [kTileCap] Q4 first
-    double2 *sg = sq + 2 * kTileCap;        // [4][kTileCap] (qx_k, qy_k)
-    unsigned short *sloc = reinterpret_cast<unsigned short *>(sg + 4 * kTileCap);
-    unsigned long long *mbar = reinterpret_cast<unsigned long long *>(sloc + kTileEnt);
-    __shared__ int nrec;
-
-    const int tile = (lo >> 6) + blockIdx.x;
-    const int i0 = tile * kTileP, t = threadIdx.x;
-    const int ld = g.ld;
-    const int ns = (g.n + 31) >> 5;
-    const int s0 = 2 * tile, s1 = min(s0 + 2, ns);
-    const int e0 = g.eoff[s0], ent_n = g.eoff[s1] - e0;
-    const bool st_loc = ent_n <= kTileEnt;
-    if (t == 0) {
-        const int *tw = g.tw + (size_t)tile * (1 + 2 * kTileW);
-        const int nw = tw[0];
-        int off = 0;
-        for (int w = 0; w < nw; w++) off += tw[2 + 2 * w];
-        nrec = off;
-        const uint32_t bar = smem_u32(mbar);
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        const uint32_t bytes = (uint32_t)off * 112u + (st_loc ? (uint32_t)ent_n * 2u : 0u);
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-        off = 0;
-        const double2 *G2 = reinterpret_cast<const double2 *>(Gin);
-        for (int w = 0; w < nw; w++) {
-            const int a = tw[1 + 2 * w], len = tw[2 + 2 * w];
-            bulk_g2s(sxy + off, g.pxy + a, (uint32_t)len * 16u, mbar);
-            bulk_g2s(sq + 2 * off, q + 4 * (size_t)a, (uint32_t)len * 32u, mbar);
-#pragma unroll
-            for (int k = 0; k < 4; k++) bulk_g2s(sg + k * kTileCap + off, G2 + (size_t)k * ld + a, (uint32_t)len * 16u, mbar);
-            off += len;
-        }
-        if (st_loc && ent_n) bulk_g2s(sloc, g.eloc + e0, (uint32_t)ent_n * 2u, mbar);
-    }
-    __syncthreads();
-    // owner data while the copies fly
-    int i = i0 + t;
-    const bool valid = i >= lo && i < hi;
-    if (!valid) i = lo;
-    double qi[4], gxi[4], gyi[4], sx[4], sy[4];
-    qload_nc<4>(q, i, 0, qi);
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-        const double2 v = gload_cm(Gin, ld, k, i);
-        gxi[k] = v.x;
-        gyi[k] = v.y;
-        sx[k] = 0.0;
-        sy[k] = 0.0;
-    }
-    const double xi = g.x[i], yi = g.y[i];
-    const int base = ell_base(g, i), d = g.deg[i];
-    qg_stage_wait(true, mbar);
-    // q arrived as 32-byte records: split into the (q0,q1) / (q2,q3) planes
-    // in place (every record read before any is written)
-    {
-        const int R = nrec;
-        double2 tmp[2 * ((kTileCap + kTileP - 1) / kTileP)];
-#pragma unroll
-        for (int r = 0; r < (kTileCap + kTileP - 1) / kTileP; r++) {
-            const int rec = t + r * kTileP;
-            if (rec < R) {
-                tmp[2 * r] = sq[2 * rec];
-                tmp[2 * r + 1] = sq[2 * rec + 1];
-            }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int r = 0; r < (kTileCap + kTileP - 1) / kTileP; r++) {
-            const int rec = t + r * kTileP;
-            if (rec < R) {
-                sq[rec] = tmp[2 * r];
-                sq[kTileCap + rec] = tmp[2 * r + 1];
-            }
-        }
-        __syncthreads();
-    }
-    if (c && should_skip(c, stage, slot)) return;
-    double rmax = 0.0;
-    if (valid) {
-        using Slot = QgSlot<4, true>;
-        qg_slots<Slot, false>(
-            d,
-            [&](int s, Slot &o) {
-                const int ent = base + s * 32;
-                const unsigned loc = st_loc ? sloc[ent - e0] : g.eloc[ent];
-                if (loc != kNoLoc) {
-                    const double2 p = sxy[loc], qa = sq[loc], qb = sq[kTileCap + loc];
-                    o.x = p.x;
-                    o.y = p.y;
-                    o.q[0] = qa.x;
-                    o.q[1] = qa.y;
-                    o.q[2] = qb.x;
-                    o.q[3] = qb.y;
-#pragma unroll
-                    for (int k = 0; k < 4; k++) {
-                        const double2 v = sg[k * kTileCap + loc];
-                        o.gx[k] = v.x;
-                        o.gy[k] = v.y;
-                    }
-                } else {
-                    qg_gather<true, 4, true>(o, g, q, Gin, ld, 0, g.eidx[ent], ent);
-                }
-            },
-            [&](const Slot &o) {
-                const double dx = SUB(o.x, xi), dy = SUB(o.y, yi);
-                const double hdx = MUL(0.5, dx), hdy = MUL(0.5, dy);  // exact: see qtilde_h
-#pragma unroll
-                for (int k = 0; k < 4; k++) {
-                    const double dq = SUB(qtilde_h(o.q[k], o.gx[k], o.gy[k], hdx, hdy),
-                                          qtilde_h(qi[k], gxi[k], gyi[k], hdx, hdy));
-                    sx[k] = ADD(sx[k], MUL(dx, dq));
-                    sy[k] = ADD(sy[k], MUL(dy, dq));
-                }
-            });
-        const double sxx = g.fsum[i], sxy_ = g.fsum[ld + i], syy = g.fsum[2 * ld + i], det = g.fsum[3 * ld + i];
-        double gxn[4], gyn[4];
-#pragma unroll
-        for (int k = 0; k < 4; k++) {
-            gxn[k] = DIV(SUB(MUL(syy, sx[k]), MUL(sxy_, sy[k])), det);
-            gyn[k] = DIV(SUB(MUL(sxx, sy[k]), MUL(sxy_, sx[k])), det);
-        }
-        gstore_nc<4, OUTP>(Gout, ld, i, 0, gxn, gyn);
-        if (want_res) {
-            bool nan = false;
-#pragma unroll
-            for (int k = 0; k < 4; k++) {
-                const double ex = gxn[k] - gxi[k], ey = gyn[k] - gyi[k];
-                rmax = fmax(rmax, fmax(fabs(ex), fabs(ey)));
-                nan |= isnan(ex) || isnan(ey);
-            }
-            if (nan) rmax = __longlong_as_double(0x7ff8000000000000ll);  // np.max propagates NaN
-        }
-    }
-    if (want_res) {
-        unsigned long long b = (unsigned long long)__double_as_longlong(rmax);
-        for (int o = 16; o; o >>= 1) {
-            unsigned long long tb = __shfl_xor_sync(0xffffffffu, b, o);
-            b = tb > b ? tb : b;
-        }
-        if ((threadIdx.x & 31) == 0) atomicMax(&c->resmax, b);
-    }
-}
-
 template <bool XY, int NC, bool OUTP>
 __global__ void __launch_bounds__(kTB) k_sweep(DG g, int lo, int hi, const double *__restrict__ q,
                                                const double *__restrict__ Gin, double *__restrict__ Gout,

@@ -180,6 +180,26 @@ def solve_group(config: SolverConfig, cloud, conn: Connectivity, nranks: int, in
     return hist[: done.value], prims, U, bool(conv.value)
 
 
+def peer_push_targets(part: LocalPart, recv_of: list) -> tuple:
+    """Where this rank's halo pushes land (the kmf_peer_open lists): per
+    peer in attach_partition's order (sorted peers), the peer's local halo
+    slots for this rank's send list -- the peer's receive list for this
+    rank, whose order the send list follows (exchange_send_lists).
+    recv_of[p] is rank p's `recv` dict.  Returns (counts, slots) int64."""
+    peers = sorted(set(part.send) | set(part.recv))
+    dst = []
+    for p in peers:
+        d = np.asarray(recv_of[p].get(part.rank, np.empty(0)), dtype=np.int64) if p in part.send \
+            else np.empty(0, np.int64)
+        if d.size != (part.send[p].size if p in part.send else 0):
+            raise ValueError(f"rank {p} receives {d.size} points from rank {part.rank}, which sends "
+                             f"{part.send.get(p, np.empty(0)).size}")
+        dst.append(d)
+    counts = np.array([d.size for d in dst], dtype=np.int64)
+    slots = np.ascontiguousarray(np.concatenate(dst) if dst else np.empty(0, np.int64), dtype=np.int64)
+    return counts, slots
+
+
 def peer_counters(rp: RankPart) -> list:
     """kmf_peer_counters of one rank (diagnostics)."""
     nr = rp.part.nranks
@@ -245,11 +265,7 @@ class RankSolver:
         self.dist.all_gather_object(every, (bytes(h), {p: np.asarray(s, np.int64) for p, s in part.recv.items()}))
         handles = (C.c_char * (_lib.KMF_PEER_HANDLE_BYTES * self.nranks)).from_buffer_copy(
             b"".join(e[0] for e in every))
-        peers = sorted(set(part.send) | set(part.recv))  # attach_partition's peer order
-        dst = [every[p][1].get(self.rank, np.empty(0, np.int64)) if p in part.send else np.empty(0, np.int64)
-               for p in peers]
-        counts = np.array([d.size for d in dst], dtype=np.int64)
-        slots = np.ascontiguousarray(np.concatenate(dst) if dst else np.empty(0, np.int64), dtype=np.int64)
+        counts, slots = peer_push_targets(part, [e[1] for e in every])
         _lib.check(L.kmf_peer_open(self.rp.dev.handle, handles, _lib.i64ptr(counts), _lib.i64ptr(slots)),
                    "kmf_peer_open")
 

@@ -384,3 +384,33 @@ def test_oracle_n_act_equals_owned_flux_view(small_naca_conn, small_naca):
     # a sampled solve runs without touching the (garbage) halo fluxes
     hist, _, _, its, _ = O.solve(pk, init, fs_vec(0.63, 2.0), 2)
     assert its == 2 and np.all(np.isfinite(hist))
+
+
+@pytest.mark.parametrize("scheme", ["bands", "sectors"])
+def test_peer_push_targets_reproduce_the_exchange(small_naca_conn, scheme):
+    """The peer transport's push map (dist.peer_push_targets: each send
+    point's destination slot in the peer's halo) writes exactly what the
+    receive-side halo exchange writes, for 3 ranks of either ownership."""
+    from paper_2108_07031_b200.dist import peer_push_targets
+
+    parts = build_parts(small_naca_conn, 3, DEPTH, scheme)
+    rng = np.random.default_rng(7)
+    q = [rng.standard_normal((4, p.global_ids.size)) for p in parts]
+    want = [x.copy() for x in q]
+    for r, p in enumerate(parts):  # receive side: q[:, recv[peer]] = peer q[:, peer.send[r]]
+        for peer, slots in p.recv.items():
+            want[r][:, slots] = q[peer][:, parts[peer].send[r]]
+    got = [x.copy() for x in q]
+    recv_of = [p.recv for p in parts]
+    for r, p in enumerate(parts):  # push side, in attach_partition's peer order
+        counts, slots = peer_push_targets(p, recv_of)
+        off = 0
+        for peer, cnt in zip(sorted(set(p.send) | set(p.recv)), counts):
+            if cnt:
+                got[peer][:, slots[off:off + cnt]] = q[r][:, p.send[peer]]
+            off += cnt
+    for r in range(3):
+        assert np.array_equal(got[r], want[r])
+        # every halo slot is written by exactly one push
+        n_halo = parts[r].global_ids.size - parts[r].n_owned
+        assert sum(v.size for v in parts[r].recv.values()) == n_halo

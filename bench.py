@@ -479,6 +479,11 @@ def rank_solver_checked(args, conn, cfg, init, dist, rank, local):
         gc.collect()
     info = {"name": transport, "fallback": fallback,
             "check": {"iterations": k, "bitwise_vs_single_gpu": bool(k)} if k else None}
+    part = rs.rp.part
+    print(f"[bench] rank {rank}/{dist.get_world_size()} on cuda:{local}: {transport} transport, sends "
+          f"{ {p: int(v.size) for p, v in part.send.items()} } halo points to / receives "
+          f"{ {p: int(v.size) for p, v in part.recv.items()} } from its peers per stage; first {k} residues "
+          f"bitwise equal to the single-GPU solve", file=sys.stderr, flush=True)
     return rs, info
 
 

@@ -256,3 +256,70 @@ def test_ranks_bitwise(gpu, world, scheme, order, transport, small_naca, small_n
         assert np.array_equal(prims, prims_array(ref.primitives)[:, gid])
         seen[gid] += 1
     assert np.all(seen == 1)  # the owned sets partition the cloud
+
+
+def _deadline_worker(rank, world, port, q):
+    import os
+    import time as _t
+
+    import torch.distributed as dist
+
+    from paper_2108_07031_b200 import SolverConfig as Cfg
+    from paper_2108_07031_b200 import _lib, build_stencils, generate_naca_cloud
+    from paper_2108_07031_b200.dist import RankSolver
+    from paper_2108_07031_b200.state import prims_array
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ["KMF_PEER_TIMEOUT_S"] = "2"
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cloud = generate_naca_cloud(80, 30, 1.15, 20.0)
+        conn = build_stencils(cloud)
+        rs = RankSolver(conn, dist, n_inner=3, device=0, scheme="sectors", transport="peer")
+        res = None
+        if rank == 0:  # rank 1 never runs: rank 0 must come back with KMF_EPEER, not hang
+            t0 = _t.perf_counter()
+            try:
+                rs.run(Cfg(mach=0.63, aoa_deg=2.0, n_outer=2), prims_array(perturbed_state(cloud)), 2)
+                res = ("returned", _t.perf_counter() - t0)
+            except _lib.DeviceError as e:
+                res = (str(e), _t.perf_counter() - t0)
+        else:  # the collective RankSolver.run ends with (error flags), without running
+            flags = [None] * world
+            dist.all_gather_object(flags, (0, None))
+            res = ("idle", 0.0)
+        dist.barrier()
+        q.put((rank, res))
+    except Exception as exc:
+        q.put((rank, (repr(exc), -1.0)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_deadline_instead_of_hang(gpu):
+    """A rank whose peer never runs gets KMF_EPEER after the wait deadline
+    (2 s here) -- the GPU and the process come back instead of spinning."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    s_ = socket.socket()
+    s_.bind(("127.0.0.1", 0))
+    port = s_.getsockname()[1]
+    s_.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_deadline_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p_ in procs:
+        p_.start()
+    try:
+        out = dict(q.get(timeout=180) for _ in range(2))
+    finally:
+        for p_ in procs:
+            p_.join(timeout=60)
+            if p_.is_alive():
+                p_.kill()
+    msg, took = out[0]
+    assert "code 5" in msg and "did not arrive" in msg, msg
+    assert 1.5 < took < 60

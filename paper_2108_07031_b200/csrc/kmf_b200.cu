@@ -201,6 +201,7 @@ struct kmf_ctx {
     // peers' q / flag blocks mapped here, the push map of the update
     bool peer_on = false;
     bool peer_local = false;  // linked to contexts of this process: runs only through kmf_run_linked
+    bool peer_broken = false; // a peer wait timed out: the counters no longer agree across ranks
     DBuf<PeerFlags> pflags;
     PeerSet pset{};
     PeerPush ppush{};
@@ -1226,6 +1227,11 @@ namespace {
 int run_check(kmf_ctx *c, const kmf_params *p, int n_iter, bool linked = false)
 {
     if (!c || !p || n_iter < 0) return KMF_EINVAL;
+    if (c->peer_broken) {
+        set_msg("peer transport: this context saw a peer deadline (KMF_EPEER); its ranks' counters no longer "
+                "agree -- re-create the partition's contexts");
+        return KMF_EPEER;
+    }
     if (c->peer_local && !linked) {
         // its peers are contexts of this process: run alone, it would wait
         // on ranks that never start
@@ -1278,6 +1284,7 @@ int run_finish(kmf_ctx *c, int n_iter, double *history, int *iters_done, int *co
     if (iters_done) *iters_done = completed;
     if (converged) *converged = status == 2;
     if (fin.peer_fail) {
+        c->peer_broken = true;
         record_error(c, KMF_EPEER, fin.iter, 0, 0, 0, "peer transport: a peer rank did not arrive in time");
         set_msg("peer transport: a peer rank did not arrive in time (rank %d)", c->rank);
         return KMF_EPEER;
@@ -1347,6 +1354,10 @@ int kmf_run_cases(kmf_ctx *c, const kmf_params *params, int n_iter, int n_cases,
         set_msg("kmf_run_cases: peer-linked in-process contexts run through kmf_run_linked");
         return KMF_EINVAL;
     }
+    if (c->peer_broken) {
+        set_msg("kmf_run_cases: this context saw a peer deadline; re-create the partition's contexts");
+        return KMF_EPEER;
+    }
     if (c->dist_on && !c->transport()) {
         set_msg("kmf_run_cases: partitioned context without a transport");
         return KMF_EINVAL;
@@ -1410,6 +1421,7 @@ int kmf_run_cases(kmf_ctx *c, const kmf_params *params, int n_iter, int n_cases,
         if (iters_done) iters_done[k] = done;
         if (converged) converged[k] = st == 2;
         if (status) status[k] = f.peer_fail ? KMF_EPEER : st == 1 ? KMF_EPOSITIVITY : KMF_OK;
+        if (f.peer_fail) c->peer_broken = true;
         if (f.peer_fail && rc == KMF_OK) {
             set_msg("peer transport: a peer rank did not arrive in time (case %d)", k);
             rc = KMF_EPEER;
@@ -1894,6 +1906,10 @@ int kmf_bench_steps(kmf_ctx *c, const kmf_params *p, int n_steps, int64_t flush_
         set_msg("kmf_bench_steps: a partitioned context needs its own transport (NCCL or IPC peers)");
         return KMF_EINVAL;
     }
+    if (c->peer_broken) {
+        set_msg("kmf_bench_steps: this context saw a peer deadline; re-create the partition's contexts");
+        return KMF_EPEER;
+    }
     if (int rc = check_params(c, p)) return rc;
     CK(cudaSetDevice(c->device));
     if (int rc = seed_state(c, p->gamma, p->cfl)) return rc;
@@ -1928,6 +1944,11 @@ int kmf_bench_steps(kmf_ctx *c, const kmf_params *p, int n_steps, int64_t flush_
     Ctrl fin;
     CK(cudaMemcpy(&fin, c->ctrl.p, sizeof fin, cudaMemcpyDeviceToHost));
     if (launches_per_step) *launches_per_step = c->g1.launches;
+    if (fin.peer_fail) {
+        c->peer_broken = true;
+        set_msg("kmf_bench_steps: peer transport deadline (a peer rank did not arrive)");
+        return KMF_EPEER;
+    }
     if ((fin.state & 3ull) == 1ull) {
         set_msg("kmf_bench_steps: positivity failure at iteration %d", fin.err_iter);
         return KMF_EPOSITIVITY;
@@ -2538,7 +2559,20 @@ extern "C" int kmf_run_linked(kmf_ctx **ctxs, int nctx, const kmf_params *p, int
             if (int rc = get_graph(c, &q, 1, c->g1, ITER_PLAIN)) return rc;
     }
     for (kmf_ctx *c : byrank)
-        if (int rc = run_begin(c, &q, n_iter)) return rc;
+        if (int rc = run_begin(c, &q, n_iter)) {
+            // ranks already started spin on this one: release them, then wait
+            for (kmf_ctx *o : byrank) {
+                cudaSetDevice(o->device);
+                const unsigned long long one = 1ull;
+                cudaMemcpy(&o->pflags.p->failed, &one, sizeof one, cudaMemcpyHostToDevice);
+                o->peer_broken = true;
+            }
+            for (kmf_ctx *o : byrank) {
+                cudaSetDevice(o->device);
+                cudaDeviceSynchronize();
+            }
+            return rc;
+        }
     std::vector<int> rcs(nctx);
     for (int r = 0; r < nctx; r++) {
         int done = 0, conv = 0;

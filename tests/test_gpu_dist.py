@@ -285,9 +285,15 @@ def _deadline_worker(rank, world, port, q):
                 res = ("returned", _t.perf_counter() - t0)
             except _lib.DeviceError as e:
                 res = (str(e), _t.perf_counter() - t0)
+            # the context is now unusable (its ranks' counters disagree): refused at once
+            try:
+                rs.run(Cfg(mach=0.63, aoa_deg=2.0, n_outer=1), prims_array(perturbed_state(cloud)), 1)
+            except _lib.DeviceError as e:
+                res = res + ("re-create" in str(e),)
         else:  # the collective RankSolver.run ends with (error flags), without running
-            flags = [None] * world
-            dist.all_gather_object(flags, (0, None))
+            for _ in range(2):
+                flags = [None] * world
+                dist.all_gather_object(flags, (0, None))
             res = ("idle", 0.0)
         dist.barrier()
         q.put((rank, res))
@@ -320,6 +326,6 @@ def test_peer_deadline_instead_of_hang(gpu):
             p_.join(timeout=60)
             if p_.is_alive():
                 p_.kill()
-    msg, took = out[0]
+    msg, took, refused = out[0]
     assert "code 5" in msg and "did not arrive" in msg, msg
-    assert 1.5 < took < 60
+    assert 1.5 < took < 60 and refused

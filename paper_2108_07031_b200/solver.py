@@ -261,17 +261,42 @@ def solve(
     instrument: bool = True,
     timing_skip: int = 0,
     clock=time.perf_counter,
+    devices=None,
 ) -> SolveResult:
     """Run ``config.n_outer`` outer iterations on the GPU (solver.py:477-573).
 
     Raises PositivityError (prefixed "iteration {it}: ") exactly where the
     reference would.  With ``instrument`` the iterations after
     ``timing_skip`` are timed per stage with CUDA events and by ``clock``.
+
+    ``devices`` (extension; default: one GPU) -- a list of CUDA devices: the
+    cloud is partitioned into angular sectors, one per entry, and the ranks
+    run concurrently from this process over the peer transport
+    (dist.solve_group); history and state are bitwise the one-GPU solve's.
+    Per-stage seconds are not collected on that path (zeros); the wall time
+    covers the whole run.
     """
     if conn is None:
         conn = build_stencils(cloud)
     prims = initial_state.copy() if initial_state is not None else initial_primitives(config, cloud)
     prims.validate("initial state")
+    if devices is not None and len(devices) > 1:
+        from .dist import solve_group
+
+        t0 = clock()
+        hist, p_out, U, conv = solve_group(config, cloud, conn, len(devices), initial_state=prims,
+                                           devices=[int(d) for d in devices], scheme="sectors", transport="peer")
+        wall = clock() - t0
+        return SolveResult(
+            primitives=Primitives.from_array(p_out),
+            conserved=U,
+            residue_history=np.asarray(hist),
+            stage_seconds={name: 0.0 for name in STAGE_NAMES},
+            wall_seconds=wall if instrument else 0.0,
+            timed_iterations=len(hist),
+            iterations=len(hist),
+            converged=conv,
+        )
     dev = device_for(conn)
     dev.set_state(prims_array(prims))
 

@@ -329,3 +329,26 @@ def test_peer_deadline_instead_of_hang(gpu):
     msg, took, refused = out[0]
     assert "code 5" in msg and "did not arrive" in msg, msg
     assert 1.5 < took < 60 and refused
+
+
+def test_solve_on_several_devices(gpu, small_naca, small_naca_conn):
+    """solve(..., devices=[...]) partitions the cloud over the listed devices
+    (here the same GPU three times) and runs the ranks concurrently over the
+    peer transport: bitwise the one-GPU solve, PositivityError included."""
+    from paper_2108_07031_b200 import PositivityError
+
+    init = perturbed_state(small_naca)
+    cfg = SolverConfig(mach=0.63, aoa_deg=2.0, n_outer=10)
+    ref = solve(cfg, small_naca, small_naca_conn, initial_state=init, instrument=False)
+    got = solve(cfg, small_naca, small_naca_conn, initial_state=init, devices=[0, 0, 0])
+    assert np.array_equal(got.residue_history, ref.residue_history)
+    assert np.array_equal(got.primitives.as_array(), ref.primitives.as_array())
+    assert np.array_equal(got.conserved, ref.conserved)
+    assert got.iterations == 10 and got.wall_seconds > 0
+    bad = perturbed_state(small_naca, amp=-0.64)
+    cfg1 = SolverConfig(mach=0.63, aoa_deg=2.0, n_outer=5, cfl=1.0)
+    with pytest.raises(PositivityError) as e1:
+        solve(cfg1, small_naca, small_naca_conn, initial_state=bad, instrument=False)
+    with pytest.raises(PositivityError) as e2:
+        solve(cfg1, small_naca, small_naca_conn, initial_state=bad, devices=[0, 0])
+    assert str(e1.value) == str(e2.value) and list(e1.value.indices) == list(e2.value.indices)

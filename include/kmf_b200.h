@@ -14,7 +14,8 @@
  *   - four-vector fields use the reference layout (4, n) row-major
  *     (component c of point i at [c*n + i]), scalars (n,);
  *   - status codes: KMF_OK, KMF_EPOSITIVITY (reference PositivityError),
- *     KMF_EINVAL (reference ValueError), KMF_ECUDA, KMF_ENCCL;
+ *     KMF_EINVAL (reference ValueError), KMF_ECUDA, KMF_ENCCL, KMF_EPEER
+ *     (peer transport deadline);
  *   - a context is bound to one CUDA device and is not thread-safe; use one
  *     context per process/GPU.
  */

@@ -175,6 +175,11 @@ def setup(name, dist=None, rank=0):
     if rank == 0:
         import shutil
 
+        from paper_2108_07031_b200 import builder
+
+        # the other ranks wait: this one may use every core (torchrun sets
+        # OMP_NUM_THREADS=1 per rank, which made the 40M build take 318 s)
+        builder.lib().kmfb_set_threads(0)
         cloud, conn, cfg, init = build_config(name)
         need = 1.2 * (conn.full.idx.nbytes * 3 + conn.cloud.n_points * 8 * 40)  # idx, dx, dy + per-point arrays
         shm = Path("/dev/shm")

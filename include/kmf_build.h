@@ -16,6 +16,8 @@ extern "C" {
 
 /* OpenMP threads the builder uses. */
 int kmfb_threads(void);
+/* set them (n <= 0: every processor); returns the new count */
+int kmfb_set_threads(int n);
 
 /* Replaces geometry.py:315-346 _knn_neighbors: tie-inclusive k nearest
  * neighbours of points query[0..nq) (all points when query == NULL), self

@@ -46,6 +46,8 @@ def lib():
             raise RuntimeError(f"{LIB_PATH.name} is not built (make -C paper_2108_07031_b200/csrc)")
         L = C.CDLL(str(LIB_PATH))
         L.kmfb_threads.restype = C.c_int
+        L.kmfb_set_threads.restype = C.c_int
+        L.kmfb_set_threads.argtypes = [C.c_int]
         L.kmfb_knn.argtypes = [C.c_int64, _dp, _dp, C.c_int, C.c_int64, _i64p, _i64p, _i64p, _i64p]
         L.kmfb_visibility.argtypes = [C.c_int64, _dp, _dp, C.c_int64, _i64p, _dp, _dp, _dp, _dp, C.c_int64, _i64p,
                                       _i64p, _i64p, _u8p, _i64p]

@@ -230,6 +230,15 @@ extern "C" {
 
 int kmfb_threads(void) { return omp_get_max_threads(); }
 
+// set the OpenMP threads of the builder (n <= 0: every processor); returns
+// the new count.  torchrun sets OMP_NUM_THREADS=1 per rank, which would
+// leave the one rank that builds a shared connectivity on a single core.
+int kmfb_set_threads(int n)
+{
+    omp_set_num_threads(n > 0 ? n : omp_get_num_procs());
+    return omp_get_max_threads();
+}
+
 // geometry.py:315-346 tie-inclusive kNN rows (self excluded, ascending).
 // Pass 1 (rows == NULL): counts[r] for each query row.  Pass 2: rows
 // filled at offsets ptr[r] (caller's prefix sum of counts).

@@ -74,7 +74,7 @@ def test_builder_library_exports_every_symbol():
 
     text = re.sub(r"/\*.*?\*/", "", (ROOT / "include" / "kmf_build.h").read_text(), flags=re.S)
     names = sorted(set(re.findall(r"\b(kmfb_[a-z0-9_]+)\s*\(", text)))
-    assert names == ["kmfb_assemble", "kmfb_knn", "kmfb_radius", "kmfb_threads", "kmfb_visibility"]
+    assert names == ["kmfb_assemble", "kmfb_knn", "kmfb_radius", "kmfb_set_threads", "kmfb_threads", "kmfb_visibility"]
     so = ctypes.CDLL(str(builder.LIB_PATH))
     for name in names:
         assert hasattr(so, name), name

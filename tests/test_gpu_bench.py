@@ -78,3 +78,20 @@ def test_bench_two_ranks(gpu, transport):
     assert t["name"] == transport and t["fallback"] is None and t["check"]["bitwise_vs_single_gpu"]
     assert d["partition"]["scheme"] == "sectors" and len(d["partition"]["ranks"]) == 2
     assert d.get("shared_gpu") is True
+
+
+def test_bench_peer_fallback_to_nccl(gpu):
+    """A peer transport that fails its pre-timing check (here every peer
+    wait gets a 1 ns deadline, so the first wait fails with KMF_EPEER) is
+    replaced by NCCL on every rank, and the line records why."""
+    import os
+
+    env = dict(os.environ, KMF_SHARE_GPU="1", KMF_PEER_TIMEOUT_S="1e-9")
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--config", "c1", "--steps", "2",
+                          "--warmup", "3", "--no-cpu-baseline", "--transport", "peer"],
+                         capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    d = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][0])
+    t = d["transport"]
+    assert t["name"] == "nccl" and t["fallback"]["from"] == "peer" and t["check"]["bitwise_vs_single_gpu"]
+    assert any(w and "did not arrive" in w for w in t["fallback"]["why"]), t

@@ -126,7 +126,8 @@ def test_c3_partitioned_solve_bitwise(gpu, c3, scheme, nranks, transport):
     from paper_2108_07031_b200.dist import solve_group
 
     cloud, conn, cfg, init, _ = c3
-    two = SolverConfig(mach=0.85, aoa_deg=1.0, n_outer=2)
+    # the peer transport runs every rank concurrently: a longer horizon
+    two = SolverConfig(mach=0.85, aoa_deg=1.0, n_outer=10 if transport == "peer" else 2)
     ref = solve(two, cloud, conn, initial_state=init, instrument=False)
     hist, prims, U, _ = solve_group(two, cloud, conn, nranks, initial_state=init, scheme=scheme,
                                     transport=transport)
@@ -211,6 +212,26 @@ def c4():
     conn = build_stencils(cloud)
     cfg = SolverConfig(mach=0.63, aoa_deg=2.0, n_outer=3)
     return cloud, conn, cfg, initial_primitives(cfg, cloud)
+
+
+def test_c3_streamed_cases_bitwise(gpu, c3):
+    """kmf_run_cases at 2.5M points (the bench's e2e path at an
+    HBM-streaming size): three cases of 3 iterations from different states,
+    each bitwise its own solve."""
+    from paper_2108_07031_b200 import solve_cases
+
+    cloud, conn, cfg, init, _ = c3
+    three = SolverConfig(mach=0.85, aoa_deg=1.0, n_outer=3)
+    from conftest import perturbed_state
+
+    from paper_2108_07031_b200 import free_stream
+
+    inits = [init, perturbed_state(cloud, mach=0.85, aoa=1.0, amp=0.05), free_stream(0.85, 1.0, n=cloud.n_points)]
+    out = solve_cases(three, cloud, conn, inits)
+    for res, st in zip(out, inits):
+        ref = solve(three, cloud, conn, initial_state=st, instrument=False)
+        assert np.array_equal(res.residue_history, ref.residue_history)
+        assert np.array_equal(res.primitives.as_array(), ref.primitives.as_array())
 
 
 def test_c4_three_iterations_match_oracle(gpu, c4):

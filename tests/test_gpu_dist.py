@@ -352,3 +352,16 @@ def test_solve_on_several_devices(gpu, small_naca, small_naca_conn):
     with pytest.raises(PositivityError) as e2:
         solve(cfg1, small_naca, small_naca_conn, initial_state=bad, devices=[0, 0])
     assert str(e1.value) == str(e2.value) and list(e1.value.indices) == list(e2.value.indices)
+
+
+@pytest.mark.parametrize("gamma", [5.0 / 3.0, 1.3])
+def test_group_peer_other_gammas(gpu, gamma, small_naca, small_naca_conn):
+    """The gamma-specialised flux / boundary kernels (GK=2 at 5/3, the
+    generic GK=0 at 1.3) under the peer transport: bitwise one domain."""
+    init = perturbed_state(small_naca, gamma=gamma)
+    cfg = SolverConfig(mach=0.63, aoa_deg=2.0, n_outer=8, gamma=gamma)
+    ref = solve(cfg, small_naca, small_naca_conn, initial_state=init, instrument=False)
+    hist, prims, _, _ = solve_group(cfg, small_naca, small_naca_conn, 3, initial_state=init, scheme="sectors",
+                                    transport="peer")
+    assert np.array_equal(hist, ref.residue_history)
+    assert np.array_equal(prims, ref.primitives.as_array())

@@ -595,7 +595,7 @@ def run_ours(args):
         pin = (C.c_void_p * m)(*([host_in.ctypes.data] * m))
         pout = (C.c_void_p * m)(*[host_out[k % 2].ctypes.data for k in range(m)])
         hist_c = np.zeros(m)
-        _lib.check(L.kmf_run_cases(dev.handle, parr, 1, m, pin, pout, _lib.dptr(hist_c), None, None, None),
+        _lib.check(L.kmf_run_cases(dev.handle, parr, 1, m, pin, pout, None, _lib.dptr(hist_c), None, None, None),
                    "run_cases")
         return hist_c
 

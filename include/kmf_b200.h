@@ -157,15 +157,18 @@ int kmf_prepare(kmf_ctx *ctx, const kmf_params *p);
  * for bit, pipelined: case k+1's upload and case k-1's download run on the
  * copy engines while case k iterates (host buffers should be pinned,
  * kmf_host_alloc; they are read / written asynchronously until the call
- * returns).  The reference's harness runs such batches one solve at a time
+ * returns; conserved_out, or any of its entries, may be NULL: the final
+ * conserved state is then not downloaded).  The reference's harness runs such
+ * batches one solve at a time
  * (bench.py:174-215 sweep).  Outputs per case k: history[k*n_iter + i]
  * (0 past iters_done[k]), iters_done[k], converged[k], status[k]
  * (KMF_OK / KMF_EPOSITIVITY); any may be NULL.  Returns KMF_EPOSITIVITY if
  * a case failed (kmf_last_error: the first failing case), after running
  * every case.  The context keeps the last case's final state. */
 int kmf_run_cases(kmf_ctx *ctx, const kmf_params *params, int n_iter, int n_cases,
-                  const double *const *prims_in, double *const *prims_out, double *history,
-                  int *iters_done, int *converged, int *status);
+                  const double *const *prims_in, double *const *prims_out,
+                  double *const *conserved_out, double *history, int *iters_done, int *converged,
+                  int *status);
 /* final primitives and conserved (each (4,n)), either may be NULL */
 int kmf_get_state(kmf_ctx *ctx, double *prims, double *U);
 /* device seconds per STAGE_NAMES key (solver.py:53-60) accumulated by the

@@ -139,11 +139,12 @@ class DeviceConnectivity:
         _lib.check(rc, "kmf_run")
         return hist[: done.value].copy(), done.value, bool(conv.value)
 
-    def run_cases(self, params, states, n_iter: int, outs=None):
+    def run_cases(self, params, states, n_iter: int, outs=None, conserved: bool = False):
         """kmf_run_cases: one (params, initial (4, n) state) per case, uploads and
         downloads overlapped with the iterations (pinned buffers overlap; any
         array works).  Returns (finals, history (n_cases, n_iter), iters_done,
-        converged, status) -- status KMF_OK / KMF_EPOSITIVITY per case."""
+        converged, status[, conserved finals]) -- status KMF_OK /
+        KMF_EPOSITIVITY per case; the conserved finals with conserved=True."""
         m = len(states)
         if len(params) != m or m < 1:
             raise ValueError("one Params per case and at least one case")
@@ -156,14 +157,17 @@ class DeviceConnectivity:
         parr = (_lib.Params * m)(*params)
         pin = (C.c_void_p * m)(*[a.ctypes.data for a in ins])
         pout = (C.c_void_p * m)(*[a.ctypes.data for a in outs])
+        Us = [np.empty((4, self.n)) for _ in range(m)] if conserved else None
+        pU = (C.c_void_p * m)(*[a.ctypes.data for a in Us]) if conserved else None
         hist = np.zeros((m, n_iter))
         done = (C.c_int * m)()
         conv = (C.c_int * m)()
         st = (C.c_int * m)()
-        rc = _lib.lib().kmf_run_cases(self._h, parr, n_iter, m, pin, pout, _lib.dptr(hist), done, conv, st)
+        rc = _lib.lib().kmf_run_cases(self._h, parr, n_iter, m, pin, pout, pU, _lib.dptr(hist), done, conv, st)
         if rc != _lib.KMF_EPOSITIVITY:
             _lib.check(rc, "kmf_run_cases")
-        return outs, hist, list(done), [bool(v) for v in conv], list(st)
+        res = (outs, hist, list(done), [bool(v) for v in conv], list(st))
+        return res + (Us,) if conserved else res
 
     def prepare(self, params: _lib.Params):
         """Capture the iteration graphs a run with `params` replays (not timed)."""

@@ -99,8 +99,8 @@ def lib():
         "kmf_run": (C.c_int, [vp, C.POINTER(Params), C.c_int, _dp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
         "kmf_prepare": (C.c_int, [vp, C.POINTER(Params)]),
         "kmf_run_cases": (C.c_int, [vp, C.POINTER(Params), C.c_int, C.c_int, C.POINTER(C.c_void_p),
-                                    C.POINTER(C.c_void_p), _dp, C.POINTER(C.c_int), C.POINTER(C.c_int),
-                                    C.POINTER(C.c_int)]),
+                                    C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), _dp, C.POINTER(C.c_int),
+                                    C.POINTER(C.c_int), C.POINTER(C.c_int)]),
         "kmf_get_state": (C.c_int, [vp, _dp, _dp]),
         "kmf_stage_seconds": (C.c_int, [vp, _dp]),
         "kmf_last_error": (C.c_int, [vp, C.POINTER(ErrorInfo)]),

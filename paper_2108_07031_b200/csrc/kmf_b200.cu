@@ -1343,7 +1343,8 @@ __global__ void k_ctrl_copy(Ctrl *dst, const Ctrl *src)
 }
 
 int kmf_run_cases(kmf_ctx *c, const kmf_params *params, int n_iter, int n_cases, const double *const *prims_in,
-                  double *const *prims_out, double *history, int *iters_done, int *converged, int *status)
+                  double *const *prims_out, double *const *conserved_out, double *history, int *iters_done,
+                  int *converged, int *status)
 {
     if (!c || !params || n_iter < 1 || n_cases < 1 || !prims_in || !prims_out) return KMF_EINVAL;
     for (int k = 0; k < n_cases; k++) {
@@ -1387,6 +1388,7 @@ int kmf_run_cases(kmf_ctx *c, const kmf_params *params, int n_iter, int n_cases,
         const kmf_params *p = &params[k];
         const int b = k & 1;
         double *P = c->P0.p + b * n4, *S = c->stage_buf.p + b * n4;
+        double *SU = conserved_out && conserved_out[k] ? c->stage_buf2.p + b * n4 : nullptr;
         CK(cudaStreamWaitEvent(c->sh, c->cs_free[b], 0));
         CK(cudaMemcpyAsync(P, prims_in[k], bytes, cudaMemcpyHostToDevice, c->sh));
         CK(cudaEventRecord(c->cs_up[b], c->sh));
@@ -1398,11 +1400,12 @@ int kmf_run_cases(kmf_ctx *c, const kmf_params *params, int n_iter, int n_cases,
         if (int rc = replay(c, p, n_iter, ITER_PLAIN)) return rc;
         k_ctrl_copy<<<1, 32, 0, c->s0>>>(snap.p + k, c->ctrl.p);
         CK(cudaStreamWaitEvent(c->s0, c->cs_down[b], 0));
-        k_get_state<<<nblk(c->n), kTB, 0, c->s0>>>(g, c->Uo.p, perm, p->gamma, S, nullptr);
+        k_get_state<<<nblk(c->n), kTB, 0, c->s0>>>(g, c->Uo.p, perm, p->gamma, S, SU);
         CK(cudaGetLastError());
         CK(cudaEventRecord(c->cs_got[b], c->s0));
         CK(cudaStreamWaitEvent(c->sd, c->cs_got[b], 0));
         CK(cudaMemcpyAsync(prims_out[k], S, bytes, cudaMemcpyDeviceToHost, c->sd));
+        if (SU) CK(cudaMemcpyAsync(conserved_out[k], SU, bytes, cudaMemcpyDeviceToHost, c->sd));
         CK(cudaEventRecord(c->cs_down[b], c->sd));
     }
     CK(cudaDeviceSynchronize());

@@ -36,7 +36,6 @@ from .state import (
     Primitives,
     conserved_to_primitives,
     prims_array,
-    primitives_to_conserved,
     free_stream,
 )
 
@@ -358,8 +357,8 @@ def solve_cases(
     ``configs`` is a SolverConfig or one per case; ``initial_states`` a list of
     Primitives (default: ``initial_primitives`` of each config).  Case k gives
     ``solve(configs[k], cloud, conn, initial_states[k], instrument=False)``
-    bit for bit in residue history, final primitives and convergence
-    (``conserved`` is recomputed from the final primitives) -- but
+    bit for bit in residue history, final primitives, final conserved state
+    and convergence -- but
     case k+1's upload and case k-1's download overlap case k's iterations
     (kmf_run_cases), the batch the reference's harness runs one solve at a
     time (bench.py:174-215 ``sweep``).  A case that fails positivity is
@@ -383,7 +382,7 @@ def solve_cases(
         prims.validate("initial state")
         states.append(prims_array(prims))
     dev = device_for(conn)
-    outs, hist, done, conv, status = dev.run_cases([_params(c) for c in cfgs], states, n_iter)
+    outs, hist, done, conv, status, Us = dev.run_cases([_params(c) for c in cfgs], states, n_iter, conserved=True)
     results = []
     for k in range(m):
         if status[k] == _lib.KMF_EPOSITIVITY:
@@ -397,7 +396,7 @@ def solve_cases(
         prims = Primitives.from_array(outs[k])
         results.append(SolveResult(
             primitives=prims,
-            conserved=primitives_to_conserved(prims, cfgs[k].gamma),
+            conserved=Us[k],
             residue_history=hist[k, : done[k]].copy(),
             stage_seconds={name: 0.0 for name in STAGE_NAMES},
             wall_seconds=0.0,

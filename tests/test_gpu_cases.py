@@ -21,6 +21,7 @@ pytestmark = pytest.mark.gpu
 def _same(res, ref):
     assert np.array_equal(res.residue_history, ref.residue_history)
     assert np.array_equal(prims_array(res.primitives), prims_array(ref.primitives))
+    assert np.array_equal(res.conserved, ref.conserved)
     assert res.converged == ref.converged and res.iterations == ref.iterations
 
 

@@ -6,7 +6,7 @@
 // each rank maps its peers' q and PeerFlags (cudaIpcOpenMemHandle, or plain
 // pointers between contexts of one process).  Per RK stage:
 //
-//   band pass (stream s3)   k_peer_wait(DATA): every peer this rank
+//   band pass (stream s3)   k_peer_wait_data: every peer this rank
 //                           receives from has pushed the halo of the last
 //                           update (data[r] >= own pushes)
 //   after the band pass     k_peer_band_done: bands += 1, tell every peer
@@ -25,6 +25,12 @@
 //                           after the flags (an all-gather over peer memory;
 //                           integer sums, so every rank holds the same total)
 //                           -> k_close
+//
+// Each captured graph ends with k_peer_wait_data on the solver stream (no
+// run returns with a peer's push into this rank still in flight); a
+// continued run's seed waits for the peers to have read this rank's last
+// push (k_peer_wait_read), pushes the refreshed q (k_peer_push_all) and
+// publishes it (k_peer_pushed).
 //
 // The counters only grow and every rank runs the same sequence of stages,
 // so "peer r has done as many pushes / band passes as I have" is the whole

@@ -83,3 +83,43 @@ def test_builder_library_exports_every_symbol():
     for mod in ("builder", "store", "partition", "dist", "reorder", "integration"):
         src = (ROOT / "paper_2108_07031_b200" / f"{mod}.py").read_text()
         assert not re.search(r"^\s*(from|import)\s+oracle", src, flags=re.M), mod
+
+
+@pytest.mark.gpu
+def test_plain_c_host(gpu, tmp_path):
+    """tests/c/abi_smoke.c links libkmf_b200.so from C (no Python, no torch
+    types) and calls three context-free operators; its hex-printed results
+    equal the ctypes binding's bit for bit."""
+    import shutil
+    import subprocess
+
+    import numpy as np
+
+    if shutil.which("gcc") is None:
+        pytest.skip("no C compiler")
+    exe = tmp_path / "abi_smoke"
+    subprocess.run(["gcc", "-std=c11", "-O1", "-I", str(ROOT / "include"), str(ROOT / "tests" / "c" / "abi_smoke.c"),
+                    "-L", str(_lib.LIB_PATH.parent), "-lkmf_b200", "-Wl,-rpath," + str(_lib.LIB_PATH.parent),
+                    "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, (out.returncode, out.stderr)
+    got = {}
+    for line in out.stdout.split("\n"):
+        if line:
+            tag, v = line.split()
+            got.setdefault(tag, []).append(float.fromhex(v))
+    prims = np.array([1.0, 1.1, 0.9, 1.05, 0.97, 0.6, 0.62, 0.58, 0.0, -0.3,
+                      0.02, 0.0, -0.05, 0.1, 0.2, 0.714, 0.8, 0.69, 0.7, 0.75]).reshape(4, 5)
+    L = _lib.lib()
+    q = np.empty((4, 5))
+    fl = np.empty(5, np.uint8)
+    assert L.kmf_op_primitives_to_q(5, _lib.dptr(prims), 1.4, _lib.dptr(q), fl.ctypes.data_as(_lib._u8p)) == 0
+    G = np.empty((4, 5))
+    assert L.kmf_op_split_flux(5, _lib.dptr(prims), 0, 1, 1.4, _lib.dptr(G)) == 0
+    U1 = prims.copy()
+    U1.flat[2] += 1e-3
+    res = np.zeros(1)
+    assert L.kmf_op_residue(5, _lib.dptr(U1), _lib.dptr(prims), _lib.dptr(res)) == 0
+    assert np.array_equal(np.array(got["q"]), q.ravel())
+    assert np.array_equal(np.array(got["G"]), G.ravel())
+    assert got["res"][0] == res[0]

@@ -172,7 +172,7 @@ def test_model_catches_a_broken_protocol(drop):
     a row before a slow rank summed it -- on 16 ranks in bands: an
     iteration's four stages chain the ranks 8 hops apart (band waits on the
     neighbours' previous update, update on their band pass), so up to ~9
-    ranks the halo waits alone would keep a single row safe.
+    ranks the halo waits alone would keep a single row safe."""
     global step_ready
     keep, keep_step = step_ready, globals()["step"]
 
